@@ -1,0 +1,139 @@
+/*
+ * hexfuse_b200.h -- C ABI of the B200-native fused flux + divergence library
+ * (libhexfuse_b200.so).  Plain C types only: pointers, sizes, a POD problem
+ * descriptor.  No torch, no C++ types cross this boundary.
+ *
+ * The boundary this replaces (reference = /root/reference/proj/include/hexfuse):
+ *
+ *   (b3) the rendered device kernel
+ *          extern "C" __global__ void <name>(int n_elements, const REAL* u, REAL* divf)
+ *        render.hpp:79-80, launched on n_blocks() x block_threads (layout.hpp:87-90)
+ *        -> hf_fused_divergence(): same operands (caller-owned device arrays in
+ *           StateField AoSoA order, n_groups*group_words REAL each), but p, d,
+ *           group, nu/zeta/T/jac and the D table are runtime arguments instead
+ *           of generation-time immediates, and the launch shape is the library's.
+ *   (b2) generate_kernel(KernelRequest) + execute(ir, field, grid)
+ *        presets.hpp:144-161, simulator.hpp:184-192
+ *        -> hf_fused_divergence() with hf_problem.method (auto / planar / lines)
+ *   (b1) StateField oracle_divergence(const StateField&, const PhysParams&,
+ *                                     const std::array<double,3>& jac, bool with_source)
+ *        oracle.hpp:20-21
+ *        -> hf_fused_divergence_host() (host buffers in, host buffers out);
+ *           include/hexfuse_b200.hpp wraps it with exactly that C++ signature.
+ *
+ * Error model (mirrors the reference's exception classes and CLI exit codes,
+ * cli.hpp:360-368):  HF_EINVAL  <=> std::invalid_argument (exit 2)
+ *                    HF_ERUNTIME <=> std::runtime_error / CUDA error (exit 1)
+ * The message of the last failure on the calling thread is hf_last_error().
+ *
+ * Threading: every entry point is reentrant; the operator table travels in the
+ * kernel's __grid_constant__ parameters, so there is no per-device state on
+ * the launch path and no allocation in hf_fused_divergence().
+ */
+#ifndef HEXFUSE_B200_H
+#define HEXFUSE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HF_API __attribute__((visibility("default")))
+#else
+#define HF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HF_OK 0
+#define HF_ERUNTIME 1 /* runtime_error: CUDA failure, missing device        */
+#define HF_EINVAL 2   /* invalid_argument: bad p/d/params/group/method combo */
+
+#define HF_FP32 0 /* Precision::fp32 (core.hpp:10), 4-byte words */
+#define HF_FP64 1 /* Precision::fp64, 8-byte words                */
+
+#define HF_METHOD_AUTO 0    /* measured selection table (replaces preset_table, presets.hpp:25-37) */
+#define HF_METHOD_PLANAR 1  /* Alg. 1, thread per (element, z-plane)  (codegen_planar.hpp:251-273) */
+#define HF_METHOD_LINES 2   /* higher-parallelism, thread per line     (codegen_lines.hpp:299-318)  */
+#define HF_METHOD_UNFUSED 3 /* stage 2 + stage 3 (+ stage 6) kernels  (io_model.hpp:32-34)         */
+
+/* One fused-divergence problem.  Field layout is StateField's
+ * (layout.hpp:104-134): word (e,i,j,k,v) at
+ *   (e/group)*group_words + e%group + group*(i + m j + m^2 k + m^d v),
+ *   group_words = group * m^d * n_v, m = p+1, n_v = 1+d+d^2,
+ * padded to ceil(n_elem/group) groups; padding elements are never read or written. */
+typedef struct hf_problem {
+    int d;            /* 2 or 3                                       */
+    int p;            /* order: 1..7 (d=3), 1..8 (d=2)                */
+    int64_t n_elem;   /* real elements                                */
+    int group;        /* AoSoA group size (StateField::group), >= 1   */
+    int precision;    /* HF_FP32 | HF_FP64                            */
+    double nu, zeta, T; /* PhysParams (equations.hpp:14-24)           */
+    double jac[3];    /* constant per-axis metric, jac[2] unused for d=2 */
+    int with_source;  /* fuse stage 6 (-g/T on the gradient rows)     */
+    int method;       /* HF_METHOD_*                                  */
+} hf_problem;
+
+/* Static description of the kernel a problem would launch. */
+typedef struct hf_kernel_info {
+    int method;          /* resolved HF_METHOD_* (never AUTO)            */
+    int elems_per_cta;   /* elements one CTA owns (the preferred group)  */
+    int block_threads;
+    int shared_bytes;    /* dynamic shared memory per CTA                */
+    int registers;       /* per thread, from cudaFuncGetAttributes (0 if no device) */
+    int64_t grid;        /* CTAs for this problem                        */
+    int bulk_path;       /* 1 if full chunks stage through cp.async.bulk */
+    char name[96];
+} hf_kernel_info;
+
+/* ---- layout helpers (pure host functions, no device needed) ---- */
+HF_API int hf_n_vars(int d);                                   /* equations.hpp:27-30 */
+HF_API int64_t hf_field_words(const hf_problem* pr);           /* layout.hpp:115,125  */
+HF_API int64_t hf_offset(const hf_problem* pr, int64_t e, int i, int j, int k, int v); /* layout.hpp:128-134 */
+HF_API int hf_validate(const hf_problem* pr);                  /* HF_OK or HF_EINVAL  */
+/* D on the Gauss-Legendre nodes of order m = p+1, row-major (operators.hpp:17-74); m in [2,9] */
+HF_API int hf_derivative_matrix(int m, double* D_out, double* nodes_out);
+/* Algorithmic (io_model Fused23) bytes per solution point: 2 * n_v * word bytes. */
+HF_API int64_t hf_algorithmic_bytes_per_point(const hf_problem* pr);
+
+/* ---- selection (replaces preset_table / default_lines_n, presets.hpp:25-103) ---- */
+HF_API int hf_selected_method(const hf_problem* pr);    /* resolves HF_METHOD_AUTO */
+HF_API int hf_preferred_group(const hf_problem* pr);    /* group that enables the bulk-copy path */
+HF_API int hf_kernel_info_get(const hf_problem* pr, hf_kernel_info* out);
+
+/* ---- device-buffer entry points (the (b3)/(b2) replacement) ----
+ * u_dev, divf_dev: device pointers, hf_field_words(pr) words of the problem's
+ * precision each, distinct.  stream: a cudaStream_t (NULL = legacy default).
+ * Asynchronous: returns after enqueueing; errors from the launch are reported. */
+HF_API int hf_fused_divergence(const hf_problem* pr, const void* u_dev, void* divf_dev, void* stream);
+
+HF_API size_t hf_unfused_workspace_bytes(const hf_problem* pr); /* d*n_v words per padded point */
+HF_API int hf_unfused_divergence(const hf_problem* pr, const void* u_dev, void* divf_dev, void* ws_dev, void* stream);
+
+/* ---- host-buffer entry point (the (b1) replacement) ----
+ * u_host / divf_host: host arrays of hf_field_words(pr) words of the problem's
+ * precision (float for HF_FP32, double for HF_FP64).  Pinned memory is used
+ * directly; pageable memory is staged.  The field is streamed through the GPU
+ * in group-aligned slices with host->device copy, kernel and device->host copy
+ * overlapped on three streams.  Synchronous: returns when divf_host is filled. */
+typedef struct hf_context hf_context;
+HF_API hf_context* hf_context_create(int device);
+HF_API void hf_context_destroy(hf_context* ctx);
+HF_API int hf_fused_divergence_host(hf_context* ctx, const hf_problem* pr, const void* u_host, void* divf_host);
+
+/* ---- multi-GPU partition (element-parallel, no collective) ----
+ * Part `part` of `n_parts` contiguous, group-aligned slices: elements
+ * [*e_begin, *e_begin + *n_elem_part), starting at word *word_offset of the
+ * field.  The slice is itself a valid field with the same group. */
+HF_API int hf_partition(const hf_problem* pr, int n_parts, int part, int64_t* e_begin, int64_t* n_elem_part,
+                 int64_t* word_offset);
+
+HF_API const char* hf_last_error(void);
+HF_API const char* hf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HEXFUSE_B200_H */

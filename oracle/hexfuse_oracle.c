@@ -1,0 +1,402 @@
+/*
+ * hexfuse_oracle.c -- CPU restatement of the reference hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This file is the parity checker for the B200
+ * kernels in paper_2107_14027_b200/csrc.  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline leg may load it.  It is never the product path:
+ * the shipped library (libhexfuse_b200.so) does not link it and has no CPU
+ * fallback.
+ *
+ * Parity status: PINNED.  Every function here is checked bit-for-bit against
+ * the reference itself, compiled from /root/reference/proj/include by
+ * oracle/Makefile into oracle/_ref/libhexfuse_ref.so (tests/test_oracle_vs_ref.py),
+ * and against the golden vectors in tests/golden/ that the same reference
+ * library produced (tests/golden/make_golden.py).  The one exception is m = 9
+ * (d = 2, p = 8), which the reference rejects (operators.hpp:18); that row is
+ * "parity unpinned by reference" and is labelled so in DESIGN.md.
+ *
+ * Build: plain C99, -O2 -ffp-contract=off (no FMA contraction), so that the
+ * arithmetic order below reproduces the reference's double results exactly.
+ *
+ * Each function cites the reference file:line it restates (paths relative to
+ * /root/reference/proj/include/hexfuse/).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+
+#define HFO_EXPORT __attribute__((visibility("default")))
+
+/* equations.hpp:27-30 */
+HFO_EXPORT int hfo_n_vars(int d) { return (d == 2 || d == 3) ? 1 + d + d * d : -1; }
+
+/* equations.hpp:34-36 : P, V_b, then gradient rows g(b,a) = 1 + d + b*d + a */
+static inline int var_gradient(int d, int b, int a) { return 1 + d + b * d + a; }
+
+/* operators.hpp:17-45.  Newton iteration from Chebyshev guesses, then exact
+ * symmetrisation.  The reference accepts m in [2,8]; this restatement runs the
+ * same algorithm up to m = 9 for the d = 2, p = 8 configuration (unpinned). */
+HFO_EXPORT int hfo_gauss_legendre_points(int m, double *x) {
+    if (m < 2 || m > 9) return -1;
+    for (int i = 0; i < m; ++i) {
+        double z = cos(M_PI * (i + 0.75) / (m + 0.5));
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = 0.0;
+            for (int j = 0; j < m; ++j) {
+                const double p2 = p1;
+                p1 = p0;
+                p0 = ((2.0 * j + 1.0) * z * p1 - j * p2) / (j + 1.0);
+            }
+            const double dp = m * (z * p0 - p1) / (z * z - 1.0);
+            const double z1 = z;
+            z = z1 - p0 / dp;
+            if (fabs(z - z1) < 1e-15) break;
+        }
+        x[m - 1 - i] = z;
+    }
+    for (int i = 0; i < m / 2; ++i) {
+        const double v = 0.5 * (x[m - 1 - i] - x[i]);
+        x[i] = -v;
+        x[m - 1 - i] = v;
+    }
+    if (m % 2 == 1) x[m / 2] = 0.0;
+    return 0;
+}
+
+/* operators.hpp:49-74.  D(j,k) = l_k'(x_j) by barycentric weights; the
+ * diagonal is minus the off-diagonal row sum.  D is row-major m x m. */
+HFO_EXPORT int hfo_derivative_matrix(int m, const double *nodes, double *D) {
+    double wb[16];
+    if (m < 1 || m > 16) return -1;
+    for (int i = 0; i < m; ++i)
+        for (int j = i + 1; j < m; ++j)
+            if (nodes[i] == nodes[j]) return -1;
+    for (int k = 0; k < m; ++k) {
+        wb[k] = 1.0;
+        for (int j = 0; j < m; ++j)
+            if (j != k) wb[k] /= (nodes[k] - nodes[j]);
+    }
+    for (int j = 0; j < m; ++j) {
+        double diag = 0.0;
+        for (int k = 0; k < m; ++k) {
+            if (k == j) continue;
+            const double v = (wb[k] / wb[j]) / (nodes[j] - nodes[k]);
+            D[j * m + k] = v;
+            diag -= v;
+        }
+        D[j * m + j] = diag;
+    }
+    return 0;
+}
+
+/* Convenience: D on the Gauss-Legendre nodes of order m. */
+HFO_EXPORT int hfo_gl_derivative_matrix(int m, double *D) {
+    double x[16];
+    if (hfo_gauss_legendre_points(m, x) != 0) return -1;
+    return hfo_derivative_matrix(m, x, D);
+}
+
+/* equations.hpp:70-83.  f[a*nv + row]; column a: zeta*V_a on P,
+ * V_b*V_a - nu*g(b,a) (+P if a==b) on momentum b, -V_b/T on g(b,a). */
+HFO_EXPORT void hfo_flux(int d, const double *s, double nu, double zeta, double T, double *f) {
+    const int nv = 1 + d + d * d;
+    memset(f, 0, sizeof(double) * (size_t)(d * nv));
+    for (int a = 0; a < d; ++a) {
+        f[a * nv + 0] = zeta * s[1 + a];
+        for (int b = 0; b < d; ++b) {
+            double mom = s[1 + b] * s[1 + a] - nu * s[var_gradient(d, b, a)];
+            if (a == b) mom += s[0];
+            f[a * nv + 1 + b] = mom;
+            f[a * nv + var_gradient(d, b, a)] = -s[1 + b] / T;
+        }
+    }
+}
+
+/* equations.hpp:87-94 */
+HFO_EXPORT void hfo_source(int d, const double *s, double T, double *out) {
+    const int nv = 1 + d + d * d;
+    for (int v = 0; v < nv; ++v) out[v] = 0.0;
+    for (int b = 0; b < d; ++b)
+        for (int a = 0; a < d; ++a) out[var_gradient(d, b, a)] = -s[var_gradient(d, b, a)] / T;
+}
+
+/* equations.hpp:97-103 */
+HFO_EXPORT int hfo_flux_structural_nonzero(int d, int a, int row) {
+    if (row == 0) return 1;
+    if (row >= 1 && row <= d) return 1;
+    for (int b = 0; b < d; ++b)
+        if (row == var_gradient(d, b, a)) return 1;
+    return 0;
+}
+
+/* layout.hpp:121-134.  AoSoA word offset of (e, i, j, k, v). */
+static inline int64_t field_offset(int d, int m, int group, int e, int i, int j, int k, int v) {
+    const int64_t np = (d == 3) ? (int64_t)m * m * m : (int64_t)m * m;
+    const int64_t nv = 1 + d + d * d;
+    const int64_t gw = (int64_t)group * np * nv;
+    const int64_t pt = i + (int64_t)m * j + (int64_t)m * m * k;
+    return (int64_t)(e / group) * gw + (e % group) + (int64_t)group * (pt + np * v);
+}
+
+HFO_EXPORT int64_t hfo_offset(int d, int p, int group, int e, int i, int j, int k, int v) {
+    return field_offset(d, p + 1, group, e, i, j, k, v);
+}
+
+/* layout.hpp:121-125: padded word count of a field */
+HFO_EXPORT int64_t hfo_field_words(int d, int p, int n_elem, int group) {
+    const int m = p + 1;
+    const int64_t np = (d == 3) ? (int64_t)m * m * m : (int64_t)m * m;
+    const int64_t ng = (n_elem + group - 1) / group;
+    return ng * group * np * (1 + d + d * d);
+}
+
+/* oracle.hpp:20-62.  The reference fused result, all in double.  The loop
+ * nest (e, k, j, i, axis, t, v) and the summation order are the reference's.
+ * Elements [e_begin, e_end) are computed; out must be pre-zeroed by the caller
+ * for padding (the reference returns a zeroed copy of U). */
+HFO_EXPORT int hfo_oracle_divergence_range(int d, int p, int group, const double *U, double *out,
+                                           double nu, double zeta, double T, const double *jac,
+                                           int with_source, int e_begin, int e_end) {
+    if (d != 2 && d != 3) return -1;
+    if (nu < 0.0 || zeta <= 0.0 || T <= 0.0) return -1; /* equations.hpp:19-23 */
+    const int m = p + 1, nv = 1 + d + d * d;
+    double D[16 * 16];
+    if (hfo_gl_derivative_matrix(m, D) != 0) return -1;
+    double line[16][3 * 13];
+    double st[13], acc[13], src[13];
+    const int mk = (d == 3) ? m : 1;
+    for (int e = e_begin; e < e_end; ++e)
+        for (int k = 0; k < mk; ++k)
+            for (int j = 0; j < m; ++j)
+                for (int i = 0; i < m; ++i) {
+                    for (int v = 0; v < nv; ++v) acc[v] = 0.0;
+                    for (int axis = 0; axis < d; ++axis) {
+                        const int row = (axis == 0) ? i : (axis == 1) ? j : k;
+                        for (int t = 0; t < m; ++t) {
+                            const int ii = (axis == 0) ? t : i;
+                            const int jj = (axis == 1) ? t : j;
+                            const int kk = (axis == 2) ? t : k;
+                            for (int v = 0; v < nv; ++v)
+                                st[v] = U[field_offset(d, m, group, e, ii, jj, kk, v)];
+                            hfo_flux(d, st, nu, zeta, T, line[t]);
+                        }
+                        for (int v = 0; v < nv; ++v) {
+                            if (!hfo_flux_structural_nonzero(d, axis, v)) continue;
+                            double s = 0.0;
+                            for (int t = 0; t < m; ++t) s += D[row * m + t] * line[t][axis * nv + v];
+                            acc[v] += jac[axis] * s;
+                        }
+                    }
+                    for (int v = 0; v < nv; ++v) st[v] = U[field_offset(d, m, group, e, i, j, k, v)];
+                    if (with_source) hfo_source(d, st, T, src);
+                    for (int v = 0; v < nv; ++v) {
+                        double o = -acc[v];
+                        if (with_source) o += src[v];
+                        out[field_offset(d, m, group, e, i, j, k, v)] = o;
+                    }
+                }
+    return 0;
+}
+
+HFO_EXPORT int hfo_oracle_divergence(int d, int p, int n_elem, int group, const double *U, double *out,
+                                     double nu, double zeta, double T, const double *jac, int with_source) {
+    if (p < 1 || p > 8 || n_elem < 0 || group < 1) return -1;
+    memset(out, 0, sizeof(double) * (size_t)hfo_field_words(d, p, n_elem, group));
+    return hfo_oracle_divergence_range(d, p, group, U, out, nu, zeta, T, jac, with_source, 0, n_elem);
+}
+
+/* ---- std::mt19937_64 (the C++11 standard engine; oracle.hpp:156) ---------- */
+typedef struct {
+    uint64_t mt[312];
+    int idx;
+} mt64;
+
+static void mt64_seed(mt64 *s, uint64_t seed) {
+    s->mt[0] = seed;
+    for (int i = 1; i < 312; ++i)
+        s->mt[i] = 6364136223846793005ULL * (s->mt[i - 1] ^ (s->mt[i - 1] >> 62)) + (uint64_t)i;
+    s->idx = 312;
+}
+
+static uint64_t mt64_next(mt64 *s) {
+    static const uint64_t UPPER = 0xFFFFFFFF80000000ULL, LOWER = 0x7FFFFFFFULL;
+    static const uint64_t A = 0xB5026F5AA96619E9ULL;
+    if (s->idx >= 312) {
+        for (int i = 0; i < 312; ++i) {
+            const uint64_t x = (s->mt[i] & UPPER) | (s->mt[(i + 1) % 312] & LOWER);
+            uint64_t xa = x >> 1;
+            if (x & 1ULL) xa ^= A;
+            s->mt[i] = s->mt[(i + 156) % 312] ^ xa;
+        }
+        s->idx = 0;
+    }
+    uint64_t y = s->mt[s->idx++];
+    y ^= (y >> 29) & 0x5555555555555555ULL;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+    y ^= y >> 43;
+    return y;
+}
+
+/* libstdc++ uniform_real_distribution<double>(a,b) over a 64-bit engine:
+ * generate_canonical<double,53> takes one draw, x / 2^64 (clamped below 1),
+ * then r * (b - a) + a. */
+static double mt64_uniform(mt64 *s, double a, double b) {
+    double r = (double)mt64_next(s) / 18446744073709551616.0;
+    if (r >= 1.0) r = nextafter(1.0, 0.0);
+    return r * (b - a) + a;
+}
+
+HFO_EXPORT uint64_t hfo_mt19937_64_first(uint64_t seed, int skip) {
+    mt64 s;
+    mt64_seed(&s, seed);
+    uint64_t v = 0;
+    for (int i = 0; i <= skip; ++i) v = mt64_next(&s);
+    return v;
+}
+
+/* oracle.hpp:154-166.  U(-1,1) per word in draw order e, k, j, i, v, then
+ * quantised to float when fp32 (layout.hpp:149-152).  Padding stays 0.
+ * Elements [0, e_end) are drawn; only [e_begin, e_end) are stored, so that a
+ * streaming caller can regenerate any prefix-aligned slice bit-exactly. */
+HFO_EXPORT int hfo_random_field(int d, int p, int n_elem, int group, int fp32, uint64_t seed, double *out) {
+    const int m = p + 1, nv = 1 + d + d * d, mk = (d == 3) ? m : 1;
+    mt64 s;
+    mt64_seed(&s, seed);
+    memset(out, 0, sizeof(double) * (size_t)hfo_field_words(d, p, n_elem, group));
+    for (int e = 0; e < n_elem; ++e)
+        for (int k = 0; k < mk; ++k)
+            for (int j = 0; j < m; ++j)
+                for (int i = 0; i < m; ++i)
+                    for (int v = 0; v < nv; ++v) {
+                        double x = mt64_uniform(&s, -1.0, 1.0);
+                        if (fp32) x = (double)(float)x;
+                        out[field_offset(d, m, group, e, i, j, k, v)] = x;
+                    }
+    return 0;
+}
+
+/* oracle.hpp:65-83 */
+static void tgv_point(double x, double y, double z, double gamma, double mach, double *s) {
+    memset(s, 0, sizeof(double) * 13);
+    s[0] = 1.0 / (gamma * mach * mach) + (1.0 / 16.0) * cos(2.0 * z + 2.0) * (cos(2.0 * x) + cos(2.0 * y));
+    s[1] = sin(x) * cos(y) * cos(z);
+    s[2] = -cos(x) * sin(y) * cos(z);
+    s[3] = 0.0;
+    s[4] = cos(x) * cos(y) * cos(z);
+    s[5] = -sin(x) * sin(y) * cos(z);
+    s[6] = -sin(x) * cos(y) * sin(z);
+    s[7] = sin(x) * sin(y) * cos(z);
+    s[8] = -cos(x) * cos(y) * cos(z);
+    s[9] = cos(x) * sin(y) * sin(z);
+    s[10] = s[11] = s[12] = 0.0;
+}
+
+/* oracle.hpp:94-110 */
+HFO_EXPORT void hfo_factor3(int n, int *out3) {
+    int best[3] = {n, 1, 1};
+    long best_score = 1L << 60;
+    for (int a = 1; a <= n; ++a) {
+        if (n % a) continue;
+        const int bc = n / a;
+        for (int b = 1; b <= bc; ++b) {
+            if (bc % b) continue;
+            const int c = bc / b;
+            int mx = a, mn = a;
+            if (b > mx) mx = b;
+            if (c > mx) mx = c;
+            if (b < mn) mn = b;
+            if (c < mn) mn = c;
+            const long score = (long)mx - mn;
+            if (score < best_score) {
+                best_score = score;
+                best[0] = a;
+                best[1] = b;
+                best[2] = c;
+            }
+        }
+    }
+    if (best[0] < best[2]) {
+        const int t = best[0];
+        best[0] = best[2];
+        best[2] = t;
+    }
+    out3[0] = best[0];
+    out3[1] = best[1];
+    out3[2] = best[2];
+}
+
+/* oracle.hpp:116-151.  d = 3 vortex field on an elems[0] x elems[1] x elems[2]
+ * brick of elements with the given widths and origin. */
+HFO_EXPORT int hfo_tgv_field(int p, int group, const int *elems, const double *origin, const double *width,
+                             double gamma, double mach, int zero_mean_pressure, int fp32, double *out) {
+    const int m = p + 1, n_elem = elems[0] * elems[1] * elems[2];
+    double nodes[16], s[13];
+    double coords[3][16];
+    if (hfo_gauss_legendre_points(m, nodes) != 0) return -1;
+    const double offset = zero_mean_pressure ? 1.0 / (gamma * mach * mach) : 0.0;
+    memset(out, 0, sizeof(double) * (size_t)hfo_field_words(3, p, n_elem, group));
+    for (int e = 0; e < n_elem; ++e) {
+        const int ec[3] = {e % elems[0], (e / elems[0]) % elems[1], e / (elems[0] * elems[1])};
+        for (int a = 0; a < 3; ++a) {
+            const double lo = origin[a] + width[a] * ec[a];
+            for (int t = 0; t < m; ++t) coords[a][t] = lo + 0.5 * width[a] * (nodes[t] + 1.0);
+        }
+        for (int k = 0; k < m; ++k)
+            for (int j = 0; j < m; ++j)
+                for (int i = 0; i < m; ++i) {
+                    tgv_point(coords[0][i], coords[1][j], coords[2][k], gamma, mach, s);
+                    s[0] -= offset;
+                    for (int v = 0; v < 13; ++v) {
+                        double x = s[v];
+                        if (fp32) x = (double)(float)x;
+                        out[field_offset(3, m, group, e, i, j, k, v)] = x;
+                    }
+                }
+    }
+    return 0;
+}
+
+/* verify.hpp:19-33.  max|got-ref| / max(1, max|ref|) over real elements. */
+HFO_EXPORT double hfo_field_rel_error(int d, int p, int n_elem, int group, const double *got, const double *ref) {
+    const int m = p + 1, nv = 1 + d + d * d, mk = (d == 3) ? m : 1;
+    double maxdiff = 0.0, maxref = 0.0;
+    for (int e = 0; e < n_elem; ++e)
+        for (int k = 0; k < mk; ++k)
+            for (int j = 0; j < m; ++j)
+                for (int i = 0; i < m; ++i)
+                    for (int v = 0; v < nv; ++v) {
+                        const int64_t o = field_offset(d, m, group, e, i, j, k, v);
+                        const double r = ref[o];
+                        const double df = fabs(got[o] - r);
+                        if (df > maxdiff || df != df) maxdiff = (df != df) ? INFINITY : df;
+                        if (fabs(r) > maxref) maxref = fabs(r);
+                    }
+    return maxdiff / (maxref > 1.0 ? maxref : 1.0);
+}
+
+/* verify.hpp:35 */
+HFO_EXPORT double hfo_verify_tolerance(int fp32) { return fp32 ? 1e-5 : 1e-11; }
+
+/* io_model.hpp:27-40: words per point of the stage pipeline.
+ * stage: 0=S2, 1=S3, 2=S6, 3=Fused23, 4=Fused236 */
+HFO_EXPORT int hfo_io_model(int d, const int *stages, int n_stages, int64_t *reads, int64_t *writes) {
+    const int64_t nv = hfo_n_vars(d);
+    if (nv < 0) return -1;
+    *reads = *writes = 0;
+    for (int i = 0; i < n_stages; ++i) {
+        switch (stages[i]) {
+            case 0: *reads += nv; *writes += d * nv; break;
+            case 1: *reads += d * nv; *writes += nv; break;
+            case 2: *reads += nv + d * d; *writes += nv; break;
+            case 3: case 4: *reads += nv; *writes += nv; break;
+            default: return -1;
+        }
+    }
+    return 0;
+}

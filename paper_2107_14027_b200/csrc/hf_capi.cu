@@ -1,0 +1,495 @@
+// hf_capi.cu -- the C ABI (include/hexfuse_b200.h): validation, operator
+// construction, method selection, launches, the pipelined host-buffer path and
+// the multi-GPU partition.  Everything here is host code; the kernels live in
+// the hf_inst_*.cu units.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/hexfuse_b200.h"
+#include "hf_dispatch.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(HF_ERUNTIME, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+int64_t ipow64(int64_t b, int e) {
+    int64_t r = 1;
+    for (int i = 0; i < e; ++i) r *= b;
+    return r;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Operators (operators.hpp:17-74): Gauss-Legendre nodes by Newton iteration from
+// Chebyshev guesses with exact symmetrisation; D by barycentric weights with the
+// row-sum diagonal.  The reference stops at m = 8 (operators.hpp:18); the same
+// construction is used for m = 9 (d = 2, p = 8).
+// ---------------------------------------------------------------------------------------------
+bool gl_nodes(int m, double* x) {
+    if (m < 2 || m > 9) return false;
+    for (int i = 0; i < m; ++i) {
+        double z = std::cos(M_PI * (i + 0.75) / (m + 0.5));
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = 0.0;
+            for (int j = 0; j < m; ++j) {
+                const double p2 = p1;
+                p1 = p0;
+                p0 = ((2.0 * j + 1.0) * z * p1 - j * p2) / (j + 1.0);
+            }
+            const double dp = m * (z * p0 - p1) / (z * z - 1.0);
+            const double z1 = z;
+            z = z1 - p0 / dp;
+            if (std::fabs(z - z1) < 1e-15) break;
+        }
+        x[m - 1 - i] = z;
+    }
+    for (int i = 0; i < m / 2; ++i) {
+        const double v = 0.5 * (x[m - 1 - i] - x[i]);
+        x[i] = -v;
+        x[m - 1 - i] = v;
+    }
+    if (m % 2 == 1) x[m / 2] = 0.0;
+    return true;
+}
+
+void derivative_matrix(int m, const double* x, double* D) {
+    double wb[16];
+    for (int k = 0; k < m; ++k) {
+        wb[k] = 1.0;
+        for (int j = 0; j < m; ++j)
+            if (j != k) wb[k] /= (x[k] - x[j]);
+    }
+    for (int j = 0; j < m; ++j) {
+        double diag = 0.0;
+        for (int k = 0; k < m; ++k) {
+            if (k == j) continue;
+            const double v = (wb[k] / wb[j]) / (x[j] - x[k]);
+            D[j * m + k] = v;
+            diag -= v;
+        }
+        D[j * m + j] = diag;
+    }
+}
+
+struct OpCache {
+    double D[10][hfb::kMaxM * hfb::kMaxM];
+    bool ok[10];
+    OpCache() {
+        for (int m = 0; m < 10; ++m) {
+            double x[16];
+            ok[m] = gl_nodes(m, x);
+            if (ok[m]) derivative_matrix(m, x, D[m]);
+        }
+    }
+};
+const OpCache& ops() {
+    static const OpCache c;
+    return c;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Validation (equations.hpp:19-23, layout.hpp:92-99, operators.hpp:18)
+// ---------------------------------------------------------------------------------------------
+int validate(const hf_problem* pr) {
+    if (!pr) return fail(HF_EINVAL, "hf_problem: null");
+    if (pr->d != 2 && pr->d != 3) return fail(HF_EINVAL, "hf_problem: d must be 2 or 3");
+    const int pmax = (pr->d == 3) ? 7 : 8;
+    if (pr->p < 1 || pr->p > pmax)
+        return fail(HF_EINVAL, "hf_problem: p must be in [1," + std::to_string(pmax) + "] for d=" +
+                                   std::to_string(pr->d));
+    if (pr->n_elem < 0) return fail(HF_EINVAL, "hf_problem: n_elem must be >= 0");
+    if (pr->group < 1) return fail(HF_EINVAL, "hf_problem: group must be >= 1");
+    if (pr->precision != HF_FP32 && pr->precision != HF_FP64)
+        return fail(HF_EINVAL, "hf_problem: precision must be HF_FP32 or HF_FP64");
+    if (!(pr->nu >= 0.0)) return fail(HF_EINVAL, "PhysParams: nu must be >= 0");
+    if (!(pr->zeta > 0.0)) return fail(HF_EINVAL, "PhysParams: zeta must be > 0");
+    if (!(pr->T > 0.0)) return fail(HF_EINVAL, "PhysParams: T must be > 0");
+    if (pr->method < HF_METHOD_AUTO || pr->method > HF_METHOD_UNFUSED)
+        return fail(HF_EINVAL, "hf_problem: unknown method");
+    if (pr->method == HF_METHOD_PLANAR && (pr->d != 3 || pr->p > 6))
+        return fail(HF_EINVAL, "planar method: d must be 3 and p <= 6");
+    const int64_t words = ipow64(pr->p + 1, pr->d) * (1 + pr->d + pr->d * pr->d) * int64_t(pr->group);
+    if (words > (int64_t(1) << 31)) return fail(HF_EINVAL, "hf_problem: group too large");
+    return HF_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Selection
+// ---------------------------------------------------------------------------------------------
+struct SelRow {
+    int d, p, prec, method, variant;
+};
+const SelRow kSelect[] = {
+#include "hf_select_table.inc"
+    {0, 0, 0, 0, 0}};
+
+void select_method(const hf_problem* pr, int* method, int* variant) {
+    *variant = 0;
+    if (pr->method != HF_METHOD_AUTO) {
+        *method = pr->method;
+        return;
+    }
+    *method = HF_METHOD_LINES;
+    for (const SelRow& r : kSelect)
+        if (r.d == pr->d && r.p == pr->p && r.prec == pr->precision) {
+            *method = r.method;
+            *variant = r.variant;
+        }
+}
+
+template <class R>
+hfb::Params<R> make_params(const hf_problem* pr, const void* u, void* out, void* ws) {
+    hfb::Params<R> p;
+    std::memset(&p, 0, sizeof(p));
+    const int m = pr->p + 1;
+    for (int i = 0; i < m * m; ++i) p.D[i] = R(ops().D[m][i]);
+    p.nu = R(pr->nu);
+    p.zeta = R(pr->zeta);
+    p.invT = R(1.0 / pr->T);
+    for (int a = 0; a < 3; ++a) {
+        p.jac[a] = R(pr->jac[a]);
+        p.jac_invT[a] = R(pr->jac[a] / pr->T);
+    }
+    p.u = static_cast<const R*>(u);
+    p.out = static_cast<R*>(out);
+    p.ws = static_cast<R*>(ws);
+    p.n_elem = pr->n_elem;
+    p.group = pr->group;
+    p.group_words = int64_t(pr->group) * ipow64(m, pr->d) * (1 + pr->d + pr->d * pr->d);
+    p.fast_ok = 0;
+    return p;
+}
+
+// Resolve + launch (dry: describe only).  ws only for the unfused method.
+int dispatch(const hf_problem* pr, const void* u, void* out, void* ws, cudaStream_t st, hfb::KInfo* info, bool dry,
+             int force_method = -1, int force_variant = -1) {
+    int method, variant;
+    select_method(pr, &method, &variant);
+    if (force_method >= 0) method = force_method;
+    if (force_variant >= 0) variant = force_variant;
+    const bool src = pr->with_source != 0;
+    int rc;
+    if (pr->precision == HF_FP32) {
+        const auto prm = make_params<float>(pr, u, out, ws);
+        if (method == HF_METHOD_PLANAR) rc = hfb::planar_f32(pr->p, src, prm, st, info, dry);
+        else if (method == HF_METHOD_UNFUSED) rc = hfb::unfused_f32(pr->d, pr->p, src, prm, st, info, dry);
+        else rc = pr->d == 3 ? hfb::lines_f32_d3(pr->p, variant, src, prm, st, info, dry)
+                             : hfb::lines_f32_d2(pr->p, variant, src, prm, st, info, dry);
+    } else {
+        const auto prm = make_params<double>(pr, u, out, ws);
+        if (method == HF_METHOD_PLANAR) rc = hfb::planar_f64(pr->p, src, prm, st, info, dry);
+        else if (method == HF_METHOD_UNFUSED) rc = hfb::unfused_f64(pr->d, pr->p, src, prm, st, info, dry);
+        else rc = pr->d == 3 ? hfb::lines_f64_d3(pr->p, variant, src, prm, st, info, dry)
+                             : hfb::lines_f64_d2(pr->p, variant, src, prm, st, info, dry);
+    }
+    if (rc == hfb::kUnsupported) return fail(HF_EINVAL, "no kernel for this (method, d, p, variant)");
+    if (rc != 0) return cuda_fail(cudaError_t(rc), "kernel launch");
+    return HF_OK;
+}
+
+size_t word_bytes(const hf_problem* pr) { return pr->precision == HF_FP32 ? 4 : 8; }
+
+}  // namespace
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+extern "C" {
+
+const char* hf_last_error(void) { return g_last_error.c_str(); }
+const char* hf_version(void) { return "hexfuse_b200 0.1 (sm_100a)"; }
+
+int hf_n_vars(int d) { return (d == 2 || d == 3) ? 1 + d + d * d : -1; }
+
+int hf_validate(const hf_problem* pr) { return validate(pr); }
+
+int64_t hf_field_words(const hf_problem* pr) {
+    if (!pr || pr->group < 1 || (pr->d != 2 && pr->d != 3) || pr->n_elem < 0) return -1;
+    const int64_t ng = (pr->n_elem + pr->group - 1) / pr->group;
+    return ng * pr->group * ipow64(pr->p + 1, pr->d) * (1 + pr->d + pr->d * pr->d);
+}
+
+int64_t hf_offset(const hf_problem* pr, int64_t e, int i, int j, int k, int v) {
+    const int m = pr->p + 1;
+    const int64_t np = ipow64(m, pr->d);
+    const int64_t gw = int64_t(pr->group) * np * (1 + pr->d + pr->d * pr->d);
+    const int64_t pt = i + int64_t(m) * j + int64_t(m) * m * k;
+    return (e / pr->group) * gw + (e % pr->group) + int64_t(pr->group) * (pt + np * v);
+}
+
+int hf_derivative_matrix(int m, double* D_out, double* nodes_out) {
+    double x[16];
+    if (!gl_nodes(m, x)) return fail(HF_EINVAL, "gauss_legendre_points: m must be in [2,9]");
+    if (nodes_out) std::memcpy(nodes_out, x, sizeof(double) * m);
+    if (D_out) derivative_matrix(m, x, D_out);
+    return HF_OK;
+}
+
+int64_t hf_algorithmic_bytes_per_point(const hf_problem* pr) {
+    return 2 * int64_t(1 + pr->d + pr->d * pr->d) * int64_t(word_bytes(pr));
+}
+
+int hf_selected_method(const hf_problem* pr) {
+    if (int rc = validate(pr)) return -rc;
+    int method, variant;
+    select_method(pr, &method, &variant);
+    return method;
+}
+
+int hf_kernel_info_get(const hf_problem* pr, hf_kernel_info* out) {
+    if (int rc = validate(pr)) return rc;
+    hfb::KInfo ki;
+    if (int rc = dispatch(pr, nullptr, nullptr, nullptr, nullptr, &ki, true)) return rc;
+    out->method = ki.method;
+    out->elems_per_cta = ki.elems_per_cta;
+    out->block_threads = ki.block_threads;
+    out->shared_bytes = ki.shared_bytes;
+    out->registers = ki.registers;
+    out->grid = ki.grid;
+    out->bulk_path = ki.bulk_path;
+    std::memcpy(out->name, ki.name, sizeof(out->name));
+    return HF_OK;
+}
+
+int hf_preferred_group(const hf_problem* pr) {
+    if (int rc = validate(pr)) return -rc;
+    hf_problem q = *pr;
+    int method, variant;
+    select_method(pr, &method, &variant);
+    if (method == HF_METHOD_UNFUSED) return 32;
+    hfb::KInfo ki;
+    if (dispatch(&q, nullptr, nullptr, nullptr, nullptr, &ki, true)) return -HF_EINVAL;
+    return ki.elems_per_cta;
+}
+
+int hf_fused_divergence(const hf_problem* pr, const void* u_dev, void* divf_dev, void* stream) {
+    if (int rc = validate(pr)) return rc;
+    int method, variant;
+    select_method(pr, &method, &variant);
+    if (method == HF_METHOD_UNFUSED)
+        return fail(HF_EINVAL, "hf_fused_divergence: use hf_unfused_divergence for the unfused method");
+    if (pr->n_elem > 0 && (!u_dev || !divf_dev)) return fail(HF_EINVAL, "hf_fused_divergence: null buffer");
+    if (u_dev == divf_dev && pr->n_elem > 0) return fail(HF_EINVAL, "hf_fused_divergence: in-place not supported");
+    return dispatch(pr, u_dev, divf_dev, nullptr, static_cast<cudaStream_t>(stream), nullptr, false);
+}
+
+size_t hf_unfused_workspace_bytes(const hf_problem* pr) {
+    if (validate(pr)) return 0;
+    return size_t(hf_field_words(pr)) * size_t(pr->d) * word_bytes(pr);
+}
+
+int hf_unfused_divergence(const hf_problem* pr, const void* u_dev, void* divf_dev, void* ws_dev, void* stream) {
+    if (int rc = validate(pr)) return rc;
+    if (pr->n_elem > 0 && (!u_dev || !divf_dev || !ws_dev)) return fail(HF_EINVAL, "hf_unfused_divergence: null buffer");
+    return dispatch(pr, u_dev, divf_dev, ws_dev, static_cast<cudaStream_t>(stream), nullptr, false,
+                    HF_METHOD_UNFUSED, 0);
+}
+
+// Internal hook for tuning sweeps (tools/select_methods.py): launch a specific
+// method/variant regardless of the selection table.  Not part of the header.
+HF_API int hf_fused_divergence_variant(const hf_problem* pr, int method, int variant, const void* u_dev, void* divf_dev,
+                                void* stream, hf_kernel_info* info) {
+    if (int rc = validate(pr)) return rc;
+    hfb::KInfo ki;
+    int rc = dispatch(pr, u_dev, divf_dev, nullptr, static_cast<cudaStream_t>(stream), &ki, info != nullptr && !u_dev,
+                      method, variant);
+    if (rc) return rc;
+    if (info) {
+        if (u_dev) {
+            hfb::KInfo k2;
+            dispatch(pr, nullptr, nullptr, nullptr, nullptr, &k2, true, method, variant);
+            ki = k2;
+        }
+        info->method = ki.method;
+        info->elems_per_cta = ki.elems_per_cta;
+        info->block_threads = ki.block_threads;
+        info->shared_bytes = ki.shared_bytes;
+        info->registers = ki.registers;
+        info->grid = ki.grid;
+        info->bulk_path = ki.bulk_path;
+        std::memcpy(info->name, ki.name, sizeof(info->name));
+    }
+    return HF_OK;
+}
+
+int hf_partition(const hf_problem* pr, int n_parts, int part, int64_t* e_begin, int64_t* n_elem_part,
+                 int64_t* word_offset) {
+    if (int rc = validate(pr)) return rc;
+    if (n_parts < 1 || part < 0 || part >= n_parts) return fail(HF_EINVAL, "hf_partition: bad part");
+    const int64_t ng = (pr->n_elem + pr->group - 1) / pr->group;
+    const int64_t g0 = ng * part / n_parts, g1 = ng * (part + 1) / n_parts;
+    const int64_t e0 = g0 * pr->group;
+    const int64_t e1 = std::min<int64_t>(pr->n_elem, g1 * pr->group);
+    *e_begin = e0;
+    *n_elem_part = std::max<int64_t>(0, e1 - e0);
+    const int64_t gw = int64_t(pr->group) * ipow64(pr->p + 1, pr->d) * (1 + pr->d + pr->d * pr->d);
+    *word_offset = g0 * gw;
+    return HF_OK;
+}
+
+}  // extern "C"
+
+// =============================================================================================
+// Host-buffer path: slices of whole groups streamed through the GPU, H2D / kernel / D2H on
+// three rotating streams so both copy engines and the SMs are busy at once.
+// =============================================================================================
+struct hf_context {
+    int device = 0;
+    static constexpr int kSlots = 3;
+    cudaStream_t stream[kSlots] = {};
+    cudaEvent_t done[kSlots] = {};
+    void* d_in[kSlots] = {};
+    void* d_out[kSlots] = {};
+    size_t slot_bytes = 0;
+};
+
+namespace {
+
+int ctx_reserve(hf_context* c, size_t bytes) {
+    if (bytes <= c->slot_bytes) return HF_OK;
+    for (int s = 0; s < hf_context::kSlots; ++s) {
+        if (c->d_in[s]) cudaFree(c->d_in[s]);
+        if (c->d_out[s]) cudaFree(c->d_out[s]);
+        c->d_in[s] = c->d_out[s] = nullptr;
+    }
+    c->slot_bytes = 0;
+    for (int s = 0; s < hf_context::kSlots; ++s) {
+        cudaError_t e = cudaMalloc(&c->d_in[s], bytes);
+        if (e == cudaSuccess) e = cudaMalloc(&c->d_out[s], bytes);
+        if (e != cudaSuccess) return cuda_fail(e, "hf_context: cudaMalloc");
+    }
+    c->slot_bytes = bytes;
+    return HF_OK;
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+extern "C" {
+
+hf_context* hf_context_create(int device) {
+    auto* c = new (std::nothrow) hf_context;
+    if (!c) return nullptr;
+    c->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    for (int s = 0; s < hf_context::kSlots && e == cudaSuccess; ++s) {
+        e = cudaStreamCreateWithFlags(&c->stream[s], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->done[s], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) {
+        cuda_fail(e, "hf_context_create");
+        hf_context_destroy(c);
+        return nullptr;
+    }
+    return c;
+}
+
+void hf_context_destroy(hf_context* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    for (int s = 0; s < hf_context::kSlots; ++s) {
+        if (c->stream[s]) cudaStreamSynchronize(c->stream[s]);
+        if (c->d_in[s]) cudaFree(c->d_in[s]);
+        if (c->d_out[s]) cudaFree(c->d_out[s]);
+        if (c->done[s]) cudaEventDestroy(c->done[s]);
+        if (c->stream[s]) cudaStreamDestroy(c->stream[s]);
+    }
+    delete c;
+}
+
+int hf_fused_divergence_host(hf_context* c, const hf_problem* pr, const void* u_host, void* divf_host) {
+    if (!c) return fail(HF_EINVAL, "hf_fused_divergence_host: null context");
+    if (int rc = validate(pr)) return rc;
+    if (pr->n_elem == 0) return HF_OK;
+    if (!u_host || !divf_host) return fail(HF_EINVAL, "hf_fused_divergence_host: null buffer");
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+
+    const size_t w = word_bytes(pr);
+    const int64_t gw = int64_t(pr->group) * ipow64(pr->p + 1, pr->d) * (1 + pr->d + pr->d * pr->d);
+    const int64_t n_groups = (pr->n_elem + pr->group - 1) / pr->group;
+    // Slice: whole groups, ~48 MB per slot, a multiple of the kernel's chunk.
+    int pref = hf_preferred_group(pr);
+    if (pref < 1) pref = 1;
+    int64_t slice_groups = std::max<int64_t>(1, (int64_t(48) << 20) / int64_t(gw * w));
+    const int64_t chunk_groups = std::max<int64_t>(1, (pref + pr->group - 1) / pr->group);
+    slice_groups = std::max<int64_t>(chunk_groups, slice_groups / chunk_groups * chunk_groups);
+    slice_groups = std::min<int64_t>(slice_groups, n_groups);
+    if (int rc = ctx_reserve(c, size_t(slice_groups * gw) * w)) return rc;
+
+    // Pageable host memory is pinned for the duration of the call.
+    const size_t total = size_t(n_groups * gw) * w;
+    bool reg_in = false, reg_out = false;
+    if (!is_pinned(u_host)) {
+        if (cudaHostRegister(const_cast<void*>(u_host), total, cudaHostRegisterReadOnly) == cudaSuccess) reg_in = true;
+        else cudaGetLastError();
+    }
+    if (!is_pinned(divf_host)) {
+        if (cudaHostRegister(divf_host, total, cudaHostRegisterDefault) == cudaSuccess) reg_out = true;
+        else cudaGetLastError();
+    }
+
+    int rc = HF_OK;
+    int64_t s_idx = 0;
+    for (int64_t g0 = 0; g0 < n_groups && rc == HF_OK; g0 += slice_groups, ++s_idx) {
+        const int slot = int(s_idx % hf_context::kSlots);
+        const int64_t ng = std::min<int64_t>(slice_groups, n_groups - g0);
+        const size_t bytes = size_t(ng * gw) * w;
+        cudaStream_t st = c->stream[slot];
+        const auto* src = static_cast<const unsigned char*>(u_host) + size_t(g0 * gw) * w;
+        auto* dst = static_cast<unsigned char*>(divf_host) + size_t(g0 * gw) * w;
+        // the stream is in-order, so the slot's previous D2H has completed before this H2D lands
+        if ((e = cudaMemcpyAsync(c->d_in[slot], src, bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
+            rc = cuda_fail(e, "H2D");
+            break;
+        }
+        hf_problem sp = *pr;
+        sp.n_elem = std::min<int64_t>(pr->n_elem - g0 * pr->group, ng * pr->group);
+        if (sp.method == HF_METHOD_UNFUSED) sp.method = HF_METHOD_AUTO;
+        if (sp.n_elem < ng * pr->group) {
+            // partial last group: padding comes back as zeros, like the reference's zeroed result (oracle.hpp:26-27)
+            if ((e = cudaMemsetAsync(c->d_out[slot], 0, bytes, st)) != cudaSuccess) {
+                rc = cuda_fail(e, "memset");
+                break;
+            }
+        }
+        rc = dispatch(&sp, c->d_in[slot], c->d_out[slot], nullptr, st, nullptr, false);
+        if (rc) break;
+        if ((e = cudaMemcpyAsync(dst, c->d_out[slot], bytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess) {
+            rc = cuda_fail(e, "D2H");
+            break;
+        }
+    }
+    for (int s = 0; s < hf_context::kSlots; ++s) {
+        e = cudaStreamSynchronize(c->stream[s]);
+        if (e != cudaSuccess && rc == HF_OK) rc = cuda_fail(e, "hf_fused_divergence_host");
+    }
+    if (reg_in) cudaHostUnregister(const_cast<void*>(u_host));
+    if (reg_out) cudaHostUnregister(divf_host);
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,103 @@
+// hf_common.cuh -- shared definitions for the B200 (sm_100a) fused flux +
+// divergence kernels: the launch parameter block, the AoSoA layout
+// (layout.hpp:128-134), and the PTX wrappers for mbarriers and bulk async
+// copies (cp.async.bulk, TMA's non-tensor form).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hfb {
+
+constexpr int kMaxM = 9;  // m = p+1 <= 9 (d=2 p=8)
+
+__host__ __device__ constexpr int ipow_c(int b, int e) { return e == 0 ? 1 : b * ipow_c(b, e - 1); }
+__host__ __device__ constexpr int n_vars_c(int d) { return 1 + d + d * d; }
+__host__ __device__ constexpr int var_grad_c(int d, int b, int a) { return 1 + d + b * d + a; }
+
+// Everything a launch needs, passed by value as a __grid_constant__ so that the
+// operator matrix and physical constants live in the kernel-parameter constant
+// bank (immediate c[0x0][...] operands in DFMA/FFMA) and launches are
+// reentrant across streams with no per-device __constant__ state.
+template <class R>
+struct Params {
+    R D[kMaxM * kMaxM];  // derivative matrix, row-major m x m (operators.hpp:49-74)
+    R nu, zeta, invT;    // PhysParams (equations.hpp:14-24), 1/T precomputed
+    R jac[3];            // constant per-axis metric (oracle.hpp:47)
+    R jac_invT[3];       // jac[a] / T : gradient-row scale
+    const R* __restrict__ u;  // input field, AoSoA (layout.hpp:128-134)
+    R* __restrict__ out;      // divergence, same layout
+    R* __restrict__ ws;       // unfused only: flux workspace
+    long long n_elem;
+    long long group_words;    // group * m^d * n_v
+    int group;
+    int fast_ok;              // host-verified: bulk-copy alignment holds for full chunks
+};
+
+// ---------------------------------------------------------------------------------------------
+// PTX: mbarrier + cp.async.bulk (SASS UBLKCP / SYNCS.*)
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0, both ends 16B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// shared -> global bulk copy, bulk-group completion
+__device__ __forceinline__ void bulk_s2g(void* dst_gmem, const void* src_smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst_gmem),
+                 "r"(smem_u32(src_smem)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+__device__ __forceinline__ void bulk_wait_read_all() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// make generic-proxy shared-memory writes visible to the async proxy (bulk store)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// streaming (read-once) global load for the generic loader
+template <class R>
+__device__ __forceinline__ R ld_stream(const R* p) {
+    return __ldcs(p);
+}
+
+}  // namespace hfb

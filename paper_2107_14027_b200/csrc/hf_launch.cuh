@@ -1,0 +1,170 @@
+// hf_launch.cuh -- per-configuration launch shapes and the templated launchers.
+//
+// The reference picks one static configuration per (p, precision) from the
+// paper's Volta measurements (preset_table, presets.hpp:25-37;
+// default_lines_n, presets.hpp:86-103, sized for a 96 KiB shared-memory cap).
+// On B200 (227 KB shared per CTA, 228 KB per SM) the lines kernel's chunk is
+// sized for about three co-resident CTAs per SM, so one CTA can be staging its
+// next chunk through the bulk-copy engine while the others compute; the
+// variant knob (0: default, 1: half, 2: double the elements per CTA) exists so
+// the measured selection (hf_select_table.inc) can pick the best of three.
+#pragma once
+
+#include <cstdio>
+#include <cstring>
+
+#include "hf_common.cuh"
+#include "hf_lines.cuh"
+#include "hf_planar.cuh"
+#include "hf_unfused.cuh"
+
+namespace hfb {
+
+struct KInfo {
+    int method = 0;
+    int elems_per_cta = 0;
+    int block_threads = 0;
+    int shared_bytes = 0;
+    int registers = 0;
+    long long grid = 0;
+    int bulk_path = 0;
+    char name[96] = {0};
+};
+
+constexpr int kLinesSmemBudget = 72 * 1024;
+constexpr int kMaxSmemPerCta = 227 * 1024;
+
+template <class R, int DIM, int M>
+constexpr int lines_ne_default() {
+    constexpr int min_ne = 16 / int(sizeof(R));  // a chunk row must be a 16-byte multiple
+    int ne = (DIM == 2) ? 128 : 64;
+    while (ne > min_ne && (LinesShape<R, DIM, M, 1>::HDR +
+                           size_t(ne) * ipow_c(M, DIM) * (n_vars_c(DIM) + 1 + DIM) * sizeof(R) >
+                               size_t(kLinesSmemBudget) ||
+                           ne * ipow_c(M, DIM - 1) > 512))
+        ne /= 2;
+    return ne;
+}
+
+template <class R, int DIM, int M, int VARIANT>
+constexpr int lines_ne() {
+    constexpr int ne0 = lines_ne_default<R, DIM, M>();
+    constexpr int min_ne = 16 / int(sizeof(R));
+    if constexpr (VARIANT == 1) return ne0 / 2 >= min_ne ? ne0 / 2 : 0;
+    else if constexpr (VARIANT == 2) {
+        constexpr int ne = ne0 * 2;
+        return (LinesShape<R, DIM, M, ne>::SMEM <= size_t(kMaxSmemPerCta) && ne * ipow_c(M, DIM - 1) <= 1024) ? ne
+                                                                                                            : 0;
+    } else return ne0;
+}
+
+template <class R, int M>
+constexpr int planar_ne() {
+    int ne = 64;
+    while (ne > 8 && ne * M > 128) ne /= 2;
+    return ne;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <class K>
+inline int set_smem_attr(K kernel, size_t smem) {
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return int(e);
+    }
+    return 0;
+}
+
+template <class K>
+inline void fill_regs(K kernel, KInfo* info) {
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess) info->registers = fa.numRegs;
+    else {
+        cudaGetLastError();
+        info->registers = 0;
+    }
+}
+
+inline const char* prec_name(size_t w) { return w == 4 ? "fp32" : "fp64"; }
+
+// Launch (or, with dry = true, only describe) the lines kernel.
+template <class R, int DIM, int M, int NE, bool SRC>
+cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
+    using S = LinesShape<R, DIM, M, NE>;
+    auto kernel = hf_lines_kernel<R, DIM, M, NE, SRC>;
+    const long long grid = (p.n_elem + NE - 1) / NE;
+    const bool fast_layout = (p.group % NE == 0) && ((long long)p.group * sizeof(R)) % 16 == 0;
+    if (info) {
+        info->method = 2;
+        info->elems_per_cta = NE;
+        info->block_threads = S::BS;
+        info->shared_bytes = int(S::SMEM);
+        info->grid = grid;
+        info->bulk_path = fast_layout ? 1 : 0;
+        std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d%s", DIM, M - 1, prec_name(sizeof(R)),
+                      NE, SRC ? "_src" : "");
+        if (dry) fill_regs(kernel, info);
+    }
+    if (dry || p.n_elem == 0) return cudaSuccess;
+    p.fast_ok = fast_layout && aligned16(p.u) && aligned16(p.out);
+    if (int e = set_smem_attr(kernel, S::SMEM)) return cudaError_t(e);
+    kernel<<<dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <class R, int M, int NE, bool SRC>
+cudaError_t launch_planar(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
+    using S = PlanarShape<R, M, NE>;
+    auto kernel = hf_planar_kernel<R, M, NE, SRC>;
+    const long long grid = (p.n_elem + NE - 1) / NE;
+    if (info) {
+        info->method = 1;
+        info->elems_per_cta = NE;
+        info->block_threads = S::BS;
+        info->shared_bytes = int(S::SMEM);
+        info->grid = grid;
+        info->bulk_path = 0;
+        std::snprintf(info->name, sizeof(info->name), "hf_planar_d3_p%d_%s_ne%d%s", M - 1, prec_name(sizeof(R)), NE,
+                      SRC ? "_src" : "");
+        if (dry) fill_regs(kernel, info);
+    }
+    if (dry || p.n_elem == 0) return cudaSuccess;
+    if (int e = set_smem_attr(kernel, S::SMEM)) return cudaError_t(e);
+    kernel<<<dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <class R, int DIM, int M>
+cudaError_t launch_unfused(Params<R> p, bool src, cudaStream_t st, KInfo* info, bool dry) {
+    const long long groups = (p.n_elem + p.group - 1) / p.group;
+    if (info) {
+        info->method = 3;
+        info->elems_per_cta = p.group;
+        info->block_threads = kUnfusedBS;
+        info->shared_bytes = 0;
+        info->grid = groups;
+        info->bulk_path = 0;
+        std::snprintf(info->name, sizeof(info->name), "hf_flux+hf_div%s_d%d_p%d_%s", src ? "+hf_source" : "", DIM,
+                      M - 1, prec_name(sizeof(R)));
+        if (dry) fill_regs(hf_div_kernel<R, DIM, M>, info);
+    }
+    if (dry || p.n_elem == 0) return cudaSuccess;
+    hf_flux_kernel<R, DIM, M><<<dim3(unsigned(groups)), dim3(kUnfusedBS), 0, st>>>(p);
+    hf_div_kernel<R, DIM, M><<<dim3(unsigned(groups)), dim3(kUnfusedBS), 0, st>>>(p);
+    if (src) hf_source_kernel<R, DIM, M><<<dim3(unsigned(groups)), dim3(kUnfusedBS), 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+// Runtime -> template dispatch, defined per precision in hf_inst_*.cu.
+// Return cudaErrorInvalidValue (as an int) for an unsupported combination.
+template <class R>
+int run_lines(int d, int p, int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry);
+template <class R>
+int run_planar(int p, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry);
+template <class R>
+int run_unfused(int d, int p, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry);
+
+constexpr int kUnsupported = -1;
+
+}  // namespace hfb

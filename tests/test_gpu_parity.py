@@ -1,0 +1,170 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) vs the CPU oracle
+restatement (oracle/hexfuse_oracle.c, itself pinned bit-exactly to the
+reference).  Tolerances: 1e-12 relative for FP64 and 1e-5 for FP32 in the
+reference's field_rel_error metric (verify.hpp:19-35; BASELINE north star).
+Seeds and physical parameters follow acceptance.cpp:46-52 (seed 2024,
+nu = 1/1600) and test_oracle.cpp:134-165 (jac {1,0.5,2}, alternating source)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2107_14027_b200 import Method, PhysParams
+
+pytestmark = pytest.mark.gpu
+
+from gpu_util import PAR, check_parity, run_device  # noqa: E402
+
+
+def _field(d, p, n, group, fp32, seed):
+    return O.random_field(d, p, n, group, fp32, seed)
+
+
+# ---------------------------------------------------------------- lines (default) method, all orders
+@pytest.mark.parametrize("fp32", [False, True])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7])
+def test_lines_d3_random(cuda, p, fp32):
+    import paper_2107_14027_b200 as hf
+    g = hf.preferred_group(hf.make_problem(3, p, 1, 1, int(not fp32), PAR, method=Method.lines))
+    n = 3 * g + 1  # full bulk chunks plus a partial last group
+    for t, src in enumerate([False, True]):
+        U = _field(3, p, n, g, fp32, 2024 + t)
+        check_parity(3, p, n, g, fp32, U, with_source=src, method=Method.lines)
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_lines_d2_random(cuda, p, fp32):
+    import paper_2107_14027_b200 as hf
+    g = hf.preferred_group(hf.make_problem(2, p, 1, 1, int(not fp32), PAR, method=Method.lines))
+    n = 2 * g + 3
+    for t, src in enumerate([False, True]):
+        U = _field(2, p, n, g, fp32, 77 + t)
+        check_parity(2, p, n, g, fp32, U, with_source=src, jac=(1.0, 2.0, 0.0), method=Method.lines)
+
+
+# ---------------------------------------------------------------- non-unit metric (test_oracle.cpp:134-146)
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_nonunit_jac_fp64(cuda, p):
+    par = PhysParams(3e-3, 2.5, 1.0)
+    for t in range(3):
+        U = _field(3, p, 37, 4, False, 100 + 10 * p + t)
+        for method in (Method.lines, Method.planar, Method.unfused):
+            check_parity(3, p, 37, 4, False, U, params=par, jac=(1.0, 0.5, 2.0), with_source=(t % 2 == 0),
+                         method=method)
+
+
+# ---------------------------------------------------------------- every layout path of the lines kernel
+@pytest.mark.parametrize("group", [1, 2, 3, 5, 8, 16, 32, 64])
+def test_lines_groups_fp64_p3(cuda, group):
+    U = _field(3, 3, 70, group, False, 5)
+    check_parity(3, 3, 70, group, False, U, with_source=True, method=Method.lines)
+
+
+@pytest.mark.parametrize("group", [1, 4, 6, 16, 32, 48])
+def test_lines_groups_fp32_p4(cuda, group):
+    U = _field(3, 4, 50, group, True, 6)
+    check_parity(3, 4, 50, group, True, U, method=Method.lines)
+
+
+def test_lines_misaligned_pointer(cuda):
+    # a base pointer that is not 16-byte aligned must fall back to the guarded path
+    U = _field(3, 2, 64, 16, False, 9)
+    check_parity(3, 2, 64, 16, False, U, method=Method.lines, offset_bytes=8)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("p,fp32", [(1, True), (3, False), (4, True), (6, False)])
+def test_lines_variants(cuda, p, fp32, variant):
+    import paper_2107_14027_b200 as hf
+    pr = hf.make_problem(3, p, 1, 1, int(not fp32), PAR)
+    try:
+        info = hf.variant_info(pr, Method.lines, variant)
+    except hf.HexfuseInvalid:
+        pytest.skip("variant not instantiated for this order")
+    g = info["elems_per_cta"]
+    U = _field(3, p, 2 * g + 1, g, fp32, 11)
+    got = run_device(3, p, 2 * g + 1, g, fp32, U, method=Method.lines, variant=variant)
+    ref = O.oracle_divergence(3, p, 2 * g + 1, g, U, PAR.nu, PAR.zeta, PAR.T)
+    assert O.field_rel_error(3, p, 2 * g + 1, g, got, ref) <= (1e-5 if fp32 else 1e-12)
+
+
+# ---------------------------------------------------------------- planar method (d = 3)
+@pytest.mark.parametrize("fp32", [False, True])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6])
+def test_planar_random(cuda, p, fp32):
+    for t, src in enumerate([False, True]):
+        U = _field(3, p, 45, 32, fp32, 2024 + t)
+        check_parity(3, p, 45, 32, fp32, U, with_source=src, method=Method.planar)
+
+
+# ---------------------------------------------------------------- unfused comparator
+@pytest.mark.parametrize("d,p", [(3, 1), (3, 3), (3, 4), (3, 6), (2, 2), (2, 8)])
+@pytest.mark.parametrize("fp32", [False, True])
+def test_unfused_random(cuda, d, p, fp32):
+    for t, src in enumerate([False, True]):
+        U = _field(d, p, 40, 8, fp32, 31 + t)
+        check_parity(d, p, 40, 8, fp32, U, with_source=src, method=Method.unfused)
+
+
+# ---------------------------------------------------------------- deterministic vortex fixture (verify.hpp:85-91)
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("fp32", [False, True])
+def test_tgv_fixture(cuda, p, fp32):
+    import paper_2107_14027_b200 as hf
+    g = hf.preferred_group(hf.make_problem(3, p, 1, 1, int(not fp32), PAR))
+    n = 64
+    U = O.tgv_field(p, n, g, fp32)
+    for method in (Method.auto, Method.planar):
+        check_parity(3, p, n, g, fp32, U, method=method)
+
+
+# ---------------------------------------------------------------- analytic known answers (test_oracle.cpp:90-132)
+def test_constant_field_zero_divergence(cuda):
+    from gpu_util import padding_mask
+    d, p, n, g = 3, 2, 3, 2
+    U = np.zeros(O.field_words(d, p, n, g)).reshape(-1, 13, 27, g)
+    for v in range(13):
+        U[:, v, :, :] = 0.5 + 0.1 * v
+    U = U.reshape(-1)
+    real = padding_mask(d, p, n, g).reshape(-1, 13, 27, g)
+    for method in (Method.lines, Method.planar, Method.unfused):
+        got = run_device(d, p, n, g, False, U, method=method).reshape(-1, 13, 27, g)
+        assert np.max(np.abs(got[real])) < 1e-12
+        src = run_device(d, p, n, g, False, U, with_source=True, method=method).reshape(-1, 13, 27, g)
+        for v in range(13):
+            want = -(0.5 + 0.1 * v) if v >= 4 else 0.0
+            sel = src[:, v][real[:, v]]
+            assert np.max(np.abs(sel - want)) < 1e-12
+
+
+def test_linear_velocity_exact(cuda):
+    par = PhysParams(1e-2, 2.5, 0.5)
+    for p in (2, 3):
+        m = p + 1
+        nodes = O.gl_nodes(m)
+        U = np.zeros(O.field_words(3, p, 1, 1))
+        for k in range(m):
+            for j in range(m):
+                for i in range(m):
+                    U[i + m * j + m * m * k + m ** 3 * 1] = nodes[i]  # u = x
+        for method in (Method.lines, Method.planar, Method.unfused):
+            got = run_device(3, p, 1, 1, False, U, params=par, method=method)
+            for k in range(m):
+                for j in range(m):
+                    for i in range(m):
+                        pt = i + m * j + m * m * k
+                        assert abs(got[pt] - (-par.zeta)) < 1e-10 * par.zeta
+                        assert abs(got[pt + m ** 3] - (-2.0 * nodes[i])) < 1e-10
+                        assert abs(got[pt + 4 * m ** 3] - (1.0 / par.T)) < 1e-10 / par.T
+
+
+# ---------------------------------------------------------------- config 1 at full size (32768 x p3 fp64)
+def test_config1_full_oracle(cuda):
+    """BASELINE config 1: d=3 p=3 FP64, 32768 elements, seed 2024, the whole field vs the oracle."""
+    import paper_2107_14027_b200 as hf
+    g = hf.preferred_group(hf.make_problem(3, 3, 1, 1, 1, PAR))
+    U = _field(3, 3, 32768, g, False, 2024)
+    err = check_parity(3, 3, 32768, g, False, U, with_source=False)
+    assert err <= 1e-12
+    err = check_parity(3, 3, 32768, g, False, U, with_source=True)
+    assert err <= 1e-12

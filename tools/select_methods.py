@@ -1,0 +1,133 @@
+"""Measure every fused method/variant per (d, p, precision) on the GPU and emit
+the selection table (paper_2107_14027_b200/csrc/hf_select_table.inc).
+
+This replaces the reference's static preset_table (presets.hpp:25-37), which
+encodes Titan V measurements, with B200 measurements: for each configuration
+the method/variant with the highest achieved HBM bandwidth wins (ties within
+2% go to the lines method, whose shared-memory footprint is smaller).
+
+Usage (on a GPU box):
+    python tools/select_methods.py --points 1e7 --out gpurun_out/select.jsonl [--write-table]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2107_14027_b200 as hf  # noqa: E402
+from paper_2107_14027_b200 import Method, PhysParams, Precision  # noqa: E402
+
+PAR = PhysParams(1.0 / 1600.0, 2.5, 1.0)
+
+
+def time_launch(fn, iters=20, warmup=3):
+    st = torch.cuda.current_stream()
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        fn()
+        b.record(st)
+        b.synchronize()
+        ts.append(a.elapsed_time(b) * 1e-3)
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def measure(d, p, prec, method, variant, points, src=False):
+    pr0 = hf.make_problem(d, p, 1, 1, prec, PAR, method=method)
+    if method == Method.unfused:
+        group = 32
+        info = {"elems_per_cta": group, "name": f"unfused_d{d}_p{p}"}
+    else:
+        info = hf.variant_info(pr0, method, variant)
+        group = info["elems_per_cta"]
+    npt = (p + 1) ** d
+    n_elem = max(group, int(round(points / npt / group)) * group)
+    pr = hf.make_problem(d, p, n_elem, group, prec, PAR, with_source=src, method=method)
+    words = hf.field_words(pr)
+    dt = torch.float32 if prec == Precision.fp32 else torch.float64
+    u = torch.rand(words, dtype=dt, device="cuda") * 2 - 1
+    o = torch.empty_like(u)
+    if method == Method.unfused:
+        ws = torch.empty(hf.unfused_workspace_bytes(pr) // u.element_size(), dtype=dt, device="cuda")
+        fn = lambda: hf.unfused_divergence_device(pr, u, o, ws)  # noqa: E731
+    else:
+        fn = lambda: hf.fused_divergence_variant(pr, method, variant, u, o)  # noqa: E731
+    t = time_launch(fn)
+    pts = n_elem * npt
+    alg = pts * 2 * hf.n_vars(d) * (4 if prec == Precision.fp32 else 8)
+    del u, o
+    return {"d": d, "p": p, "precision": prec.name, "method": method.name, "variant": variant, "src": src,
+            "n_elem": n_elem, "group": group, "points": pts, "seconds": t, "gdofs": pts / t / 1e9,
+            "alg_GBps": alg / t / 1e9, "kernel": info.get("name"), "smem": info.get("shared_bytes"),
+            "regs": info.get("registers"), "block": info.get("block_threads")}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--points", type=float, default=1e7)
+    ap.add_argument("--dims", default="3,2")
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--write-table", action="store_true")
+    ap.add_argument("--no-unfused", action="store_true")
+    args = ap.parse_args()
+    rows = []
+    fh = open(args.out, "w") if args.out else None
+    for d in [int(x) for x in args.dims.split(",")]:
+        pmax = 6 if d == 3 else 8
+        for prec in (Precision.fp32, Precision.fp64):
+            for p in range(1, pmax + 1):
+                cands = [(Method.lines, v) for v in (0, 1, 2)]
+                if d == 3:
+                    cands.append((Method.planar, 0))
+                if not args.no_unfused:
+                    cands.append((Method.unfused, 0))
+                for method, variant in cands:
+                    try:
+                        r = measure(d, p, prec, method, variant, args.points)
+                    except hf.HexfuseInvalid:
+                        continue
+                    rows.append(r)
+                    line = json.dumps(r)
+                    print(line, flush=True)
+                    if fh:
+                        fh.write(line + "\n")
+                        fh.flush()
+    if args.write_table:
+        best = {}
+        for r in rows:
+            if r["method"] == "unfused":
+                continue
+            key = (r["d"], r["p"], r["precision"])
+            cur = best.get(key)
+            score = r["alg_GBps"] * (1.02 if r["method"] == "lines" else 1.0)
+            if cur is None or score > cur[0]:
+                best[key] = (score, r)
+        path = os.path.join(ROOT, "paper_2107_14027_b200", "csrc", "hf_select_table.inc")
+        with open(path, "w") as f:
+            f.write("// hf_select_table.inc -- measured method selection (replaces the reference's\n"
+                    "// preset_table, presets.hpp:25-37, and default_lines_n, presets.hpp:86-103).\n"
+                    "//\n// Row: { d, p, precision(0=fp32,1=fp64), method(1=planar,2=lines), variant }.\n"
+                    "// Generated by tools/select_methods.py from on-GPU measurements (achieved\n"
+                    f"// HBM GB/s at ~{args.points:.0e} points per configuration).\n")
+            for (d, p, prec), (_, r) in sorted(best.items()):
+                m = 1 if r["method"] == "planar" else 2
+                f.write(f"    {{{d}, {p}, {0 if prec == 'fp32' else 1}, {m}, {r['variant']}}},"
+                        f"  // {r['kernel']}: {r['alg_GBps']:.0f} GB/s, {r['gdofs']:.2f} GDoF/s\n")
+        print("wrote", path)
+
+
+if __name__ == "__main__":
+    main()
