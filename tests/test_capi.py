@@ -1,0 +1,128 @@
+"""CPU: the C-ABI library loads, exports every symbol include/hexfuse_b200.h
+declares, and its host-only functions (layout, validation, operators,
+selection, partition) agree with the oracle.  No kernel launches here."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2107_14027_b200 as hf
+from paper_2107_14027_b200 import HexfuseInvalid, Method, PhysParams, Precision, _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "hexfuse_b200.h")
+
+
+def header_symbols():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"HF_API\s+[\w\s\*]+?\b(hf_\w+)\s*\(", txt)))
+
+
+def test_header_symbols_are_exported():
+    syms = header_symbols()
+    assert len(syms) >= 15
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (hf_\w+)", out))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, f"declared but not exported: {missing}"
+    assert sorted(_lib.EXPORTED) == syms
+    L = _lib.load()
+    for s in syms:
+        assert hasattr(L, s)
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    arches = set(re.findall(r"sm_(\d+a?)", out))
+    assert arches == {"100a"}, arches
+
+
+def test_no_torch_in_the_abi():
+    code = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)  # declarations only
+    assert "torch" not in code.lower()
+    assert "std::" not in code and "template" not in code
+
+
+@pytest.mark.parametrize("d,p,g,n", [(3, 1, 1, 5), (3, 3, 8, 17), (3, 6, 2, 3), (2, 8, 16, 33), (2, 4, 3, 10)])
+def test_field_words_and_offsets(d, p, g, n):
+    pr = hf.make_problem(d, p, n, g, Precision.fp64, PhysParams())
+    assert hf.field_words(pr) == O.field_words(d, p, n, g)
+    L = _lib.load()
+    m = p + 1
+    for e in range(n):
+        for v in (0, 1, 1 + d + d * d - 1):
+            for (i, j, k) in [(0, 0, 0), (m - 1, 0, m - 1 if d == 3 else 0), (1 % m, m - 1, 0)]:
+                assert L.hf_offset(C.byref(pr), e, i, j, k, v) == O.lib().hfo_offset(d, p, g, e, i, j, k, v)
+
+
+def test_validation_mirrors_reference_errors():
+    base = dict(d=3, p=3, n_elem=10, group=4, precision=Precision.fp64, params=PhysParams())
+    for kw, msg in [({"d": 4}, "d must"), ({"p": 0}, "p must"), ({"p": 8}, "p must"), ({"group": 0}, "group"),
+                    ({"params": PhysParams(nu=-1)}, "nu"), ({"params": PhysParams(zeta=0)}, "zeta"),
+                    ({"params": PhysParams(T=0)}, "T must")]:
+        a = dict(base)
+        a.update(kw)
+        pr = hf.make_problem(a["d"], a["p"], a["n_elem"], a["group"], a["precision"], a["params"])
+        with pytest.raises(HexfuseInvalid, match=msg):
+            hf.validate(pr)
+    pr = hf.make_problem(2, 8, 10, 4, Precision.fp32, PhysParams())  # d=2 p=8 is supported (unpinned)
+    hf.validate(pr)
+    pr = hf.make_problem(2, 3, 10, 4, Precision.fp32, PhysParams(), method=Method.planar)
+    with pytest.raises(HexfuseInvalid, match="planar"):
+        hf.validate(pr)  # the reference's planar generator rejects d=2 (codegen_planar.hpp:102)
+
+
+def test_derivative_matrix_bitexact_vs_oracle():
+    for m in range(2, 10):
+        x, D = hf.derivative_matrix(m)
+        assert np.array_equal(x, O.gl_nodes(m))
+        assert np.array_equal(D, O.derivative_matrix(x))
+
+
+def test_selection_and_kernel_info_without_device():
+    for d, pmax in ((3, 7), (2, 8)):
+        for p in range(1, pmax + 1):
+            for prec in (Precision.fp32, Precision.fp64):
+                pr = hf.make_problem(d, p, 1000, 1, prec, PhysParams())
+                meth = hf.selected_method(pr)
+                assert meth in (Method.lines, Method.planar)
+                info = hf.kernel_info(pr)
+                g = hf.preferred_group(pr)
+                assert g == info["elems_per_cta"] >= 1
+                assert info["shared_bytes"] <= 227 * 1024
+                assert info["block_threads"] % 32 == 0
+                w = 4 if prec == Precision.fp32 else 8
+                assert (g * w) % 16 == 0, "preferred group must allow 16-byte bulk rows"
+                pr2 = hf.make_problem(d, p, 1000, g, prec, PhysParams())
+                assert hf.kernel_info(pr2)["bulk_path"]
+
+
+def test_algorithmic_bytes():
+    L = _lib.load()
+    pr = hf.make_problem(3, 3, 1, 1, Precision.fp64, PhysParams())
+    assert L.hf_algorithmic_bytes_per_point(C.byref(pr)) == 208
+    pr = hf.make_problem(3, 3, 1, 1, Precision.fp32, PhysParams())
+    assert L.hf_algorithmic_bytes_per_point(C.byref(pr)) == 104
+    pr = hf.make_problem(2, 3, 1, 1, Precision.fp32, PhysParams())
+    assert L.hf_algorithmic_bytes_per_point(C.byref(pr)) == 56
+
+
+@pytest.mark.parametrize("n,g,parts", [(1000, 8, 1), (1000, 8, 2), (1001, 8, 4), (7, 4, 8), (2343750, 8, 8)])
+def test_partition_covers_every_element_once(n, g, parts):
+    pr = hf.make_problem(3, 3, n, g, Precision.fp64, PhysParams())
+    gw = g * 64 * 13
+    nxt = 0
+    for r in range(parts):
+        e0, ne, wo = hf.partition(pr, parts, r)
+        assert e0 == nxt and e0 % g == 0 and wo == (e0 // g) * gw
+        nxt = e0 + ne
+    assert nxt == n
+
+
+def test_unfused_workspace_bytes():
+    pr = hf.make_problem(3, 4, 100, 8, Precision.fp32, PhysParams())
+    assert hf.unfused_workspace_bytes(pr) == hf.field_words(pr) * 3 * 4
