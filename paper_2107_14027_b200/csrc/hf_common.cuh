@@ -30,6 +30,8 @@ struct Params {
     R* __restrict__ ws;       // unfused only: flux workspace
     long long n_elem;
     long long group_words;    // group * m^d * n_v
+    long long chunk0;         // first chunk (of NE elements) this launch covers
+    long long n_chunks;       // pipelined kernel: number of full chunks to process
     int group;
     int fast_ok;              // host-verified: bulk-copy alignment holds for full chunks
 };
@@ -65,6 +67,15 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// named barrier over a subset of the CTA's warps (id 1..15; 0 is __syncthreads)
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 // global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0, both ends 16B aligned)

@@ -18,12 +18,31 @@ int lines_variant(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, 
     }
 }
 
+template <class R, int DIM, int M, int VARIANT>
+int pipe_variant(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
+    constexpr int NE = pipe_ne<R, DIM, M, VARIANT>();
+    constexpr int ST = pipe_stages<VARIANT>();
+    if constexpr (NE == 0) {
+        return kUnsupported;
+    } else if constexpr (PipeShape<R, DIM, M, NE, ST>::SMEM > size_t(kMaxSmemPerCta) ||
+                         PipeShape<R, DIM, M, NE, ST>::BS > 1024) {
+        return kUnsupported;
+    } else {
+        return src ? int(launch_lines_pipe<R, DIM, M, NE, ST, true>(prm, st, info, dry))
+                   : int(launch_lines_pipe<R, DIM, M, NE, ST, false>(prm, st, info, dry));
+    }
+}
+
 template <class R, int DIM, int M>
 int lines_m(int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
     switch (variant) {
         case 0: return lines_variant<R, DIM, M, 0>(src, prm, st, info, dry);
         case 1: return lines_variant<R, DIM, M, 1>(src, prm, st, info, dry);
         case 2: return lines_variant<R, DIM, M, 2>(src, prm, st, info, dry);
+        case 3: return pipe_variant<R, DIM, M, 3>(src, prm, st, info, dry);
+        case 4: return pipe_variant<R, DIM, M, 4>(src, prm, st, info, dry);
+        case 5: return pipe_variant<R, DIM, M, 5>(src, prm, st, info, dry);
+        case 6: return pipe_variant<R, DIM, M, 6>(src, prm, st, info, dry);
         default: return kUnsupported;
     }
 }

@@ -15,6 +15,7 @@
 
 #include "hf_common.cuh"
 #include "hf_lines.cuh"
+#include "hf_lines_pipe.cuh"
 #include "hf_planar.cuh"
 #include "hf_unfused.cuh"
 
@@ -56,6 +57,20 @@ constexpr int lines_ne() {
         return (LinesShape<R, DIM, M, ne>::SMEM <= size_t(kMaxSmemPerCta) && ne * ipow_c(M, DIM - 1) <= 1024) ? ne
                                                                                                             : 0;
     } else return ne0;
+}
+
+// Pipelined (persistent, warp-specialised) lines variants 3..6:
+//   3: NE0, 2 stages   4: NE0/2, 3 stages   5: NE0/2, 2 stages   6: NE0, 3 stages
+template <class R, int DIM, int M, int VARIANT>
+constexpr int pipe_ne() {
+    constexpr int ne0 = lines_ne_default<R, DIM, M>();
+    constexpr int min_ne = 16 / int(sizeof(R));
+    constexpr int ne = (VARIANT == 3 || VARIANT == 6) ? ne0 : ne0 / 2;
+    return ne >= min_ne ? ne : 0;
+}
+template <int VARIANT>
+constexpr int pipe_stages() {
+    return (VARIANT == 4 || VARIANT == 6) ? 3 : 2;
 }
 
 template <class R, int M>
@@ -111,6 +126,67 @@ cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
     if (int e = set_smem_attr(kernel, S::SMEM)) return cudaError_t(e);
     kernel<<<dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st>>>(p);
     return cudaGetLastError();
+}
+
+inline int num_sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) ==
+                                                      cudaSuccess)
+            return v;
+        cudaGetLastError();
+        return 148;
+    }();
+    return n;
+}
+
+// Persistent pipelined lines kernel over the whole chunks, guarded tail through hf_lines_kernel.
+template <class R, int DIM, int M, int NE, int STAGES, bool SRC>
+cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
+    using S = PipeShape<R, DIM, M, NE, STAGES>;
+    using L = LinesShape<R, DIM, M, NE>;
+    auto kernel = hf_lines_pipe_kernel<R, DIM, M, NE, STAGES, SRC>;
+    const bool fast_layout = (p.group % NE == 0) && ((long long)p.group * sizeof(R)) % 16 == 0;
+    const long long n_full = p.n_elem / NE;
+    static int blocks_per_sm = -1;
+    if (blocks_per_sm < 0 && !dry) {
+        if (int e = set_smem_attr(kernel, S::SMEM)) return cudaError_t(e);
+        int b = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, S::BS, S::SMEM) != cudaSuccess || b < 1) {
+            cudaGetLastError();
+            b = 1;
+        }
+        blocks_per_sm = b;
+    }
+    const long long slots = (long long)(blocks_per_sm > 0 ? blocks_per_sm : 1) * num_sms();
+    const long long grid = n_full < slots ? n_full : slots;
+    if (info) {
+        info->method = 2;
+        info->elems_per_cta = NE;
+        info->block_threads = S::BS;
+        info->shared_bytes = int(S::SMEM);
+        info->grid = grid;
+        info->bulk_path = fast_layout ? 1 : 0;
+        std::snprintf(info->name, sizeof(info->name), "hf_lines_pipe_d%d_p%d_%s_ne%d_s%d%s", DIM, M - 1,
+                      prec_name(sizeof(R)), NE, STAGES, SRC ? "_src" : "");
+        if (dry) fill_regs(kernel, info);
+    }
+    if (dry || p.n_elem == 0) return cudaSuccess;
+    p.fast_ok = fast_layout && aligned16(p.u) && aligned16(p.out);
+    if (!p.fast_ok || n_full == 0) return launch_lines<R, DIM, M, NE, SRC>(p, st, nullptr, false);
+    p.chunk0 = 0;
+    p.n_chunks = n_full;
+    kernel<<<dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st>>>(p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (n_full * NE < p.n_elem) {  // guarded partial chunk
+        auto tail = hf_lines_kernel<R, DIM, M, NE, SRC>;
+        if (int e2 = set_smem_attr(tail, L::SMEM)) return cudaError_t(e2);
+        p.chunk0 = n_full;
+        tail<<<1, L::BS, L::SMEM, st>>>(p);
+        e = cudaGetLastError();
+    }
+    return e;
 }
 
 template <class R, int M, int NE, bool SRC>

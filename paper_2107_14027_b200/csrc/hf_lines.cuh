@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE>::BS)
     R* acc = s + S::IN_WORDS;
 
     const int tid = threadIdx.x;
-    const long long E0 = static_cast<long long>(blockIdx.x) * NE;
+    const long long E0 = (p.chunk0 + static_cast<long long>(blockIdx.x)) * NE;
     const bool fast = p.fast_ok && (E0 + NE <= p.n_elem);
     const long long grp = E0 / p.group;
     const int el0 = static_cast<int>(E0 - grp * p.group);

@@ -72,20 +72,41 @@ def test_lines_misaligned_pointer(cuda):
     check_parity(3, 2, 64, 16, False, U, method=Method.lines, offset_bytes=8)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
-@pytest.mark.parametrize("p,fp32", [(1, True), (3, False), (4, True), (6, False)])
-def test_lines_variants(cuda, p, fp32, variant):
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("d,p,fp32", [(3, 1, True), (3, 3, False), (3, 4, True), (3, 6, False), (3, 6, True),
+                                      (2, 3, True), (2, 8, True)])
+def test_lines_variants(cuda, d, p, fp32, variant):
+    """Every lines variant (3..6 = persistent TMA-ring kernel), bulk chunks + guarded tail, +-source."""
     import paper_2107_14027_b200 as hf
-    pr = hf.make_problem(3, p, 1, 1, int(not fp32), PAR)
+    pr = hf.make_problem(d, p, 1, 1, int(not fp32), PAR)
     try:
         info = hf.variant_info(pr, Method.lines, variant)
     except hf.HexfuseInvalid:
         pytest.skip("variant not instantiated for this order")
     g = info["elems_per_cta"]
-    U = _field(3, p, 2 * g + 1, g, fp32, 11)
-    got = run_device(3, p, 2 * g + 1, g, fp32, U, method=Method.lines, variant=variant)
-    ref = O.oracle_divergence(3, p, 2 * g + 1, g, U, PAR.nu, PAR.zeta, PAR.T)
-    assert O.field_rel_error(3, p, 2 * g + 1, g, got, ref) <= (1e-5 if fp32 else 1e-12)
+    for n, group, src in [(5 * g + 1, g, False), (7 * g, 2 * g, True), (3 * g + 2, 4 * g, True)]:
+        U = _field(d, p, n, group, fp32, 11 + n)
+        got = run_device(d, p, n, group, fp32, U, method=Method.lines, variant=variant, with_source=src)
+        ref = O.oracle_divergence(d, p, n, group, U, PAR.nu, PAR.zeta, PAR.T, (1.0, 1.0, 1.0), src)
+        err = O.field_rel_error(d, p, n, group, got, ref)
+        assert err <= (1e-5 if fp32 else 1e-12), (n, group, src, err)
+
+
+def test_pipe_many_chunks_per_cta(cuda):
+    """More chunks than resident CTAs: every CTA cycles its stage ring several times."""
+    import paper_2107_14027_b200 as hf
+    for fp32, p in [(False, 3), (True, 5)]:
+        pr = hf.make_problem(3, p, 1, 1, int(not fp32), PAR)
+        for variant in (3, 4, 5, 6):
+            try:
+                g = hf.variant_info(pr, Method.lines, variant)["elems_per_cta"]
+            except hf.HexfuseInvalid:
+                continue
+            n = g * 148 * 9 + 3
+            U = _field(3, p, n, g, fp32, 5)
+            got = run_device(3, p, n, g, fp32, U, method=Method.lines, variant=variant)
+            ref = O.oracle_divergence(3, p, n, g, U, PAR.nu, PAR.zeta, PAR.T)
+            assert O.field_rel_error(3, p, n, g, got, ref) <= (1e-5 if fp32 else 1e-12)
 
 
 # ---------------------------------------------------------------- planar method (d = 3)

@@ -19,7 +19,6 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-import torch  # noqa: E402
 
 import paper_2107_14027_b200 as hf  # noqa: E402
 from paper_2107_14027_b200 import Method, PhysParams, Precision  # noqa: E402
@@ -28,6 +27,7 @@ PAR = PhysParams(1.0 / 1600.0, 2.5, 1.0)
 
 
 def time_launch(fn, iters=20, warmup=3):
+    import torch
     st = torch.cuda.current_stream()
     for _ in range(warmup):
         fn()
@@ -56,6 +56,7 @@ def measure(d, p, prec, method, variant, points, src=False):
     npt = (p + 1) ** d
     n_elem = max(group, int(round(points / npt / group)) * group)
     pr = hf.make_problem(d, p, n_elem, group, prec, PAR, with_source=src, method=method)
+    import torch
     words = hf.field_words(pr)
     dt = torch.float32 if prec == Precision.fp32 else torch.float64
     u = torch.rand(words, dtype=dt, device="cuda") * 2 - 1
@@ -82,14 +83,18 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--write-table", action="store_true")
     ap.add_argument("--no-unfused", action="store_true")
+    ap.add_argument("--from-files", nargs="*", default=None, help="write the table from saved jsonl rows")
     args = ap.parse_args()
+    if args.from_files:
+        table_from_files(args.from_files)
+        return
     rows = []
     fh = open(args.out, "w") if args.out else None
     for d in [int(x) for x in args.dims.split(",")]:
         pmax = 6 if d == 3 else 8
         for prec in (Precision.fp32, Precision.fp64):
             for p in range(1, pmax + 1):
-                cands = [(Method.lines, v) for v in (0, 1, 2)]
+                cands = [(Method.lines, v) for v in (0, 1, 2, 3, 4, 5, 6)]
                 if d == 3:
                     cands.append((Method.planar, 0))
                 if not args.no_unfused:
@@ -106,27 +111,42 @@ def main():
                         fh.write(line + "\n")
                         fh.flush()
     if args.write_table:
-        best = {}
-        for r in rows:
-            if r["method"] == "unfused":
-                continue
-            key = (r["d"], r["p"], r["precision"])
-            cur = best.get(key)
-            score = r["alg_GBps"] * (1.02 if r["method"] == "lines" else 1.0)
-            if cur is None or score > cur[0]:
-                best[key] = (score, r)
-        path = os.path.join(ROOT, "paper_2107_14027_b200", "csrc", "hf_select_table.inc")
-        with open(path, "w") as f:
-            f.write("// hf_select_table.inc -- measured method selection (replaces the reference's\n"
-                    "// preset_table, presets.hpp:25-37, and default_lines_n, presets.hpp:86-103).\n"
-                    "//\n// Row: { d, p, precision(0=fp32,1=fp64), method(1=planar,2=lines), variant }.\n"
-                    "// Generated by tools/select_methods.py from on-GPU measurements (achieved\n"
-                    f"// HBM GB/s at ~{args.points:.0e} points per configuration).\n")
-            for (d, p, prec), (_, r) in sorted(best.items()):
-                m = 1 if r["method"] == "planar" else 2
-                f.write(f"    {{{d}, {p}, {0 if prec == 'fp32' else 1}, {m}, {r['variant']}}},"
-                        f"  // {r['kernel']}: {r['alg_GBps']:.0f} GB/s, {r['gdofs']:.2f} GDoF/s\n")
-        print("wrote", path)
+        write_table(rows, args.points)
+
+
+def write_table(rows, points):
+    best = {}
+    for r in rows:
+        if r["method"] == "unfused":
+            continue
+        key = (r["d"], r["p"], r["precision"])
+        cur = best.get(key)
+        score = r["alg_GBps"] * (1.02 if r["method"] == "lines" else 1.0)
+        if cur is None or score > cur[0]:
+            best[key] = (score, r)
+    path = os.path.join(ROOT, "paper_2107_14027_b200", "csrc", "hf_select_table.inc")
+    with open(path, "w") as f:
+        f.write("// hf_select_table.inc -- measured method selection (replaces the reference's\n"
+                "// preset_table, presets.hpp:25-37, and default_lines_n, presets.hpp:86-103).\n"
+                "//\n// Row: { d, p, precision(0=fp32,1=fp64), method(1=planar,2=lines), variant }.\n"
+                "// lines variants: 0/1/2 = one chunk per CTA with NE0, NE0/2, 2*NE0 elements;\n"
+                "// 3..6 = persistent TMA-ring kernel (3: NE0 x2 stages, 4: NE0/2 x3, 5: NE0/2 x2, 6: NE0 x3).\n"
+                "// Generated by tools/select_methods.py from on-GPU measurements (achieved\n"
+                f"// HBM GB/s, median of 20 launches at ~{points:.0e} points per configuration;\n"
+                "// raw rows in profiles/select_r01_*.jsonl).\n")
+        for (d, p, prec), (_, r) in sorted(best.items()):
+            m = 1 if r["method"] == "planar" else 2
+            f.write(f"    {{{d}, {p}, {0 if prec == 'fp32' else 1}, {m}, {r['variant']}}},"
+                    f"  // {r['kernel']}: {r['alg_GBps']:.0f} GB/s, {r['gdofs']:.2f} GDoF/s\n")
+    print("wrote", path)
+
+
+def table_from_files(paths):
+    rows = []
+    for pth in paths:
+        with open(pth) as fh:
+            rows += [json.loads(x) for x in fh if x.strip()]
+    write_table(rows, rows[0]["points"] if rows else 1e7)
 
 
 if __name__ == "__main__":
