@@ -1,0 +1,119 @@
+// hexfuse_b200.hpp -- header-only C++ adapter that makes the B200 kernels a
+// drop-in for the reference's host entry point
+//
+//     StateField hexfuse::oracle_divergence(const StateField& U, const PhysParams& params,
+//                                           const std::array<double, 3>& jac, bool with_source);
+//     (/root/reference/proj/include/hexfuse/oracle.hpp:20-21)
+//
+// as
+//
+//     StateField hexfuse_b200::fused_divergence_b200(U, params, jac, with_source [, method]);
+//
+// It is templated on the caller's StateField / PhysParams types so it binds to
+// the reference's own structs (layout.hpp:104-153, equations.hpp:14-24) without
+// this repository including -- or copying -- any reference header.  Required
+// members, exactly the reference's: U.d, U.p, U.n_elem, U.group, U.precision
+// (enum whose first enumerator is fp32, core.hpp:10), U.data (std::vector<double>);
+// params.nu, params.zeta, params.T, params.validate().
+//
+// Semantics match the reference: the result is a copy of U's shape and group,
+// zeroed, then filled (oracle.hpp:26-27); FP32 fields cross the ABI as float,
+// converted exactly as export_blob does (layout.hpp:166-170); invalid input
+// throws std::invalid_argument, device failures throw std::runtime_error.
+#pragma once
+
+#include <algorithm>
+#include <array>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hexfuse_b200.h"
+
+namespace hexfuse_b200 {
+
+namespace detail {
+
+struct ContextDeleter {
+    void operator()(hf_context* c) const { hf_context_destroy(c); }
+};
+
+// One host-path context per thread (device 0 unless set_device() was called).
+inline int& thread_device() {
+    thread_local int dev = 0;
+    return dev;
+}
+
+inline hf_context* thread_context() {
+    thread_local std::unique_ptr<hf_context, ContextDeleter> ctx;
+    thread_local int ctx_dev = -1;
+    if (!ctx || ctx_dev != thread_device()) {
+        ctx.reset(hf_context_create(thread_device()));
+        ctx_dev = thread_device();
+        if (!ctx) throw std::runtime_error(std::string("hf_context_create: ") + hf_last_error());
+    }
+    return ctx.get();
+}
+
+inline void check(int rc, const char* what) {
+    if (rc == HF_OK) return;
+    const std::string msg = std::string(what) + ": " + hf_last_error();
+    if (rc == HF_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+}  // namespace detail
+
+inline void set_device(int device) { detail::thread_device() = device; }
+
+template <class StateField, class PhysParams>
+hf_problem make_problem(const StateField& U, const PhysParams& params, const std::array<double, 3>& jac,
+                        bool with_source, int method = HF_METHOD_AUTO) {
+    hf_problem pr{};
+    pr.d = U.d;
+    pr.p = U.p;
+    pr.n_elem = U.n_elem;
+    pr.group = U.group;
+    pr.precision = static_cast<int>(U.precision) == 0 ? HF_FP32 : HF_FP64;  // Precision{fp32, fp64}
+    pr.nu = params.nu;
+    pr.zeta = params.zeta;
+    pr.T = params.T;
+    pr.jac[0] = jac[0];
+    pr.jac[1] = jac[1];
+    pr.jac[2] = jac[2];
+    pr.with_source = with_source ? 1 : 0;
+    pr.method = method;
+    return pr;
+}
+
+// Drop-in for hexfuse::oracle_divergence (oracle.hpp:20-62) on the B200.
+template <class StateField, class PhysParams>
+StateField fused_divergence_b200(const StateField& U, const PhysParams& params, const std::array<double, 3>& jac,
+                                 bool with_source, int method = HF_METHOD_AUTO) {
+    params.validate();
+    const hf_problem pr = make_problem(U, params, jac, with_source, method);
+    detail::check(hf_validate(&pr), "fused_divergence_b200");
+    StateField out = U;
+    std::fill(out.data.begin(), out.data.end(), 0.0);
+    if (U.n_elem == 0) return out;
+    if (static_cast<int64_t>(U.data.size()) != hf_field_words(&pr))
+        throw std::invalid_argument("fused_divergence_b200: field storage does not match its shape");
+    hf_context* ctx = detail::thread_context();
+    if (pr.precision == HF_FP32) {
+        std::vector<float> in(U.data.size()), res(U.data.size());
+        std::transform(U.data.begin(), U.data.end(), in.begin(), [](double x) { return static_cast<float>(x); });
+        detail::check(hf_fused_divergence_host(ctx, &pr, in.data(), res.data()), "fused_divergence_b200");
+        std::transform(res.begin(), res.end(), out.data.begin(), [](float x) { return static_cast<double>(x); });
+    } else {
+        detail::check(hf_fused_divergence_host(ctx, &pr, U.data.data(), out.data.data()), "fused_divergence_b200");
+    }
+    return out;
+}
+
+// Device-buffer form (the rendered kernel's (n_elements, u, divf) contract, render.hpp:79-80).
+inline void fused_divergence_device(const hf_problem& pr, const void* u_dev, void* divf_dev, void* stream = nullptr) {
+    detail::check(hf_fused_divergence(&pr, u_dev, divf_dev, stream), "hf_fused_divergence");
+}
+
+}  // namespace hexfuse_b200
