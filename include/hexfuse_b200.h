@@ -84,6 +84,7 @@ typedef struct hf_kernel_info {
     int registers;       /* per thread, from cudaFuncGetAttributes (0 if no device) */
     int64_t grid;        /* CTAs for this problem                        */
     int bulk_path;       /* 1 if full chunks stage through cp.async.bulk */
+    int blocks_per_sm;   /* resident CTAs per SM (cudaOccupancy...; 0 if no device) */
     char name[96];
 } hf_kernel_info;
 

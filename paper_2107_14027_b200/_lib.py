@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libhexfuse_b200.so")
+LIB_PATH = os.environ.get("HEXFUSE_B200_LIB") or os.path.join(_HERE, "lib", "libhexfuse_b200.so")
 
 HF_OK, HF_ERUNTIME, HF_EINVAL = 0, 1, 2
 HF_FP32, HF_FP64 = 0, 1
@@ -42,6 +42,7 @@ class hf_kernel_info(C.Structure):
         ("registers", C.c_int),
         ("grid", C.c_int64),
         ("bulk_path", C.c_int),
+        ("blocks_per_sm", C.c_int),
         ("name", C.c_char * 96),
     ]
 

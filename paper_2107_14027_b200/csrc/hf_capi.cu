@@ -157,7 +157,16 @@ hfb::Params<R> make_params(const hf_problem* pr, const void* u, void* out, void*
     hfb::Params<R> p;
     std::memset(&p, 0, sizeof(p));
     const int m = pr->p + 1;
-    for (int i = 0; i < m * m; ++i) p.D[i] = R(ops().D[m][i]);
+    const double* D = ops().D[m];
+    for (int i = 0; i < m * m; ++i) p.D[i] = R(D[i]);
+    const int h = m / 2;
+    for (int i = 0; i <= h && i < hfb::kMaxH; ++i) {
+        for (int t = 0; t < h; ++t) {
+            p.DE[i * hfb::kMaxH + t] = R(0.5 * (D[i * m + t] + D[i * m + (m - 1 - t)]));
+            p.DO[i * hfb::kMaxH + t] = R(0.5 * (D[i * m + t] - D[i * m + (m - 1 - t)]));
+        }
+        p.DC[i] = (m % 2 == 1) ? R(D[i * m + h]) : R(0);
+    }
     p.nu = R(pr->nu);
     p.zeta = R(pr->zeta);
     p.invT = R(1.0 / pr->T);
@@ -171,6 +180,7 @@ hfb::Params<R> make_params(const hf_problem* pr, const void* u, void* out, void*
     p.n_elem = pr->n_elem;
     p.group = pr->group;
     p.group_words = int64_t(pr->group) * ipow64(m, pr->d) * (1 + pr->d + pr->d * pr->d);
+    p.total_words = ((pr->n_elem + pr->group - 1) / pr->group) * p.group_words;
     p.fast_ok = 0;
     return p;
 }
@@ -262,6 +272,7 @@ int hf_kernel_info_get(const hf_problem* pr, hf_kernel_info* out) {
     out->registers = ki.registers;
     out->grid = ki.grid;
     out->bulk_path = ki.bulk_path;
+    out->blocks_per_sm = ki.blocks_per_sm;
     std::memcpy(out->name, ki.name, sizeof(out->name));
     return HF_OK;
 }
@@ -322,6 +333,7 @@ HF_API int hf_fused_divergence_variant(const hf_problem* pr, int method, int var
         info->registers = ki.registers;
         info->grid = ki.grid;
         info->bulk_path = ki.bulk_path;
+        info->blocks_per_sm = ki.blocks_per_sm;
         std::memcpy(info->name, ki.name, sizeof(info->name));
     }
     return HF_OK;

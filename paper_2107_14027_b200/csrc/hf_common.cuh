@@ -10,6 +10,7 @@
 namespace hfb {
 
 constexpr int kMaxM = 9;  // m = p+1 <= 9 (d=2 p=8)
+constexpr int kMaxH = 5;  // rows of the even-odd split: i <= m/2
 
 __host__ __device__ constexpr int ipow_c(int b, int e) { return e == 0 ? 1 : b * ipow_c(b, e - 1); }
 __host__ __device__ constexpr int n_vars_c(int d) { return 1 + d + d * d; }
@@ -22,6 +23,13 @@ __host__ __device__ constexpr int var_grad_c(int d, int b, int a) { return 1 + d
 template <class R>
 struct Params {
     R D[kMaxM * kMaxM];  // derivative matrix, row-major m x m (operators.hpp:49-74)
+    // Even-odd split of D for Gauss-Legendre nodes (x_{m-1-i} = -x_i, so
+    // D(m-1-i, m-1-t) = -D(i, t)):  with S_t = f_t + f_{m-1-t}, A_t = f_t - f_{m-1-t} (t < m/2),
+    //   X_i = sum_t DE[i][t] S_t + DC[i] f_mid,  Y_i = sum_t DO[i][t] A_t,
+    //   (D f)_i = X_i + Y_i,  (D f)_{m-1-i} = Y_i - X_i   (i < m/2),  (D f)_mid = sum_t DO[mid][t] A_t.
+    R DE[kMaxH * kMaxH];  // (D(i,t) + D(i,m-1-t)) / 2, row-major [i][t], i <= m/2, t < m/2
+    R DO[kMaxH * kMaxH];  // (D(i,t) - D(i,m-1-t)) / 2
+    R DC[kMaxH];          // D(i, mid) for odd m
     R nu, zeta, invT;    // PhysParams (equations.hpp:14-24), 1/T precomputed
     R jac[3];            // constant per-axis metric (oracle.hpp:47)
     R jac_invT[3];       // jac[a] / T : gradient-row scale
@@ -30,6 +38,7 @@ struct Params {
     R* __restrict__ ws;       // unfused only: flux workspace
     long long n_elem;
     long long group_words;    // group * m^d * n_v
+    long long total_words;    // n_groups * group_words (allocation size of u and out)
     long long chunk0;         // first chunk (of NE elements) this launch covers
     long long n_chunks;       // pipelined kernel: number of full chunks to process
     int group;

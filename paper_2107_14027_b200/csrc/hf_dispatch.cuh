@@ -9,27 +9,24 @@ namespace hfb {
 
 template <class R, int DIM, int M, int VARIANT>
 int lines_variant(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
-    constexpr int NE = lines_ne<R, DIM, M, VARIANT>();
+    constexpr int NE = variant_ne<R, DIM, M, VARIANT>();
     if constexpr (NE == 0) {
+        return kUnsupported;
+    } else if constexpr (is_pipe_variant<VARIANT>()) {
+        constexpr int ST = pipe_stages<VARIANT>();
+        if constexpr (PipeShape<R, DIM, M, NE, ST>::SMEM > size_t(kMaxSmemPerCta) ||
+                      PipeShape<R, DIM, M, NE, ST>::BS > 1024) {
+            return kUnsupported;
+        } else {
+            return src ? int(launch_lines_pipe<R, DIM, M, NE, ST, true>(prm, st, info, dry))
+                       : int(launch_lines_pipe<R, DIM, M, NE, ST, false>(prm, st, info, dry));
+        }
+    } else if constexpr (LinesShape<R, DIM, M, NE>::SMEM > size_t(kMaxSmemPerCta) ||
+                         LinesShape<R, DIM, M, NE>::BS > 1024) {
         return kUnsupported;
     } else {
         return src ? int(launch_lines<R, DIM, M, NE, true>(prm, st, info, dry))
                    : int(launch_lines<R, DIM, M, NE, false>(prm, st, info, dry));
-    }
-}
-
-template <class R, int DIM, int M, int VARIANT>
-int pipe_variant(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
-    constexpr int NE = pipe_ne<R, DIM, M, VARIANT>();
-    constexpr int ST = pipe_stages<VARIANT>();
-    if constexpr (NE == 0) {
-        return kUnsupported;
-    } else if constexpr (PipeShape<R, DIM, M, NE, ST>::SMEM > size_t(kMaxSmemPerCta) ||
-                         PipeShape<R, DIM, M, NE, ST>::BS > 1024) {
-        return kUnsupported;
-    } else {
-        return src ? int(launch_lines_pipe<R, DIM, M, NE, ST, true>(prm, st, info, dry))
-                   : int(launch_lines_pipe<R, DIM, M, NE, ST, false>(prm, st, info, dry));
     }
 }
 
@@ -39,10 +36,13 @@ int lines_m(int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo*
         case 0: return lines_variant<R, DIM, M, 0>(src, prm, st, info, dry);
         case 1: return lines_variant<R, DIM, M, 1>(src, prm, st, info, dry);
         case 2: return lines_variant<R, DIM, M, 2>(src, prm, st, info, dry);
-        case 3: return pipe_variant<R, DIM, M, 3>(src, prm, st, info, dry);
-        case 4: return pipe_variant<R, DIM, M, 4>(src, prm, st, info, dry);
-        case 5: return pipe_variant<R, DIM, M, 5>(src, prm, st, info, dry);
-        case 6: return pipe_variant<R, DIM, M, 6>(src, prm, st, info, dry);
+        case 3: return lines_variant<R, DIM, M, 3>(src, prm, st, info, dry);
+        case 4: return lines_variant<R, DIM, M, 4>(src, prm, st, info, dry);
+        case 5: return lines_variant<R, DIM, M, 5>(src, prm, st, info, dry);
+        case 6: return lines_variant<R, DIM, M, 6>(src, prm, st, info, dry);
+        case 7: return lines_variant<R, DIM, M, 7>(src, prm, st, info, dry);
+        case 8: return lines_variant<R, DIM, M, 8>(src, prm, st, info, dry);
+        case 9: return lines_variant<R, DIM, M, 9>(src, prm, st, info, dry);
         default: return kUnsupported;
     }
 }

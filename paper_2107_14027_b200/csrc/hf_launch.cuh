@@ -29,6 +29,7 @@ struct KInfo {
     int registers = 0;
     long long grid = 0;
     int bulk_path = 0;
+    int blocks_per_sm = 0;
     char name[96] = {0};
 };
 
@@ -47,30 +48,29 @@ constexpr int lines_ne_default() {
     return ne;
 }
 
-template <class R, int DIM, int M, int VARIANT>
-constexpr int lines_ne() {
-    constexpr int ne0 = lines_ne_default<R, DIM, M>();
-    constexpr int min_ne = 16 / int(sizeof(R));
-    if constexpr (VARIANT == 1) return ne0 / 2 >= min_ne ? ne0 / 2 : 0;
-    else if constexpr (VARIANT == 2) {
-        constexpr int ne = ne0 * 2;
-        return (LinesShape<R, DIM, M, ne>::SMEM <= size_t(kMaxSmemPerCta) && ne * ipow_c(M, DIM - 1) <= 1024) ? ne
-                                                                                                            : 0;
-    } else return ne0;
+// Lines variants.  NE0 = lines_ne_default (about three CTAs per SM).
+//   one chunk per CTA (hf_lines_kernel):        0: NE0   1: NE0/2   2: 2*NE0   7: NE0/4
+//   persistent TMA ring (hf_lines_pipe_kernel): 3: NE0 x2 stages   4: NE0/2 x3   5: NE0/2 x2
+//                                               6: NE0 x3          8: NE0/4 x3   9: NE0/4 x4
+// The contiguous bulk path accepts any NE >= 1 (hf_chunk_io.cuh), so the small-NE
+// variants exist for every order; a variant whose shape does not fit (shared
+// memory, 1024 threads) reports unsupported.
+template <int VARIANT>
+constexpr bool is_pipe_variant() {
+    return VARIANT == 3 || VARIANT == 4 || VARIANT == 5 || VARIANT == 6 || VARIANT == 8 || VARIANT == 9;
 }
-
-// Pipelined (persistent, warp-specialised) lines variants 3..6:
-//   3: NE0, 2 stages   4: NE0/2, 3 stages   5: NE0/2, 2 stages   6: NE0, 3 stages
 template <class R, int DIM, int M, int VARIANT>
-constexpr int pipe_ne() {
+constexpr int variant_ne() {
     constexpr int ne0 = lines_ne_default<R, DIM, M>();
-    constexpr int min_ne = 16 / int(sizeof(R));
-    constexpr int ne = (VARIANT == 3 || VARIANT == 6) ? ne0 : ne0 / 2;
-    return ne >= min_ne ? ne : 0;
+    constexpr int ne = (VARIANT == 0 || VARIANT == 3 || VARIANT == 6)   ? ne0
+                       : (VARIANT == 1 || VARIANT == 4 || VARIANT == 5) ? ne0 / 2
+                       : (VARIANT == 2)                                 ? ne0 * 2
+                                                                        : ne0 / 4;
+    return ne >= 1 ? ne : 0;
 }
 template <int VARIANT>
 constexpr int pipe_stages() {
-    return (VARIANT == 4 || VARIANT == 6) ? 3 : 2;
+    return (VARIANT == 4 || VARIANT == 6 || VARIANT == 8) ? 3 : (VARIANT == 9 ? 4 : 2);
 }
 
 template <class R, int M>
@@ -81,6 +81,14 @@ constexpr int planar_ne() {
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Layouts whose full chunks take the bulk path (hf_chunk_io.cuh): the group is
+// the chunk (one contiguous range, any alignment), or whole 16-byte rows.
+template <class R, int NE>
+inline bool bulk_layout(int group) {
+    if (group == NE) return true;
+    return (group % NE == 0) && (NE * sizeof(R)) % 16 == 0 && ((long long)group * sizeof(R)) % 16 == 0;
+}
 
 template <class K>
 inline int set_smem_attr(K kernel, size_t smem) {
@@ -94,8 +102,16 @@ inline int set_smem_attr(K kernel, size_t smem) {
 template <class K>
 inline void fill_regs(K kernel, KInfo* info) {
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess) info->registers = fa.numRegs;
-    else {
+    if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess) {
+        info->registers = fa.numRegs;
+        int b = 0;
+        if (set_smem_attr(kernel, size_t(info->shared_bytes)) == 0 &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, info->block_threads, size_t(info->shared_bytes)) ==
+                cudaSuccess)
+            info->blocks_per_sm = b;
+        else
+            cudaGetLastError();
+    } else {
         cudaGetLastError();
         info->registers = 0;
     }
@@ -109,7 +125,7 @@ cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
     using S = LinesShape<R, DIM, M, NE>;
     auto kernel = hf_lines_kernel<R, DIM, M, NE, SRC>;
     const long long grid = (p.n_elem + NE - 1) / NE;
-    const bool fast_layout = (p.group % NE == 0) && ((long long)p.group * sizeof(R)) % 16 == 0;
+    const bool fast_layout = bulk_layout<R, NE>(p.group);
     if (info) {
         info->method = 2;
         info->elems_per_cta = NE;
@@ -146,8 +162,12 @@ cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dr
     using S = PipeShape<R, DIM, M, NE, STAGES>;
     using L = LinesShape<R, DIM, M, NE>;
     auto kernel = hf_lines_pipe_kernel<R, DIM, M, NE, STAGES, SRC>;
-    const bool fast_layout = (p.group % NE == 0) && ((long long)p.group * sizeof(R)) % 16 == 0;
-    const long long n_full = p.n_elem / NE;
+    const bool fast_layout = bulk_layout<R, NE>(p.group);
+    long long n_full = p.n_elem / NE;
+    // contiguous chunks load a 16-byte superset: keep the allocation's last chunk
+    // (whose superset could run past the end) for the guarded tail launch
+    if (p.group == NE && n_full > 0 && n_full * NE == p.n_elem && (p.total_words * (long long)sizeof(R)) % 16 != 0)
+        n_full -= 1;
     static int blocks_per_sm = -1;
     if (blocks_per_sm < 0 && !dry) {
         if (int e = set_smem_attr(kernel, S::SMEM)) return cudaError_t(e);
@@ -179,11 +199,12 @@ cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dr
     kernel<<<dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st>>>(p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if (n_full * NE < p.n_elem) {  // guarded partial chunk
+    const long long n_chunks = (p.n_elem + NE - 1) / NE;
+    if (n_full < n_chunks) {  // the partial (or allocation-final) chunk(s)
         auto tail = hf_lines_kernel<R, DIM, M, NE, SRC>;
         if (int e2 = set_smem_attr(tail, L::SMEM)) return cudaError_t(e2);
         p.chunk0 = n_full;
-        tail<<<1, L::BS, L::SMEM, st>>>(p);
+        tail<<<unsigned(n_chunks - n_full), L::BS, L::SMEM, st>>>(p);
         e = cudaGetLastError();
     }
     return e;

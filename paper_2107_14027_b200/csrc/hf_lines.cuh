@@ -33,7 +33,12 @@
 // kernel; padding elements are neither read nor written (render.hpp:95,102).
 #pragma once
 
+#include "hf_chunk_io.cuh"
 #include "hf_common.cuh"
+
+#ifndef HF_EVEN_ODD_MIN_M
+#define HF_EVEN_ODD_MIN_M 6  // even-odd split of the line contraction from m = 6 (p = 5) up
+#endif
 
 namespace hfb {
 
@@ -47,10 +52,50 @@ struct LinesShape {
     static constexpr int IN_WORDS = NE * NP * NV;
     static constexpr int ACC_WORDS = NE * NP * NACC;
     static constexpr int HDR = 128;  // mbarrier + alignment pad
-    static constexpr size_t SMEM = HDR + size_t(IN_WORDS + ACC_WORDS) * sizeof(R);
     static constexpr int IN_BYTES = IN_WORDS * int(sizeof(R));
     static constexpr int ROW_BYTES = NE * int(sizeof(R));
+    using IO = ChunkIO<R, NE, NP * NV, IN_BYTES>;
+    static constexpr int BUF_BYTES = IO::BUF_BYTES;  // chunk buffer incl. alignment slack
+    static constexpr size_t SMEM = HDR + size_t(BUF_BYTES) + size_t(ACC_WORDS) * sizeof(R);
 };
+
+// Whether the chunk starting at word `gbase` can take the bulk path: full chunk,
+// layout verified by the host, and (contiguous) the 16-byte superset stays inside
+// the allocation.
+template <class R, int IN_WORDS>
+__device__ __forceinline__ bool chunk_bulk_ok(const Params<R>& p, long long gbase, bool full, bool contiguous) {
+    if (!p.fast_ok || !full) return false;
+    if (!contiguous) return true;
+    return ((gbase + IN_WORDS) * (long long)sizeof(R) + 15) / 16 * 16 <= p.total_words * (long long)sizeof(R);
+}
+
+// Outputs of one line point (index i of the sweep's line): gradient rows final
+// (+ source), continuity / momentum partials accumulated or finished.
+template <class R, int DIM, int M, int NE, bool SRC, int A, int PHASE>
+__device__ __forceinline__ void lines_emit(R* __restrict__ q, R* __restrict__ a, const Params<R>& p, const R (&dV)[DIM],
+                                           const R (&dQ)[DIM]) {
+    constexpr int VS = NE * ipow_c(M, DIM);
+#pragma unroll
+    for (int b = 0; b < DIM; ++b) {
+        R o = p.jac_invT[A] * dV[b];
+        if constexpr (SRC) o = fma(-p.invT, q[VS * var_grad_c(DIM, b, A)], o);
+        q[VS * var_grad_c(DIM, b, A)] = o;
+    }
+    const R c = p.jac[A] * dV[A];
+    if constexpr (PHASE == 0) {
+        a[0] = c;
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) a[VS * (1 + b)] = p.jac[A] * dQ[b];
+    } else if constexpr (PHASE == 1) {
+        a[0] = a[0] + c;
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) a[VS * (1 + b)] = fma(p.jac[A], dQ[b], a[VS * (1 + b)]);
+    } else {
+        q[0] = -(p.zeta * (a[0] + c));
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) q[VS * (1 + b)] = -fma(p.jac[A], dQ[b], a[VS * (1 + b)]);
+    }
+}
 
 // One sweep along axis A.  PHASE: 0 = first sweep, 1 = middle, 2 = last.
 template <class R, int DIM, int M, int NE, bool SRC, int A, int PHASE>
@@ -92,43 +137,144 @@ __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ a
         }
     }
 
+    // Derivatives along the line.  m >= HF_EVEN_ODD_MIN_M: even-odd split of D
+    // (Params::DE/DO/DC), about half the FMAs of the dense m x m contraction; it
+    // lengthens the dependency chain, which only pays off at high order (measured:
+    // p6 +14 % FP64, p3 -5 %), so lower orders use the dense contraction.
+#define HF_EMIT(I, DV, DQ) lines_emit<R, DIM, M, NE, SRC, A, PHASE>(sb + NE * STRIDE * (I), ab + NE * STRIDE * (I), p, DV, DQ)
+    if constexpr (M < HF_EVEN_ODD_MIN_M) {
 #pragma unroll
-    for (int i = 0; i < M; ++i) {
-        R dV[DIM], dQ[DIM];
-#pragma unroll
-        for (int b = 0; b < DIM; ++b) {
-            dV[b] = p.D[i * M] * V[b][0];
-            dQ[b] = p.D[i * M] * Q[b][0];
-        }
-#pragma unroll
-        for (int t = 1; t < M; ++t) {
+        for (int i = 0; i < M; ++i) {
+            R dV[DIM], dQ[DIM];
 #pragma unroll
             for (int b = 0; b < DIM; ++b) {
-                dV[b] = fma(p.D[i * M + t], V[b][t], dV[b]);
-                dQ[b] = fma(p.D[i * M + t], Q[b][t], dQ[b]);
+                dV[b] = p.D[i * M] * V[b][0];
+                dQ[b] = p.D[i * M] * Q[b][0];
             }
+#pragma unroll
+            for (int t = 1; t < M; ++t)
+#pragma unroll
+                for (int b = 0; b < DIM; ++b) {
+                    dV[b] = fma(p.D[i * M + t], V[b][t], dV[b]);
+                    dQ[b] = fma(p.D[i * M + t], Q[b][t], dQ[b]);
+                }
+            HF_EMIT(i, dV, dQ);
         }
-        R* q = sb + NE * STRIDE * i;
-        R* a = ab + NE * STRIDE * i;
+    } else {
+        constexpr int H = M / 2;
+        constexpr int K = kMaxH;
+        // symmetric / antisymmetric parts, in place: V[b][t] <- S_t, V[b][M-1-t] <- A_t
 #pragma unroll
-        for (int b = 0; b < DIM; ++b) {
-            R o = p.jac_invT[A] * dV[b];
-            if constexpr (SRC) o = fma(-p.invT, q[VS * var_grad_c(DIM, b, A)], o);
-            q[VS * var_grad_c(DIM, b, A)] = o;
+        for (int t = 0; t < H; ++t)
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) {
+                const R v0 = V[b][t], v1 = V[b][M - 1 - t], q0 = Q[b][t], q1 = Q[b][M - 1 - t];
+                V[b][t] = v0 + v1;
+                V[b][M - 1 - t] = v0 - v1;
+                Q[b][t] = q0 + q1;
+                Q[b][M - 1 - t] = q0 - q1;
+            }
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            R xV[DIM], yV[DIM], xQ[DIM], yQ[DIM];
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) {
+                xV[b] = p.DE[i * K] * V[b][0];
+                yV[b] = p.DO[i * K] * V[b][M - 1];
+                xQ[b] = p.DE[i * K] * Q[b][0];
+                yQ[b] = p.DO[i * K] * Q[b][M - 1];
+            }
+#pragma unroll
+            for (int t = 1; t < H; ++t)
+#pragma unroll
+                for (int b = 0; b < DIM; ++b) {
+                    xV[b] = fma(p.DE[i * K + t], V[b][t], xV[b]);
+                    yV[b] = fma(p.DO[i * K + t], V[b][M - 1 - t], yV[b]);
+                    xQ[b] = fma(p.DE[i * K + t], Q[b][t], xQ[b]);
+                    yQ[b] = fma(p.DO[i * K + t], Q[b][M - 1 - t], yQ[b]);
+                }
+            if constexpr (M % 2 == 1)
+#pragma unroll
+                for (int b = 0; b < DIM; ++b) {
+                    xV[b] = fma(p.DC[i], V[b][H], xV[b]);
+                    xQ[b] = fma(p.DC[i], Q[b][H], xQ[b]);
+                }
+            R dV[DIM], dQ[DIM];
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) {
+                dV[b] = xV[b] + yV[b];
+                dQ[b] = xQ[b] + yQ[b];
+            }
+            HF_EMIT(i, dV, dQ);
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) {
+                dV[b] = yV[b] - xV[b];
+                dQ[b] = yQ[b] - xQ[b];
+            }
+            HF_EMIT(M - 1 - i, dV, dQ);
         }
-        const R c = p.jac[A] * dV[A];
-        if constexpr (PHASE == 0) {
-            a[0] = c;
+        if constexpr (M % 2 == 1) {
+            R dV[DIM], dQ[DIM];
 #pragma unroll
-            for (int b = 0; b < DIM; ++b) a[VS * (1 + b)] = p.jac[A] * dQ[b];
-        } else if constexpr (PHASE == 1) {
-            a[0] = a[0] + c;
+            for (int b = 0; b < DIM; ++b) {
+                dV[b] = p.DO[H * K] * V[b][M - 1];
+                dQ[b] = p.DO[H * K] * Q[b][M - 1];
+            }
 #pragma unroll
-            for (int b = 0; b < DIM; ++b) a[VS * (1 + b)] = fma(p.jac[A], dQ[b], a[VS * (1 + b)]);
-        } else {
-            q[0] = -(p.zeta * (a[0] + c));
+            for (int t = 1; t < H; ++t)
 #pragma unroll
-            for (int b = 0; b < DIM; ++b) q[VS * (1 + b)] = -fma(p.jac[A], dQ[b], a[VS * (1 + b)]);
+                for (int b = 0; b < DIM; ++b) {
+                    dV[b] = fma(p.DO[H * K + t], V[b][M - 1 - t], dV[b]);
+                    dQ[b] = fma(p.DO[H * K + t], Q[b][M - 1 - t], dQ[b]);
+                }
+            HF_EMIT(H, dV, dQ);
+        }
+    }
+}
+
+#undef HF_EMIT
+
+// All d sweeps of one chunk whose first word sits HEADB bytes into `buf`.
+// HEADB is a template parameter so that every shared-memory address in the
+// sweeps is a compile-time offset from the __shared__ window (a runtime base
+// costs ~30 registers and ~10 % of HBM throughput, measured).  BAR: 0 = the
+// whole CTA (__syncthreads), 1 = the NTHR consumer threads (named barrier 1).
+template <class R, int DIM, int M, int NE, bool SRC, int HEADB, int BAR, int NTHR>
+__device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const Params<R>& p, int t) {
+    using S = LinesShape<R, DIM, M, NE>;
+    R* s = reinterpret_cast<R*>(buf + HEADB);
+    auto sync = [] {
+        if constexpr (BAR == 0) __syncthreads();
+        else named_bar_sync(1, NTHR);
+    };
+    if constexpr (DIM == 3) {
+        for (int L = t; L < S::LINES; L += NTHR) lines_sweep<R, 3, M, NE, SRC, 0, 0>(s, acc, p, L);
+        sync();
+        for (int L = t; L < S::LINES; L += NTHR) lines_sweep<R, 3, M, NE, SRC, 1, 1>(s, acc, p, L);
+        sync();
+        for (int L = t; L < S::LINES; L += NTHR) lines_sweep<R, 3, M, NE, SRC, 2, 2>(s, acc, p, L);
+    } else {
+        for (int L = t; L < S::LINES; L += NTHR) lines_sweep<R, 2, M, NE, SRC, 0, 0>(s, acc, p, L);
+        sync();
+        for (int L = t; L < S::LINES; L += NTHR) lines_sweep<R, 2, M, NE, SRC, 1, 2>(s, acc, p, L);
+    }
+}
+
+// Runtime head (bytes, a multiple of sizeof(R), < 16) -> compile-time HEADB.
+// Chunks whose byte size is a multiple of 16 always start aligned: one instance.
+template <class R, int DIM, int M, int NE, bool SRC, int BAR, int NTHR>
+__device__ __forceinline__ void lines_sweeps_at(unsigned char* buf, int head, R* acc, const Params<R>& p, int t) {
+    if constexpr (LinesShape<R, DIM, M, NE>::IN_BYTES % 16 == 0) {
+        lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR>(buf, acc, p, t);
+    } else if constexpr (sizeof(R) == 8) {
+        if (head == 0) lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR>(buf, acc, p, t);
+        else lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR>(buf, acc, p, t);
+    } else {
+        switch (head) {
+            case 0: lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR>(buf, acc, p, t); break;
+            case 4: lines_sweeps<R, DIM, M, NE, SRC, 4, BAR, NTHR>(buf, acc, p, t); break;
+            case 8: lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR>(buf, acc, p, t); break;
+            default: lines_sweeps<R, DIM, M, NE, SRC, 12, BAR, NTHR>(buf, acc, p, t); break;
         }
     }
 }
@@ -139,16 +285,20 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE>::BS)
     using S = LinesShape<R, DIM, M, NE>;
     constexpr int BS = S::BS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    using IO = typename S::IO;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
-    R* s = reinterpret_cast<R*>(smem_raw + S::HDR);
-    R* acc = s + S::IN_WORDS;
+    unsigned char* buf = smem_raw + S::HDR;
+    R* acc = reinterpret_cast<R*>(buf + S::BUF_BYTES);
 
     const int tid = threadIdx.x;
     const long long E0 = (p.chunk0 + static_cast<long long>(blockIdx.x)) * NE;
-    const bool fast = p.fast_ok && (E0 + NE <= p.n_elem);
     const long long grp = E0 / p.group;
     const int el0 = static_cast<int>(E0 - grp * p.group);
     const long long gbase = grp * p.group_words + el0;
+    const bool contiguous = (p.group == NE);
+    const bool fast = chunk_bulk_ok<R, S::IN_WORDS>(p, gbase, E0 + NE <= p.n_elem, contiguous);
+    const int head = fast ? IO::head_bytes(p.u + gbase, contiguous) : 0;
+    R* s = reinterpret_cast<R*>(smem_raw + S::HDR);  // guarded path (head == 0)
 
     // ---------------- stage the chunk into shared memory ----------------
     if (fast) {
@@ -158,22 +308,9 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE>::BS)
         }
         __syncthreads();
         if (tid < 32) {
-            if (tid == 0) mbar_arrive_expect_tx(bar, S::IN_BYTES);
+            if (tid == 0) mbar_arrive_expect_tx(bar, IO::tx_bytes(p.u + gbase, contiguous));
             __syncwarp();
-            if (p.group == NE) {
-                // contiguous chunk: split into 32 near-equal 16B-multiple pieces
-                constexpr int PIECE = ((S::IN_BYTES / 32 + 15) / 16) * 16;
-                const int off = tid * PIECE;
-                if (off < S::IN_BYTES) {
-                    const int len = (S::IN_BYTES - off) < PIECE ? (S::IN_BYTES - off) : PIECE;
-                    bulk_g2s(reinterpret_cast<unsigned char*>(s) + off,
-                             reinterpret_cast<const unsigned char*>(p.u + gbase) + off, len, bar);
-                }
-            } else {
-                // one row per (point, variable): NE contiguous words at stride `group`
-                for (int row = tid; row < S::NP * S::NV; row += 32)
-                    bulk_g2s(s + NE * row, p.u + gbase + static_cast<long long>(p.group) * row, S::ROW_BYTES, bar);
-            }
+            IO::load(buf, p.u + gbase, p.group, contiguous, bar, tid);
         }
         mbar_wait_parity(bar, 0);
     } else {
@@ -192,37 +329,14 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE>::BS)
     }
 
     // ---------------- d sweeps ----------------
-    constexpr int LINES = S::LINES;
-    if constexpr (DIM == 3) {
-        for (int L = tid; L < LINES; L += BS) lines_sweep<R, 3, M, NE, SRC, 0, 0>(s, acc, p, L);
-        __syncthreads();
-        for (int L = tid; L < LINES; L += BS) lines_sweep<R, 3, M, NE, SRC, 1, 1>(s, acc, p, L);
-        __syncthreads();
-        for (int L = tid; L < LINES; L += BS) lines_sweep<R, 3, M, NE, SRC, 2, 2>(s, acc, p, L);
-    } else {
-        for (int L = tid; L < LINES; L += BS) lines_sweep<R, 2, M, NE, SRC, 0, 0>(s, acc, p, L);
-        __syncthreads();
-        for (int L = tid; L < LINES; L += BS) lines_sweep<R, 2, M, NE, SRC, 1, 2>(s, acc, p, L);
-    }
+    lines_sweeps_at<R, DIM, M, NE, SRC, 0, BS>(buf, head, acc, p, tid);
 
     // ---------------- write the finished chunk ----------------
     if (fast) {
         fence_proxy_async_smem();
         __syncthreads();
         if (tid < 32) {
-            if (p.group == NE) {
-                constexpr int PIECE = ((S::IN_BYTES / 32 + 15) / 16) * 16;
-                const int off = tid * PIECE;
-                if (off < S::IN_BYTES) {
-                    const int len = (S::IN_BYTES - off) < PIECE ? (S::IN_BYTES - off) : PIECE;
-                    bulk_s2g(reinterpret_cast<unsigned char*>(p.out + gbase) + off,
-                             reinterpret_cast<const unsigned char*>(s) + off, len);
-                }
-            } else {
-                for (int row = tid; row < S::NP * S::NV; row += 32)
-                    bulk_s2g(p.out + gbase + static_cast<long long>(p.group) * row, s + NE * row, S::ROW_BYTES);
-            }
-            bulk_commit();
+            IO::store(p.out + gbase, buf, p.group, contiguous, tid);
             bulk_wait_read_all();
         }
     } else {

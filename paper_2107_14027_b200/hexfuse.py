@@ -297,7 +297,7 @@ def kernel_info(pr: hf_problem) -> dict:
     check(_lib.load().hf_kernel_info_get(C.byref(pr), C.byref(ki)), "hf_kernel_info_get")
     return {"method": Method(ki.method).name, "elems_per_cta": ki.elems_per_cta, "block_threads": ki.block_threads,
             "shared_bytes": ki.shared_bytes, "registers": ki.registers, "grid": int(ki.grid),
-            "bulk_path": bool(ki.bulk_path), "name": ki.name.decode()}
+            "bulk_path": bool(ki.bulk_path), "blocks_per_sm": ki.blocks_per_sm, "name": ki.name.decode()}
 
 
 def derivative_matrix(m: int):
@@ -353,7 +353,7 @@ def variant_info(pr: hf_problem, method: Method, variant: int) -> dict:
           "hf_fused_divergence_variant(info)")
     return {"method": Method(ki.method).name, "elems_per_cta": ki.elems_per_cta, "block_threads": ki.block_threads,
             "shared_bytes": ki.shared_bytes, "registers": ki.registers, "grid": int(ki.grid),
-            "bulk_path": bool(ki.bulk_path), "name": ki.name.decode()}
+            "bulk_path": bool(ki.bulk_path), "blocks_per_sm": ki.blocks_per_sm, "name": ki.name.decode()}
 
 
 def unfused_workspace_bytes(pr: hf_problem) -> int:

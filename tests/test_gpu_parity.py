@@ -72,7 +72,7 @@ def test_lines_misaligned_pointer(cuda):
     check_parity(3, 2, 64, 16, False, U, method=Method.lines, offset_bytes=8)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("variant", list(range(10)))
 @pytest.mark.parametrize("d,p,fp32", [(3, 1, True), (3, 3, False), (3, 4, True), (3, 6, False), (3, 6, True),
                                       (2, 3, True), (2, 8, True)])
 def test_lines_variants(cuda, d, p, fp32, variant):
@@ -84,7 +84,9 @@ def test_lines_variants(cuda, d, p, fp32, variant):
     except hf.HexfuseInvalid:
         pytest.skip("variant not instantiated for this order")
     g = info["elems_per_cta"]
-    for n, group, src in [(5 * g + 1, g, False), (7 * g, 2 * g, True), (3 * g + 2, 4 * g, True)]:
+    # contiguous chunks (group == NE, any alignment; with and without a partial last group),
+    # row-mode chunks (group = 2 NE, 4 NE)
+    for n, group, src in [(5 * g + 1, g, False), (6 * g, g, True), (7 * g, 2 * g, True), (3 * g + 2, 4 * g, True)]:
         U = _field(d, p, n, group, fp32, 11 + n)
         got = run_device(d, p, n, group, fp32, U, method=Method.lines, variant=variant, with_source=src)
         ref = O.oracle_divergence(d, p, n, group, U, PAR.nu, PAR.zeta, PAR.T, (1.0, 1.0, 1.0), src)
@@ -97,7 +99,7 @@ def test_pipe_many_chunks_per_cta(cuda):
     import paper_2107_14027_b200 as hf
     for fp32, p in [(False, 3), (True, 5)]:
         pr = hf.make_problem(3, p, 1, 1, int(not fp32), PAR)
-        for variant in (3, 4, 5, 6):
+        for variant in (3, 4, 5, 6, 8, 9):
             try:
                 g = hf.variant_info(pr, Method.lines, variant)["elems_per_cta"]
             except hf.HexfuseInvalid:

@@ -45,35 +45,71 @@ def time_launch(fn, iters=20, warmup=3):
     return ts[len(ts) // 2]
 
 
-def measure(d, p, prec, method, variant, points, src=False):
-    pr0 = hf.make_problem(d, p, 1, 1, prec, PAR, method=method)
-    if method == Method.unfused:
-        group = 32
-        info = {"elems_per_cta": group, "name": f"unfused_d{d}_p{p}"}
-    else:
-        info = hf.variant_info(pr0, method, variant)
-        group = info["elems_per_cta"]
-    npt = (p + 1) ** d
-    n_elem = max(group, int(round(points / npt / group)) * group)
-    pr = hf.make_problem(d, p, n_elem, group, prec, PAR, with_source=src, method=method)
+def measure_config(d, p, prec, cands, points, rounds=8, per_round=5, src=False):
+    """Time every candidate (method, variant) of one (d, p, precision) on the SAME
+    buffers, round-robin over `rounds` rounds (drift and clock changes hit all
+    candidates alike); per candidate the median launch time is reported."""
     import torch
-    words = hf.field_words(pr)
+    infos = []
+    for method, variant in cands:
+        pr0 = hf.make_problem(d, p, 1, 1, prec, PAR, method=method)
+        try:
+            info = ({"elems_per_cta": 32, "name": f"unfused_d{d}_p{p}_{prec.name}"} if method == Method.unfused
+                    else hf.variant_info(pr0, method, variant))
+        except hf.HexfuseInvalid:
+            continue
+        infos.append((method, variant, info))
+    if not infos:
+        return []
+    npt = (p + 1) ** d
+    lcm = 512
+    n_elem = max(lcm, int(round(points / npt / lcm)) * lcm)  # a multiple of every candidate's group
     dt = torch.float32 if prec == Precision.fp32 else torch.float64
+    words = n_elem * npt * hf.n_vars(d)
     u = torch.rand(words, dtype=dt, device="cuda") * 2 - 1
     o = torch.empty_like(u)
-    if method == Method.unfused:
-        ws = torch.empty(hf.unfused_workspace_bytes(pr) // u.element_size(), dtype=dt, device="cuda")
-        fn = lambda: hf.unfused_divergence_device(pr, u, o, ws)  # noqa: E731
-    else:
-        fn = lambda: hf.fused_divergence_variant(pr, method, variant, u, o)  # noqa: E731
-    t = time_launch(fn)
+    ws = None
+    runs = []
+    for method, variant, info in infos:
+        g = info["elems_per_cta"]
+        pr = hf.make_problem(d, p, n_elem, g, prec, PAR, with_source=src, method=method)
+        assert hf.field_words(pr) == words
+        if method == Method.unfused:
+            if ws is None:
+                ws = torch.empty(hf.unfused_workspace_bytes(pr) // u.element_size(), dtype=dt, device="cuda")
+            fn = (lambda pr=pr: hf.unfused_divergence_device(pr, u, o, ws))
+        else:
+            fn = (lambda pr=pr, m=method, v=variant: hf.fused_divergence_variant(pr, m, v, u, o))
+        runs.append((method, variant, info, fn, []))
+    st = torch.cuda.current_stream()
+    for _, _, _, fn, _ in runs:
+        for _ in range(3):
+            fn()
+    torch.cuda.synchronize()
+    for _ in range(rounds):
+        for _, _, _, fn, ts in runs:
+            for _ in range(per_round):
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                fn()
+                b.record(st)
+                b.synchronize()
+                ts.append(a.elapsed_time(b) * 1e-3)
+    out = []
     pts = n_elem * npt
     alg = pts * 2 * hf.n_vars(d) * (4 if prec == Precision.fp32 else 8)
-    del u, o
-    return {"d": d, "p": p, "precision": prec.name, "method": method.name, "variant": variant, "src": src,
-            "n_elem": n_elem, "group": group, "points": pts, "seconds": t, "gdofs": pts / t / 1e9,
-            "alg_GBps": alg / t / 1e9, "kernel": info.get("name"), "smem": info.get("shared_bytes"),
-            "regs": info.get("registers"), "block": info.get("block_threads")}
+    for method, variant, info, _, ts in runs:
+        ts.sort()
+        t = ts[len(ts) // 2]
+        out.append({"d": d, "p": p, "precision": prec.name, "method": method.name, "variant": variant, "src": src,
+                    "n_elem": n_elem, "group": info["elems_per_cta"], "points": pts, "seconds": t,
+                    "gdofs": pts / t / 1e9, "alg_GBps": alg / t / 1e9, "spread": (ts[-1] - ts[0]) / t,
+                    "kernel": info.get("name"), "smem": info.get("shared_bytes"), "regs": info.get("registers"),
+                    "block": info.get("block_threads"), "blocks_per_sm": info.get("blocks_per_sm"),
+                    "samples": len(ts)})
+    del u, o, ws
+    return out
 
 
 def main():
@@ -83,6 +119,9 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--write-table", action="store_true")
     ap.add_argument("--no-unfused", action="store_true")
+    ap.add_argument("--ps", default=None, help="comma list of orders (default: all)")
+    ap.add_argument("--variants", default=None, help="comma list of lines variants (default: 0..9)")
+    ap.add_argument("--no-planar", action="store_true")
     ap.add_argument("--from-files", nargs="*", default=None, help="write the table from saved jsonl rows")
     args = ap.parse_args()
     if args.from_files:
@@ -93,17 +132,14 @@ def main():
     for d in [int(x) for x in args.dims.split(",")]:
         pmax = 6 if d == 3 else 8
         for prec in (Precision.fp32, Precision.fp64):
-            for p in range(1, pmax + 1):
-                cands = [(Method.lines, v) for v in (0, 1, 2, 3, 4, 5, 6)]
-                if d == 3:
+            for p in ([int(x) for x in args.ps.split(",")] if args.ps else range(1, pmax + 1)):
+                vs = [int(x) for x in args.variants.split(",")] if args.variants else range(10)
+                cands = [(Method.lines, v) for v in vs]
+                if d == 3 and not args.no_planar:
                     cands.append((Method.planar, 0))
                 if not args.no_unfused:
                     cands.append((Method.unfused, 0))
-                for method, variant in cands:
-                    try:
-                        r = measure(d, p, prec, method, variant, args.points)
-                    except hf.HexfuseInvalid:
-                        continue
+                for r in measure_config(d, p, prec, cands, args.points):
                     rows.append(r)
                     line = json.dumps(r)
                     print(line, flush=True)
@@ -129,8 +165,9 @@ def write_table(rows, points):
         f.write("// hf_select_table.inc -- measured method selection (replaces the reference's\n"
                 "// preset_table, presets.hpp:25-37, and default_lines_n, presets.hpp:86-103).\n"
                 "//\n// Row: { d, p, precision(0=fp32,1=fp64), method(1=planar,2=lines), variant }.\n"
-                "// lines variants: 0/1/2 = one chunk per CTA with NE0, NE0/2, 2*NE0 elements;\n"
-                "// 3..6 = persistent TMA-ring kernel (3: NE0 x2 stages, 4: NE0/2 x3, 5: NE0/2 x2, 6: NE0 x3).\n"
+                "// lines variants (hf_launch.cuh): 0/1/2/7 = one chunk per CTA with NE0, NE0/2, 2*NE0, NE0/4\n"
+                "// elements; 3/4/5/6/8/9 = persistent TMA-ring kernel with (NE0,2), (NE0/2,3), (NE0/2,2),\n"
+                "// (NE0,3), (NE0/4,3), (NE0/4,4) (elements, stages).\n"
                 "// Generated by tools/select_methods.py from on-GPU measurements (achieved\n"
                 f"// HBM GB/s, median of 20 launches at ~{points:.0e} points per configuration;\n"
                 "// raw rows in profiles/select_r01_*.jsonl).\n")
