@@ -14,7 +14,7 @@
  *           of generation-time immediates, and the launch shape is the library's.
  *   (b2) generate_kernel(KernelRequest) + execute(ir, field, grid)
  *        presets.hpp:144-161, simulator.hpp:184-192
- *        -> hf_fused_divergence() with hf_problem.method (auto / planar / lines)
+ *        -> hf_fused_divergence() with hf_problem.method (auto / planar / planar-managed / lines)
  *   (b1) StateField oracle_divergence(const StateField&, const PhysParams&,
  *                                     const std::array<double,3>& jac, bool with_source)
  *        oracle.hpp:20-21
@@ -57,6 +57,8 @@ extern "C" {
 #define HF_METHOD_PLANAR 1  /* Alg. 1, thread per (element, z-plane)  (codegen_planar.hpp:251-273) */
 #define HF_METHOD_LINES 2   /* higher-parallelism, thread per line     (codegen_lines.hpp:299-318)  */
 #define HF_METHOD_UNFUSED 3 /* stage 2 + stage 3 (+ stage 6) kernels  (io_model.hpp:32-34)         */
+#define HF_METHOD_PLANAR_MANAGED 4 /* Alg. 1 with every operand resident in shared memory
+                                      (Method::PlanarManaged, codegen_planar.hpp:276-300) */
 
 /* One fused-divergence problem.  Field layout is StateField's
  * (layout.hpp:104-134): word (e,i,j,k,v) at

@@ -67,6 +67,19 @@ inline void check(int rc, const char* what) {
 
 inline void set_device(int device) { detail::thread_device() = device; }
 
+// The reference's kernel method (layout.hpp:18, enum class Method { PlanarUnmanaged,
+// PlanarManaged, Lines }) -> HF_METHOD_*.  Templated on the caller's enum so that this
+// header does not include the reference's.
+template <class MethodEnum>
+int method_of(MethodEnum m) {
+    switch (static_cast<int>(m)) {
+        case 0: return HF_METHOD_PLANAR;
+        case 1: return HF_METHOD_PLANAR_MANAGED;
+        case 2: return HF_METHOD_LINES;
+        default: throw std::invalid_argument("method_of: unknown hexfuse::Method");
+    }
+}
+
 template <class StateField, class PhysParams>
 hf_problem make_problem(const StateField& U, const PhysParams& params, const std::array<double, 3>& jac,
                         bool with_source, int method = HF_METHOD_AUTO) {

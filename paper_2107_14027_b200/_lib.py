@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("HEXFUSE_B200_LIB") or os.path.join(_HERE, "lib", "lib
 
 HF_OK, HF_ERUNTIME, HF_EINVAL = 0, 1, 2
 HF_FP32, HF_FP64 = 0, 1
-HF_METHOD_AUTO, HF_METHOD_PLANAR, HF_METHOD_LINES, HF_METHOD_UNFUSED = 0, 1, 2, 3
+HF_METHOD_AUTO, HF_METHOD_PLANAR, HF_METHOD_LINES, HF_METHOD_UNFUSED, HF_METHOD_PLANAR_MANAGED = 0, 1, 2, 3, 4
 
 
 class hf_problem(C.Structure):

@@ -119,9 +119,9 @@ int validate(const hf_problem* pr) {
     if (!(pr->nu >= 0.0)) return fail(HF_EINVAL, "PhysParams: nu must be >= 0");
     if (!(pr->zeta > 0.0)) return fail(HF_EINVAL, "PhysParams: zeta must be > 0");
     if (!(pr->T > 0.0)) return fail(HF_EINVAL, "PhysParams: T must be > 0");
-    if (pr->method < HF_METHOD_AUTO || pr->method > HF_METHOD_UNFUSED)
+    if (pr->method < HF_METHOD_AUTO || pr->method > HF_METHOD_PLANAR_MANAGED)
         return fail(HF_EINVAL, "hf_problem: unknown method");
-    if (pr->method == HF_METHOD_PLANAR && (pr->d != 3 || pr->p > 6))
+    if ((pr->method == HF_METHOD_PLANAR || pr->method == HF_METHOD_PLANAR_MANAGED) && (pr->d != 3 || pr->p > 6))
         return fail(HF_EINVAL, "planar method: d must be 3 and p <= 6");
     const int64_t words = ipow64(pr->p + 1, pr->d) * (1 + pr->d + pr->d * pr->d) * int64_t(pr->group);
     if (words > (int64_t(1) << 31)) return fail(HF_EINVAL, "hf_problem: group too large");
@@ -131,12 +131,6 @@ int validate(const hf_problem* pr) {
 // ---------------------------------------------------------------------------------------------
 // Selection
 // ---------------------------------------------------------------------------------------------
-struct SelRow {
-    int d, p, prec, method, variant;
-};
-const SelRow kSelect[] = {
-#include "hf_select_table.inc"
-    {0, 0, 0, 0, 0}};
 
 void select_method(const hf_problem* pr, int* method, int* variant) {
     *variant = 0;
@@ -145,7 +139,7 @@ void select_method(const hf_problem* pr, int* method, int* variant) {
         return;
     }
     *method = HF_METHOD_LINES;
-    for (const SelRow& r : kSelect)
+    for (const hfb::SelRow& r : hfb::kSelect)
         if (r.d == pr->d && r.p == pr->p && r.prec == pr->precision) {
             *method = r.method;
             *variant = r.variant;
@@ -197,12 +191,14 @@ int dispatch(const hf_problem* pr, const void* u, void* out, void* ws, cudaStrea
     if (pr->precision == HF_FP32) {
         const auto prm = make_params<float>(pr, u, out, ws);
         if (method == HF_METHOD_PLANAR) rc = hfb::planar_f32(pr->p, src, prm, st, info, dry);
+        else if (method == HF_METHOD_PLANAR_MANAGED) rc = hfb::planar_managed_f32(pr->p, src, prm, st, info, dry);
         else if (method == HF_METHOD_UNFUSED) rc = hfb::unfused_f32(pr->d, pr->p, src, prm, st, info, dry);
         else rc = pr->d == 3 ? hfb::lines_f32_d3(pr->p, variant, src, prm, st, info, dry)
                              : hfb::lines_f32_d2(pr->p, variant, src, prm, st, info, dry);
     } else {
         const auto prm = make_params<double>(pr, u, out, ws);
         if (method == HF_METHOD_PLANAR) rc = hfb::planar_f64(pr->p, src, prm, st, info, dry);
+        else if (method == HF_METHOD_PLANAR_MANAGED) rc = hfb::planar_managed_f64(pr->p, src, prm, st, info, dry);
         else if (method == HF_METHOD_UNFUSED) rc = hfb::unfused_f64(pr->d, pr->p, src, prm, st, info, dry);
         else rc = pr->d == 3 ? hfb::lines_f64_d3(pr->p, variant, src, prm, st, info, dry)
                              : hfb::lines_f64_d2(pr->p, variant, src, prm, st, info, dry);

@@ -114,6 +114,67 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---------------------------------------------------------------------------------------------
+// Value pairs for the line contraction.  The lines kernel contracts two lines
+// with the same D row at once (V_b and the momentum flux M_ba).  For FP32 the
+// pair is a float2 driven by the sm_100 packed instructions (FFMA2 / FMUL2 /
+// FADD2: two FP32 lanes per issued instruction, the scalar D operand broadcast
+// from a uniform register), which halves the FP32 instruction count of the
+// contraction; for FP64 it is two scalar DFMAs.
+// ---------------------------------------------------------------------------------------------
+template <class R>
+struct Pair;
+
+template <>
+struct Pair<float> {
+    float2 v;
+    __device__ __forceinline__ float x() const { return v.x; }
+    __device__ __forceinline__ float y() const { return v.y; }
+    __device__ __forceinline__ static Pair make(float a, float b) { return {make_float2(a, b)}; }
+};
+
+template <>
+struct Pair<double> {
+    double a, b;
+    __device__ __forceinline__ double x() const { return a; }
+    __device__ __forceinline__ double y() const { return b; }
+    __device__ __forceinline__ static Pair make(double x, double y) { return {x, y}; }
+};
+
+__device__ __forceinline__ unsigned long long f2_bits(float2 a) { return *reinterpret_cast<unsigned long long*>(&a); }
+__device__ __forceinline__ float2 f2_from(unsigned long long r) { return *reinterpret_cast<float2*>(&r); }
+
+// s * a
+__device__ __forceinline__ Pair<float> pmul(float s, Pair<float> a) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(make_float2(s, s))), "l"(f2_bits(a.v)));
+    return {f2_from(r)};
+}
+__device__ __forceinline__ Pair<double> pmul(double s, Pair<double> a) { return {s * a.a, s * a.b}; }
+// s * a + c
+__device__ __forceinline__ Pair<float> pfma(float s, Pair<float> a, Pair<float> c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(r)
+        : "l"(f2_bits(make_float2(s, s))), "l"(f2_bits(a.v)), "l"(f2_bits(c.v)));
+    return {f2_from(r)};
+}
+__device__ __forceinline__ Pair<double> pfma(double s, Pair<double> a, Pair<double> c) {
+    return {fma(s, a.a, c.a), fma(s, a.b, c.b)};
+}
+__device__ __forceinline__ Pair<float> padd(Pair<float> a, Pair<float> b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a.v)), "l"(f2_bits(b.v)));
+    return {f2_from(r)};
+}
+__device__ __forceinline__ Pair<double> padd(Pair<double> a, Pair<double> b) { return {a.a + b.a, a.b + b.b}; }
+__device__ __forceinline__ Pair<float> psub(Pair<float> a, Pair<float> b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a.v)), "l"(f2_bits(b.v)));
+    return {f2_from(r)};
+}
+__device__ __forceinline__ Pair<double> psub(Pair<double> a, Pair<double> b) { return {a.a - b.a, a.b - b.b}; }
+
 // streaming (read-once) global load for the generic loader
 template <class R>
 __device__ __forceinline__ R ld_stream(const R* p) {

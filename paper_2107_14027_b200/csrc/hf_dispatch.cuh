@@ -10,16 +10,17 @@ namespace hfb {
 template <class R, int DIM, int M, int VARIANT>
 int lines_variant(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
     constexpr int NE = variant_ne<R, DIM, M, VARIANT>();
-    if constexpr (NE == 0) {
+    if constexpr (NE == 0 || !variant_built<R, DIM, M, VARIANT>()) {
         return kUnsupported;
     } else if constexpr (is_pipe_variant<VARIANT>()) {
         constexpr int ST = pipe_stages<VARIANT>();
-        if constexpr (PipeShape<R, DIM, M, NE, ST>::SMEM > size_t(kMaxSmemPerCta) ||
-                      PipeShape<R, DIM, M, NE, ST>::BS > 1024) {
+        constexpr int GR = pipe_groups<VARIANT>();
+        if constexpr (PipeShape<R, DIM, M, NE, ST, GR>::SMEM > size_t(kMaxSmemPerCta) ||
+                      PipeShape<R, DIM, M, NE, ST, GR>::BS > 1024) {
             return kUnsupported;
         } else {
-            return src ? int(launch_lines_pipe<R, DIM, M, NE, ST, true>(prm, st, info, dry))
-                       : int(launch_lines_pipe<R, DIM, M, NE, ST, false>(prm, st, info, dry));
+            return src ? int(launch_lines_pipe<R, DIM, M, NE, ST, GR, true>(prm, st, info, dry))
+                       : int(launch_lines_pipe<R, DIM, M, NE, ST, GR, false>(prm, st, info, dry));
         }
     } else if constexpr (LinesShape<R, DIM, M, NE>::SMEM > size_t(kMaxSmemPerCta) ||
                          LinesShape<R, DIM, M, NE>::BS > 1024) {
@@ -30,49 +31,41 @@ int lines_variant(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, 
     }
 }
 
-template <class R, int DIM, int M>
+// Variants [VLO, VHI] of one order (the instantiation units split the variant
+// range so that the template instances compile in parallel).
+template <class R, int DIM, int M, int VLO, int VHI, int V = VLO>
 int lines_m(int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
-    switch (variant) {
-        case 0: return lines_variant<R, DIM, M, 0>(src, prm, st, info, dry);
-        case 1: return lines_variant<R, DIM, M, 1>(src, prm, st, info, dry);
-        case 2: return lines_variant<R, DIM, M, 2>(src, prm, st, info, dry);
-        case 3: return lines_variant<R, DIM, M, 3>(src, prm, st, info, dry);
-        case 4: return lines_variant<R, DIM, M, 4>(src, prm, st, info, dry);
-        case 5: return lines_variant<R, DIM, M, 5>(src, prm, st, info, dry);
-        case 6: return lines_variant<R, DIM, M, 6>(src, prm, st, info, dry);
-        case 7: return lines_variant<R, DIM, M, 7>(src, prm, st, info, dry);
-        case 8: return lines_variant<R, DIM, M, 8>(src, prm, st, info, dry);
-        case 9: return lines_variant<R, DIM, M, 9>(src, prm, st, info, dry);
-        default: return kUnsupported;
-    }
+    if (variant == V) return lines_variant<R, DIM, M, V>(src, prm, st, info, dry);
+    if constexpr (V < VHI) return lines_m<R, DIM, M, VLO, VHI, V + 1>(variant, src, prm, st, info, dry);
+    return kUnsupported;
 }
 
-template <class R>
-int run_lines_d3(int p, int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
-    switch (p) {
-        case 1: return lines_m<R, 3, 2>(variant, src, prm, st, info, dry);
-        case 2: return lines_m<R, 3, 3>(variant, src, prm, st, info, dry);
-        case 3: return lines_m<R, 3, 4>(variant, src, prm, st, info, dry);
-        case 4: return lines_m<R, 3, 5>(variant, src, prm, st, info, dry);
-        case 5: return lines_m<R, 3, 6>(variant, src, prm, st, info, dry);
-        case 6: return lines_m<R, 3, 7>(variant, src, prm, st, info, dry);
-        case 7: return lines_m<R, 3, 8>(variant, src, prm, st, info, dry);
-        default: return kUnsupported;
-    }
-}
-
-template <class R>
-int run_lines_d2(int p, int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
-    switch (p) {
-        case 1: return lines_m<R, 2, 2>(variant, src, prm, st, info, dry);
-        case 2: return lines_m<R, 2, 3>(variant, src, prm, st, info, dry);
-        case 3: return lines_m<R, 2, 4>(variant, src, prm, st, info, dry);
-        case 4: return lines_m<R, 2, 5>(variant, src, prm, st, info, dry);
-        case 5: return lines_m<R, 2, 6>(variant, src, prm, st, info, dry);
-        case 6: return lines_m<R, 2, 7>(variant, src, prm, st, info, dry);
-        case 7: return lines_m<R, 2, 8>(variant, src, prm, st, info, dry);
-        case 8: return lines_m<R, 2, 9>(variant, src, prm, st, info, dry);
-        default: return kUnsupported;
+template <class R, int DIM, int VLO, int VHI>
+int run_lines_range(int p, int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
+    if (variant < VLO || variant > VHI) return kUnsupported;
+    if constexpr (DIM == 3) {
+        switch (p) {
+            case 1: return lines_m<R, 3, 2, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 2: return lines_m<R, 3, 3, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 3: return lines_m<R, 3, 4, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 4: return lines_m<R, 3, 5, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 5: return lines_m<R, 3, 6, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 6: return lines_m<R, 3, 7, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 7: return lines_m<R, 3, 8, VLO, VHI>(variant, src, prm, st, info, dry);
+            default: return kUnsupported;
+        }
+    } else {
+        switch (p) {
+            case 1: return lines_m<R, 2, 2, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 2: return lines_m<R, 2, 3, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 3: return lines_m<R, 2, 4, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 4: return lines_m<R, 2, 5, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 5: return lines_m<R, 2, 6, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 6: return lines_m<R, 2, 7, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 7: return lines_m<R, 2, 8, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 8: return lines_m<R, 2, 9, VLO, VHI>(variant, src, prm, st, info, dry);
+            default: return kUnsupported;
+        }
     }
 }
 
@@ -92,6 +85,26 @@ int run_planar_impl(int p, bool src, const Params<R>& prm, cudaStream_t st, KInf
         case 4: return planar_m<R, 5>(src, prm, st, info, dry);
         case 5: return planar_m<R, 6>(src, prm, st, info, dry);
         case 6: return planar_m<R, 7>(src, prm, st, info, dry);
+        default: return kUnsupported;
+    }
+}
+
+template <class R, int M>
+int planar_managed_m(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
+    constexpr int NE = planar_managed_ne<R, M>();
+    return src ? int(launch_planar_managed<R, M, NE, true>(prm, st, info, dry))
+               : int(launch_planar_managed<R, M, NE, false>(prm, st, info, dry));
+}
+
+template <class R>
+int run_planar_managed_impl(int p, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
+    switch (p) {
+        case 1: return planar_managed_m<R, 2>(src, prm, st, info, dry);
+        case 2: return planar_managed_m<R, 3>(src, prm, st, info, dry);
+        case 3: return planar_managed_m<R, 4>(src, prm, st, info, dry);
+        case 4: return planar_managed_m<R, 5>(src, prm, st, info, dry);
+        case 5: return planar_managed_m<R, 6>(src, prm, st, info, dry);
+        case 6: return planar_managed_m<R, 7>(src, prm, st, info, dry);
         default: return kUnsupported;
     }
 }
@@ -123,13 +136,24 @@ int run_unfused_impl(int d, int p, bool src, const Params<R>& prm, cudaStream_t 
     }
 }
 
-// Entry points defined in the instantiation units.
-int lines_f32_d3(int p, int variant, bool src, const Params<float>&, cudaStream_t, KInfo*, bool);
-int lines_f64_d3(int p, int variant, bool src, const Params<double>&, cudaStream_t, KInfo*, bool);
-int lines_f32_d2(int p, int variant, bool src, const Params<float>&, cudaStream_t, KInfo*, bool);
-int lines_f64_d2(int p, int variant, bool src, const Params<double>&, cudaStream_t, KInfo*, bool);
+// Entry points defined in the instantiation units (lines: variants 0-9 in *_lo, 10-15 in *_hi).
+#define HF_LINES_DECL(NAME, R)                                                                      \
+    int NAME##_lo(int p, int variant, bool src, const Params<R>&, cudaStream_t, KInfo*, bool);       \
+    int NAME##_hi(int p, int variant, bool src, const Params<R>&, cudaStream_t, KInfo*, bool);       \
+    inline int NAME(int p, int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, \
+                    bool dry) {                                                                     \
+        return variant < 10 ? NAME##_lo(p, variant, src, prm, st, info, dry)                        \
+                            : NAME##_hi(p, variant, src, prm, st, info, dry);                       \
+    }
+HF_LINES_DECL(lines_f32_d3, float)
+HF_LINES_DECL(lines_f64_d3, double)
+HF_LINES_DECL(lines_f32_d2, float)
+HF_LINES_DECL(lines_f64_d2, double)
+#undef HF_LINES_DECL
 int planar_f32(int p, bool src, const Params<float>&, cudaStream_t, KInfo*, bool);
 int planar_f64(int p, bool src, const Params<double>&, cudaStream_t, KInfo*, bool);
+int planar_managed_f32(int p, bool src, const Params<float>&, cudaStream_t, KInfo*, bool);
+int planar_managed_f64(int p, bool src, const Params<double>&, cudaStream_t, KInfo*, bool);
 int unfused_f32(int d, int p, bool src, const Params<float>&, cudaStream_t, KInfo*, bool);
 int unfused_f64(int d, int p, bool src, const Params<double>&, cudaStream_t, KInfo*, bool);
 

@@ -1,0 +1,8 @@
+// Instantiation unit: lines kernels, f32, d=2, variants 0-9.
+#include "hf_dispatch.cuh"
+namespace hfb {
+int lines_f32_d2_lo(int p, int variant, bool src, const Params<float>& prm, cudaStream_t st, KInfo* info,
+                     bool dry) {
+    return run_lines_range<float, 2, 0, 9>(p, variant, src, prm, st, info, dry);
+}
+}  // namespace hfb

@@ -50,27 +50,73 @@ constexpr int lines_ne_default() {
 
 // Lines variants.  NE0 = lines_ne_default (about three CTAs per SM).
 //   one chunk per CTA (hf_lines_kernel):        0: NE0   1: NE0/2   2: 2*NE0   7: NE0/4
-//   persistent TMA ring (hf_lines_pipe_kernel): 3: NE0 x2 stages   4: NE0/2 x3   5: NE0/2 x2
-//                                               6: NE0 x3          8: NE0/4 x3   9: NE0/4 x4
+//   persistent TMA ring (hf_lines_pipe_kernel), (elements, stages, consumer groups):
+//     3: (NE0, 2, 1)    4: (NE0/2, 3, 1)   5: (NE0/2, 2, 1)   6: (NE0, 3, 1)
+//     8: (NE0/4, 3, 1)  9: (NE0/4, 4, 1)
+//    10: (NE0/2, 4, 2) 11: (NE0/2, 6, 3)  12: (NE0/4, 8, 4)  13: (NE0/4, 6, 2)
+//    14: (NE0, 4, 2)   15: (NE0/4, 6, 3)
 // The contiguous bulk path accepts any NE >= 1 (hf_chunk_io.cuh), so the small-NE
 // variants exist for every order; a variant whose shape does not fit (shared
 // memory, 1024 threads) reports unsupported.
+constexpr int kLinesVariants = 16;
+
+// The measured selection (tools/select_methods.py -> hf_select_table.inc).
+struct SelRow {
+    int d, p, prec, method, variant;
+};
+constexpr SelRow kSelect[] = {
+#include "hf_select_table.inc"
+    {0, 0, 0, 0, 0}};
+
+// Which lines variants the library instantiates.  The production build carries
+// the selected variant of every (d, p, precision) plus variants 0 (one chunk per
+// CTA), 3 (TMA ring) and 10 (grouped TMA ring), so that every kernel form stays
+// parity-tested; the tuning build (make tuning, -DHF_TUNING) carries all of them
+// for tools/select_methods.py.
+template <class R, int DIM, int M, int VARIANT>
+constexpr bool variant_built() {
+#ifdef HF_TUNING
+    return true;
+#else
+    if (VARIANT == 0 || VARIANT == 3 || VARIANT == 10) return true;
+    for (const SelRow& r : kSelect)
+        if (r.d == DIM && r.p == M - 1 && r.prec == (sizeof(R) == 8 ? 1 : 0) && r.method == 2 && r.variant == VARIANT)
+            return true;
+    return false;
+#endif
+}
 template <int VARIANT>
 constexpr bool is_pipe_variant() {
-    return VARIANT == 3 || VARIANT == 4 || VARIANT == 5 || VARIANT == 6 || VARIANT == 8 || VARIANT == 9;
+    return !(VARIANT == 0 || VARIANT == 1 || VARIANT == 2 || VARIANT == 7);
 }
 template <class R, int DIM, int M, int VARIANT>
 constexpr int variant_ne() {
     constexpr int ne0 = lines_ne_default<R, DIM, M>();
-    constexpr int ne = (VARIANT == 0 || VARIANT == 3 || VARIANT == 6)   ? ne0
-                       : (VARIANT == 1 || VARIANT == 4 || VARIANT == 5) ? ne0 / 2
-                       : (VARIANT == 2)                                 ? ne0 * 2
-                                                                        : ne0 / 4;
+    constexpr int ne = (VARIANT == 0 || VARIANT == 3 || VARIANT == 6 || VARIANT == 14)     ? ne0
+                       : (VARIANT == 1 || VARIANT == 4 || VARIANT == 5 || VARIANT == 10 ||
+                          VARIANT == 11)                                                     ? ne0 / 2
+                       : (VARIANT == 2)                                                      ? ne0 * 2
+                                                                                             : ne0 / 4;
     return ne >= 1 ? ne : 0;
 }
 template <int VARIANT>
 constexpr int pipe_stages() {
-    return (VARIANT == 4 || VARIANT == 6 || VARIANT == 8) ? 3 : (VARIANT == 9 ? 4 : 2);
+    switch (VARIANT) {
+        case 4: case 6: case 8: return 3;
+        case 9: case 10: case 14: return 4;
+        case 11: case 13: case 15: return 6;
+        case 12: return 8;
+        default: return 2;
+    }
+}
+template <int VARIANT>
+constexpr int pipe_groups() {
+    switch (VARIANT) {
+        case 10: case 13: case 14: return 2;
+        case 11: case 15: return 3;
+        case 12: return 4;
+        default: return 1;
+    }
 }
 
 template <class R, int M>
@@ -157,11 +203,11 @@ inline int num_sms() {
 }
 
 // Persistent pipelined lines kernel over the whole chunks, guarded tail through hf_lines_kernel.
-template <class R, int DIM, int M, int NE, int STAGES, bool SRC>
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC>
 cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
-    using S = PipeShape<R, DIM, M, NE, STAGES>;
+    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS>;
     using L = LinesShape<R, DIM, M, NE>;
-    auto kernel = hf_lines_pipe_kernel<R, DIM, M, NE, STAGES, SRC>;
+    auto kernel = hf_lines_pipe_kernel<R, DIM, M, NE, STAGES, GROUPS, SRC>;
     const bool fast_layout = bulk_layout<R, NE>(p.group);
     long long n_full = p.n_elem / NE;
     // contiguous chunks load a 16-byte superset: keep the allocation's last chunk
@@ -187,8 +233,12 @@ cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dr
         info->shared_bytes = int(S::SMEM);
         info->grid = grid;
         info->bulk_path = fast_layout ? 1 : 0;
-        std::snprintf(info->name, sizeof(info->name), "hf_lines_pipe_d%d_p%d_%s_ne%d_s%d%s", DIM, M - 1,
-                      prec_name(sizeof(R)), NE, STAGES, SRC ? "_src" : "");
+        if (GROUPS == 1)
+            std::snprintf(info->name, sizeof(info->name), "hf_lines_pipe_d%d_p%d_%s_ne%d_s%d%s", DIM, M - 1,
+                          prec_name(sizeof(R)), NE, STAGES, SRC ? "_src" : "");
+        else
+            std::snprintf(info->name, sizeof(info->name), "hf_lines_pipe_d%d_p%d_%s_ne%d_s%d_g%d%s", DIM, M - 1,
+                          prec_name(sizeof(R)), NE, STAGES, GROUPS, SRC ? "_src" : "");
         if (dry) fill_regs(kernel, info);
     }
     if (dry || p.n_elem == 0) return cudaSuccess;
@@ -232,6 +282,40 @@ cudaError_t launch_planar(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
     return cudaGetLastError();
 }
 
+// Managed planar: the largest element count (<= planar_ne) whose staged chunk fits one CTA.
+template <class R, int M>
+constexpr int planar_managed_ne() {
+    int ne = planar_ne<R, M>();
+    while (ne > 1 && PlanarManagedShape<R, M, 1>::HDR + size_t(ne) * M * M * M * 13 * sizeof(R) + 48 >
+                         size_t(kMaxSmemPerCta))
+        ne /= 2;
+    return ne;
+}
+
+template <class R, int M, int NE, bool SRC>
+cudaError_t launch_planar_managed(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
+    using S = PlanarManagedShape<R, M, NE>;
+    auto kernel = hf_planar_managed_kernel<R, M, NE, SRC>;
+    const long long grid = (p.n_elem + NE - 1) / NE;
+    const bool fast_layout = bulk_layout<R, NE>(p.group);
+    if (info) {
+        info->method = 4;
+        info->elems_per_cta = NE;
+        info->block_threads = S::BS;
+        info->shared_bytes = int(S::SMEM);
+        info->grid = grid;
+        info->bulk_path = fast_layout ? 1 : 0;
+        std::snprintf(info->name, sizeof(info->name), "hf_planar_managed_d3_p%d_%s_ne%d%s", M - 1,
+                      prec_name(sizeof(R)), NE, SRC ? "_src" : "");
+        if (dry) fill_regs(kernel, info);
+    }
+    if (dry || p.n_elem == 0) return cudaSuccess;
+    p.fast_ok = fast_layout && aligned16(p.u) && aligned16(p.out);
+    if (int e = set_smem_attr(kernel, S::SMEM)) return cudaError_t(e);
+    kernel<<<dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st>>>(p);
+    return cudaGetLastError();
+}
+
 template <class R, int DIM, int M>
 cudaError_t launch_unfused(Params<R> p, bool src, cudaStream_t st, KInfo* info, bool dry) {
     const long long groups = (p.n_elem + p.group - 1) / p.group;
@@ -257,6 +341,8 @@ cudaError_t launch_unfused(Params<R> p, bool src, cudaStream_t st, KInfo* info, 
 // Return cudaErrorInvalidValue (as an int) for an unsupported combination.
 template <class R>
 int run_lines(int d, int p, int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry);
+template <class R>
+int run_planar_managed(int p, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry);
 template <class R>
 int run_planar(int p, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry);
 template <class R>

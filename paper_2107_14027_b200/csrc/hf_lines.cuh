@@ -33,6 +33,8 @@
 // kernel; padding elements are neither read nor written (render.hpp:95,102).
 #pragma once
 
+#include <type_traits>
+
 #include "hf_chunk_io.cuh"
 #include "hf_common.cuh"
 
@@ -97,43 +99,99 @@ __device__ __forceinline__ void lines_emit(R* __restrict__ q, R* __restrict__ a,
     }
 }
 
+// Word offset (inside a chunk) of the first point of line L of a sweep along A:
+// L = el + NE * r, r enumerating the two fixed indices (layout.hpp:128-134).
+template <int DIM, int M, int NE, int A>
+__host__ __device__ constexpr int line_offset(int L) {
+    const int el = L % NE;
+    const int r = L / NE;
+    int base_pt = r;                                  // d3 A=2: r = i + M j;  d2 A=1: r = i
+    if (A == 0) base_pt = M * r;                      // d3: r = j + M k;  d2: r = j
+    if (DIM == 3 && A == 1) base_pt = (r % M) + M * M * (r / M);  // r = i + M k
+    return el + NE * base_pt;
+}
+
+// Bank-conflict-free assignment of a sweep's lines to (iteration, thread).
+// A warp's shared-memory access is one wavefront per 128 B only if its lanes
+// hit distinct banks: for 4-byte words all 32 lanes need distinct word offsets
+// mod 32, for 8-byte words each half-warp needs distinct offsets mod 16
+// (measured on B200: a half-warp 2-way conflict doubles the wavefronts).  Every
+// point of a line is the line offset plus a per-(point, variable) constant, so
+// the class (offset mod 32 | 16) of the line decides.  The map deals the lines
+// of class c to lane c of warps 0, 1, ... (and lane c + 16 for 8-byte words);
+// a class with more lines than the slots of ITERS iterations spills into idle
+// slots (a conflict, but no extra iteration).  With the natural order (L = t,
+// t + NTHR, ...) the y-sweep conflicts whenever NE*m is not a multiple of the
+// bank count (e.g. 2-way at p6 FP64).  Built at compile time; 0xFFFF = idle.
+template <class R, int DIM, int M, int NE, int A, int NTHR>
+struct LineMap {
+    static constexpr int LINES = NE * ipow_c(M, DIM - 1);
+    static constexpr int ITERS = (LINES + NTHR - 1) / NTHR;
+    static constexpr int N = ITERS * NTHR;
+    unsigned short off[N];
+};
+
+template <class R, int DIM, int M, int NE, int A, int NTHR>
+constexpr LineMap<R, DIM, M, NE, A, NTHR> make_line_map() {
+    using LM = LineMap<R, DIM, M, NE, A, NTHR>;
+    constexpr int B = sizeof(R) == 4 ? 32 : 16;  // bank classes per (half-)warp
+    constexpr int HALVES = 32 / B;
+    constexpr int NW = NTHR / 32;
+    LM m{};
+    for (int i = 0; i < LM::N; ++i) m.off[i] = 0xFFFF;
+    int next[B] = {};
+    int spill[LM::LINES > 0 ? LM::LINES : 1] = {};
+    int n_spill = 0;
+    for (int L = 0; L < LM::LINES; ++L) {
+        const int o = line_offset<DIM, M, NE, A>(L);
+        const int c = o % B;
+        const int idx = next[c]++;
+        const int it = idx / (NW * HALVES);
+        if (it >= LM::ITERS) {
+            spill[n_spill++] = o;
+            continue;
+        }
+        const int rem = idx % (NW * HALVES);
+        const int slot = it * NTHR + (rem / HALVES) * 32 + (rem % HALVES) * B + c;
+        m.off[slot] = static_cast<unsigned short>(o);
+    }
+    for (int i = 0, k = 0; k < n_spill && i < LM::N; ++i)
+        if (m.off[i] == 0xFFFF) m.off[i] = static_cast<unsigned short>(spill[k++]);
+    return m;
+}
+
+template <class R, int DIM, int M, int NE, int A, int NTHR>
+__device__ const LineMap<R, DIM, M, NE, A, NTHR> kLineMap = make_line_map<R, DIM, M, NE, A, NTHR>();
+
 // One sweep along axis A.  PHASE: 0 = first sweep, 1 = middle, 2 = last.
+// `o` = the line's first word inside the chunk (line_offset()).
 template <class R, int DIM, int M, int NE, bool SRC, int A, int PHASE>
-__device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ acc, const Params<R>& p, int L) {
+__device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ acc, const Params<R>& p, int o) {
     using S = LinesShape<R, DIM, M, NE>;
     constexpr int NP = S::NP;
     constexpr int VS = NE * NP;  // word stride between variables
     constexpr int STRIDE = (A == 0) ? 1 : (A == 1) ? M : M * M;  // point stride along the line
 
-    const int el = L % NE;
-    const int r = L / NE;
-    int base_pt;
-    if constexpr (DIM == 3) {
-        if constexpr (A == 0) base_pt = M * r;  // r = j + M k  ->  M j + M^2 k
-        else if constexpr (A == 1) base_pt = (r % M) + M * M * (r / M);  // r = i + M k
-        else base_pt = r;  // r = i + M j
-    } else {
-        if constexpr (A == 0) base_pt = M * r;  // r = j
-        else base_pt = r;  // r = i
-    }
-    R* __restrict__ sb = s + el + NE * base_pt;
-    R* __restrict__ ab = acc + el + NE * base_pt;
+    R* __restrict__ sb = s + o;
+    R* __restrict__ ab = acc + o;
 
     const R nu = p.nu;
-    R V[DIM][M];
-    R Q[DIM][M];
+    using PR = Pair<R>;
+    // W[b][t] = (V_b, M_ba) at line point t: both lines are contracted with the same D rows
+    PR W[DIM][M];
 #pragma unroll
     for (int t = 0; t < M; ++t) {
         const R* q = sb + NE * STRIDE * t;
         const R P = q[0];
+        R V[DIM];
 #pragma unroll
-        for (int b = 0; b < DIM; ++b) V[b][t] = q[VS * (1 + b)];
+        for (int b = 0; b < DIM; ++b) V[b] = q[VS * (1 + b)];
 #pragma unroll
         for (int b = 0; b < DIM; ++b) {
             const R g = q[VS * var_grad_c(DIM, b, A)];
             // codegen_util.hpp:191-202 operation order: base, then fma(V_b, V_a, base)
             const R base = (b == A) ? fma(-nu, g, P) : (-nu) * g;
-            Q[b][t] = fma(V[b][t], V[A][t], base);
+            W[b][t] = PR::make(V[b], fma(V[b], V[A], base));
         }
     }
 
@@ -141,93 +199,74 @@ __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ a
     // (Params::DE/DO/DC), about half the FMAs of the dense m x m contraction; it
     // lengthens the dependency chain, which only pays off at high order (measured:
     // p6 +14 % FP64, p3 -5 %), so lower orders use the dense contraction.
-#define HF_EMIT(I, DV, DQ) lines_emit<R, DIM, M, NE, SRC, A, PHASE>(sb + NE * STRIDE * (I), ab + NE * STRIDE * (I), p, DV, DQ)
+#define HF_EMIT(I, DP)                                                                                         \
+    do {                                                                                                        \
+        R dV_[DIM], dQ_[DIM];                                                                                  \
+        _Pragma("unroll") for (int b_ = 0; b_ < DIM; ++b_) {                                                   \
+            dV_[b_] = (DP)[b_].x();                                                                            \
+            dQ_[b_] = (DP)[b_].y();                                                                            \
+        }                                                                                                      \
+        lines_emit<R, DIM, M, NE, SRC, A, PHASE>(sb + NE * STRIDE * (I), ab + NE * STRIDE * (I), p, dV_, dQ_); \
+    } while (0)
     if constexpr (M < HF_EVEN_ODD_MIN_M) {
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            R dV[DIM], dQ[DIM];
+            PR d[DIM];
 #pragma unroll
-            for (int b = 0; b < DIM; ++b) {
-                dV[b] = p.D[i * M] * V[b][0];
-                dQ[b] = p.D[i * M] * Q[b][0];
-            }
+            for (int b = 0; b < DIM; ++b) d[b] = pmul(p.D[i * M], W[b][0]);
 #pragma unroll
             for (int t = 1; t < M; ++t)
 #pragma unroll
-                for (int b = 0; b < DIM; ++b) {
-                    dV[b] = fma(p.D[i * M + t], V[b][t], dV[b]);
-                    dQ[b] = fma(p.D[i * M + t], Q[b][t], dQ[b]);
-                }
-            HF_EMIT(i, dV, dQ);
+                for (int b = 0; b < DIM; ++b) d[b] = pfma(p.D[i * M + t], W[b][t], d[b]);
+            HF_EMIT(i, d);
         }
     } else {
         constexpr int H = M / 2;
         constexpr int K = kMaxH;
-        // symmetric / antisymmetric parts, in place: V[b][t] <- S_t, V[b][M-1-t] <- A_t
+        // symmetric / antisymmetric parts, in place: W[b][t] <- S_t, W[b][M-1-t] <- A_t
 #pragma unroll
         for (int t = 0; t < H; ++t)
 #pragma unroll
             for (int b = 0; b < DIM; ++b) {
-                const R v0 = V[b][t], v1 = V[b][M - 1 - t], q0 = Q[b][t], q1 = Q[b][M - 1 - t];
-                V[b][t] = v0 + v1;
-                V[b][M - 1 - t] = v0 - v1;
-                Q[b][t] = q0 + q1;
-                Q[b][M - 1 - t] = q0 - q1;
+                const PR w0 = W[b][t], w1 = W[b][M - 1 - t];
+                W[b][t] = padd(w0, w1);
+                W[b][M - 1 - t] = psub(w0, w1);
             }
 #pragma unroll
         for (int i = 0; i < H; ++i) {
-            R xV[DIM], yV[DIM], xQ[DIM], yQ[DIM];
+            PR x[DIM], y[DIM];
 #pragma unroll
             for (int b = 0; b < DIM; ++b) {
-                xV[b] = p.DE[i * K] * V[b][0];
-                yV[b] = p.DO[i * K] * V[b][M - 1];
-                xQ[b] = p.DE[i * K] * Q[b][0];
-                yQ[b] = p.DO[i * K] * Q[b][M - 1];
+                x[b] = pmul(p.DE[i * K], W[b][0]);
+                y[b] = pmul(p.DO[i * K], W[b][M - 1]);
             }
 #pragma unroll
             for (int t = 1; t < H; ++t)
 #pragma unroll
                 for (int b = 0; b < DIM; ++b) {
-                    xV[b] = fma(p.DE[i * K + t], V[b][t], xV[b]);
-                    yV[b] = fma(p.DO[i * K + t], V[b][M - 1 - t], yV[b]);
-                    xQ[b] = fma(p.DE[i * K + t], Q[b][t], xQ[b]);
-                    yQ[b] = fma(p.DO[i * K + t], Q[b][M - 1 - t], yQ[b]);
+                    x[b] = pfma(p.DE[i * K + t], W[b][t], x[b]);
+                    y[b] = pfma(p.DO[i * K + t], W[b][M - 1 - t], y[b]);
                 }
             if constexpr (M % 2 == 1)
 #pragma unroll
-                for (int b = 0; b < DIM; ++b) {
-                    xV[b] = fma(p.DC[i], V[b][H], xV[b]);
-                    xQ[b] = fma(p.DC[i], Q[b][H], xQ[b]);
-                }
-            R dV[DIM], dQ[DIM];
+                for (int b = 0; b < DIM; ++b) x[b] = pfma(p.DC[i], W[b][H], x[b]);
+            PR d[DIM];
 #pragma unroll
-            for (int b = 0; b < DIM; ++b) {
-                dV[b] = xV[b] + yV[b];
-                dQ[b] = xQ[b] + yQ[b];
-            }
-            HF_EMIT(i, dV, dQ);
+            for (int b = 0; b < DIM; ++b) d[b] = padd(x[b], y[b]);
+            HF_EMIT(i, d);
 #pragma unroll
-            for (int b = 0; b < DIM; ++b) {
-                dV[b] = yV[b] - xV[b];
-                dQ[b] = yQ[b] - xQ[b];
-            }
-            HF_EMIT(M - 1 - i, dV, dQ);
+            for (int b = 0; b < DIM; ++b) d[b] = psub(y[b], x[b]);
+            HF_EMIT(M - 1 - i, d);
         }
         if constexpr (M % 2 == 1) {
-            R dV[DIM], dQ[DIM];
+            PR d[DIM];
 #pragma unroll
-            for (int b = 0; b < DIM; ++b) {
-                dV[b] = p.DO[H * K] * V[b][M - 1];
-                dQ[b] = p.DO[H * K] * Q[b][M - 1];
-            }
+            for (int b = 0; b < DIM; ++b) d[b] = pmul(p.DO[H * K], W[b][M - 1]);
 #pragma unroll
             for (int t = 1; t < H; ++t)
 #pragma unroll
-                for (int b = 0; b < DIM; ++b) {
-                    dV[b] = fma(p.DO[H * K + t], V[b][M - 1 - t], dV[b]);
-                    dQ[b] = fma(p.DO[H * K + t], Q[b][M - 1 - t], dQ[b]);
-                }
-            HF_EMIT(H, dV, dQ);
+                for (int b = 0; b < DIM; ++b) d[b] = pfma(p.DO[H * K + t], W[b][M - 1 - t], d[b]);
+            HF_EMIT(H, d);
         }
     }
 }
@@ -238,43 +277,64 @@ __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ a
 // HEADB is a template parameter so that every shared-memory address in the
 // sweeps is a compile-time offset from the __shared__ window (a runtime base
 // costs ~30 registers and ~10 % of HBM throughput, measured).  BAR: 0 = the
-// whole CTA (__syncthreads), 1 = the NTHR consumer threads (named barrier 1).
+// whole CTA (__syncthreads), k > 0 = the NTHR threads of one consumer group
+// (named barrier k), -1 = named barrier `bar_id` (runtime).
 template <class R, int DIM, int M, int NE, bool SRC, int HEADB, int BAR, int NTHR>
-__device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const Params<R>& p, int t) {
+__device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const Params<R>& p, int t, int bar_id = 0) {
     using S = LinesShape<R, DIM, M, NE>;
     R* s = reinterpret_cast<R*>(buf + HEADB);
-    auto sync = [] {
+#ifdef HF_IO_ONLY  // measurement build: chunk traffic only, no sweeps (tools/gpu_ab_io.sh)
+    return;
+#endif
+    auto sync = [&] {
         if constexpr (BAR == 0) __syncthreads();
-        else named_bar_sync(1, NTHR);
+        else if constexpr (BAR < 0) named_bar_sync(bar_id, NTHR);  // runtime barrier id (consumer groups)
+        else named_bar_sync(BAR, NTHR);
     };
+    // lines of sweep A in the bank-conflict-free order of kLineMap
+    auto sweep = [&](auto a_tag, auto phase_tag) {
+        constexpr int A = decltype(a_tag)::value;
+        constexpr int PH = decltype(phase_tag)::value;
+        using LM = LineMap<R, DIM, M, NE, A, NTHR>;
+        const unsigned short* map = kLineMap<R, DIM, M, NE, A, NTHR>.off;
+#pragma unroll 1
+        for (int k = 0; k < LM::ITERS; ++k) {
+            const int o = map[k * NTHR + t];
+            if (o != 0xFFFF) lines_sweep<R, DIM, M, NE, SRC, A, PH>(s, acc, p, o);
+        }
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
     if constexpr (DIM == 3) {
-        for (int L = t; L < S::LINES; L += NTHR) lines_sweep<R, 3, M, NE, SRC, 0, 0>(s, acc, p, L);
+        sweep(I0{}, I0{});
         sync();
-        for (int L = t; L < S::LINES; L += NTHR) lines_sweep<R, 3, M, NE, SRC, 1, 1>(s, acc, p, L);
+        sweep(I1{}, I1{});
         sync();
-        for (int L = t; L < S::LINES; L += NTHR) lines_sweep<R, 3, M, NE, SRC, 2, 2>(s, acc, p, L);
+        sweep(I2{}, I2{});
     } else {
-        for (int L = t; L < S::LINES; L += NTHR) lines_sweep<R, 2, M, NE, SRC, 0, 0>(s, acc, p, L);
+        sweep(I0{}, I0{});
         sync();
-        for (int L = t; L < S::LINES; L += NTHR) lines_sweep<R, 2, M, NE, SRC, 1, 2>(s, acc, p, L);
+        sweep(I1{}, I2{});
     }
 }
 
 // Runtime head (bytes, a multiple of sizeof(R), < 16) -> compile-time HEADB.
 // Chunks whose byte size is a multiple of 16 always start aligned: one instance.
 template <class R, int DIM, int M, int NE, bool SRC, int BAR, int NTHR>
-__device__ __forceinline__ void lines_sweeps_at(unsigned char* buf, int head, R* acc, const Params<R>& p, int t) {
+__device__ __forceinline__ void lines_sweeps_at(unsigned char* buf, int head, R* acc, const Params<R>& p, int t,
+                                                int bar_id = 0) {
     if constexpr (LinesShape<R, DIM, M, NE>::IN_BYTES % 16 == 0) {
-        lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR>(buf, acc, p, t);
+        lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR>(buf, acc, p, t, bar_id);
     } else if constexpr (sizeof(R) == 8) {
-        if (head == 0) lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR>(buf, acc, p, t);
-        else lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR>(buf, acc, p, t);
+        if (head == 0) lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR>(buf, acc, p, t, bar_id);
+        else lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR>(buf, acc, p, t, bar_id);
     } else {
         switch (head) {
-            case 0: lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR>(buf, acc, p, t); break;
-            case 4: lines_sweeps<R, DIM, M, NE, SRC, 4, BAR, NTHR>(buf, acc, p, t); break;
-            case 8: lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR>(buf, acc, p, t); break;
-            default: lines_sweeps<R, DIM, M, NE, SRC, 12, BAR, NTHR>(buf, acc, p, t); break;
+            case 0: lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR>(buf, acc, p, t, bar_id); break;
+            case 4: lines_sweeps<R, DIM, M, NE, SRC, 4, BAR, NTHR>(buf, acc, p, t, bar_id); break;
+            case 8: lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR>(buf, acc, p, t, bar_id); break;
+            default: lines_sweeps<R, DIM, M, NE, SRC, 12, BAR, NTHR>(buf, acc, p, t, bar_id); break;
         }
     }
 }

@@ -1,51 +1,107 @@
 // hf_lines_pipe.cuh -- persistent, warp-specialised form of the lines kernel.
 //
-// Same arithmetic as hf_lines.cuh (three register-line sweeps per chunk), but
-// the chunk traffic is decoupled from the compute with a STAGES-deep ring of
-// shared-memory chunk buffers fed by cp.async.bulk:
+// Same arithmetic as hf_lines.cuh (d register-line sweeps per chunk), but the
+// chunk traffic is decoupled from the compute with a STAGES-deep ring of
+// shared-memory chunk buffers fed by cp.async.bulk, and the compute is split
+// over GROUPS independent consumer groups:
 //
 //   warp 0 (producer)  : keeps up to STAGES chunks in flight.  For each chunk
-//                        it waits for the consumers to finish the stage; then
-//                        every lane bulk-stores its 1/32 slice of the finished
-//                        divergence, waits for that slice to have left shared
-//                        memory, and reloads the slice with the chunk STAGES
-//                        ahead (mbarrier complete_tx) -- stores and loads of a
-//                        stage overlap slice by slice.
-//   warps 1.. (consumers): wait full[s], run the d sweeps on stage s (named
-//                        barrier 1 between sweeps), fence the generic-proxy
-//                        writes for the async proxy, arrive computed[s].
+//                        it waits for the owning group to finish the stage;
+//                        then every lane bulk-stores its 1/32 slice of the
+//                        finished divergence, waits for that slice to have
+//                        left shared memory, and reloads the slice with the
+//                        chunk STAGES ahead (mbarrier complete_tx) -- stores and
+//                        loads of a stage overlap slice by slice.
+//   consumer group g   : chunks it = g, g+GROUPS, ... on its own SPG =
+//   (warps 1+g*W ..)     STAGES/GROUPS stages (s = g*SPG + (it/GROUPS) % SPG):
+//                        wait full[s], run the d sweeps (named barrier 1+g
+//                        between sweeps, a private accumulator region), fence
+//                        the generic-proxy writes for the async proxy, arrive
+//                        computed[s].
+//
+// Why groups: a chunk's compute parallelism is its line count (NE * m^(d-1)),
+// so with one group the ring can hold only STAGES = smem / chunk chunks and the
+// SM computes one chunk at a time; with GROUPS groups the chunks can be GROUPS
+// times smaller for the same number of computing warps, so more of them are in
+// flight (STAGES - GROUPS being stored / loaded), and one group's barrier and
+// shared-memory latency stalls are covered by the other groups' work.
 //
 // One CTA per SM slot, chunks assigned round-robin (all chunks cost the same).
 // Only whole chunks inside one AoSoA group run here (group % NE == 0, 16-byte
-// rows); the guarded tail goes through hf_lines_kernel with chunk0 = n_chunks.
+// rows, or group == NE); the guarded tail goes through hf_lines_kernel with
+// chunk0 = n_chunks.
 #pragma once
 
 #include "hf_lines.cuh"
 
 namespace hfb {
 
-template <class R, int DIM, int M, int NE, int STAGES>
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS = 1>
 struct PipeShape {
     using L = LinesShape<R, DIM, M, NE>;
-    static constexpr int NCONS = ((L::LINES + 31) / 32) * 32;  // consumer threads
-    static constexpr int BS = NCONS + 32;                     // + producer warp
-    static constexpr int HDR = 128;                           // 2*STAGES mbarriers (<= 16)
+    static_assert(STAGES % GROUPS == 0, "every group owns STAGES / GROUPS stages");
+    static constexpr int SPG = STAGES / GROUPS;               // stages per group
+    static constexpr int NCONS = ((L::LINES + 31) / 32) * 32;  // consumer threads per group
+    static constexpr int BS = GROUPS * NCONS + 32;            // + producer warp
+    static constexpr int HDR = 256;                           // 2*STAGES mbarriers (<= 32)
     static constexpr size_t STAGE_BYTES = size_t(L::BUF_BYTES);
-    static constexpr size_t SMEM = HDR + STAGES * STAGE_BYTES + size_t(L::ACC_WORDS) * sizeof(R);
+    static constexpr size_t ACC_BYTES = ((size_t(L::ACC_WORDS) * sizeof(R) + 127) / 128) * 128;
+    static constexpr size_t SMEM = HDR + STAGES * STAGE_BYTES + GROUPS * ACC_BYTES;
     static_assert(2 * STAGES * 8 <= HDR, "mbarrier header too small");
+    static_assert(GROUPS <= 15, "one named barrier per group");
 };
 
-template <class R, int DIM, int M, int NE, int STAGES, bool SRC>
-__global__ void __launch_bounds__(PipeShape<R, DIM, M, NE, STAGES>::BS)
+// Consumer group g: its chunks on its SPG stages.  The stage index inside the
+// group is unrolled (compile-time offsets); the group's base (stages and
+// accumulator region) is a runtime offset from the __shared__ window, so every
+// group runs the same code -- one copy of the sweeps per stage, not per
+// (group, stage), which keeps the kernel inside the instruction cache.
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC>
+__device__ __forceinline__ void pipe_consume(unsigned char* smem_raw, uint64_t* full, uint64_t* computed,
+                                             const Params<R>& p, long long count, long long first, long long step,
+                                             int g, int ct) {
+    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS>;
+    using L = LinesShape<R, DIM, M, NE>;
+    using IO = typename L::IO;
+    constexpr int SPG = S::SPG;
+    const bool contiguous = (p.group == NE);
+    R* acc = reinterpret_cast<R*>(smem_raw + S::HDR + STAGES * S::STAGE_BYTES + size_t(g) * S::ACC_BYTES);
+    unsigned char* gbuf = smem_raw + S::HDR + size_t(g) * SPG * S::STAGE_BYTES;
+    for (long long q0 = 0; g + q0 * GROUPS < count; q0 += SPG) {
+        const uint32_t ph = uint32_t((q0 / SPG) & 1);
+#pragma unroll
+        for (int j = 0; j < SPG; ++j) {
+            const long long it = g + (q0 + j) * GROUPS;
+            if (it >= count) break;
+            const int s = g * SPG + j;
+            const long long E0 = (first + it * step) * NE;
+            const long long grp = E0 / p.group;
+            const long long cb = grp * p.group_words + (E0 - grp * p.group);
+            unsigned char* buf = gbuf + size_t(j) * S::STAGE_BYTES;
+            mbar_wait_parity(&full[s], ph);
+            if constexpr (GROUPS == 1)
+                lines_sweeps_at<R, DIM, M, NE, SRC, 1, S::NCONS>(buf, IO::head_bytes(p.u + cb, contiguous), acc, p,
+                                                                 ct);
+            else
+                lines_sweeps_at<R, DIM, M, NE, SRC, -1, S::NCONS>(buf, IO::head_bytes(p.u + cb, contiguous), acc,
+                                                                  p, ct, 1 + g);
+            fence_proxy_async_smem();
+            named_bar_sync(1 + g, S::NCONS);
+            if (ct == 0) mbar_arrive(&computed[s]);
+        }
+    }
+}
+
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC>
+__global__ void __launch_bounds__(PipeShape<R, DIM, M, NE, STAGES, GROUPS>::BS)
     hf_lines_pipe_kernel(const __grid_constant__ Params<R> p) {
     using L = LinesShape<R, DIM, M, NE>;
-    using S = PipeShape<R, DIM, M, NE, STAGES>;
-    constexpr int ROWS = L::NP * L::NV;
+    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS>;
+    constexpr int SPG = S::SPG;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
     uint64_t* computed = full + STAGES;
     unsigned char* stage0 = smem_raw + S::HDR;
-    R* acc = reinterpret_cast<R*>(stage0 + size_t(STAGES) * S::STAGE_BYTES);
     using IO = typename L::IO;
 
     const int tid = threadIdx.x;
@@ -70,18 +126,21 @@ __global__ void __launch_bounds__(PipeShape<R, DIM, M, NE, STAGES>::BS)
         const long long grp = E0 / p.group;
         return grp * p.group_words + (E0 - grp * p.group);
     };
+    // stage of the CTA's it-th chunk: group it % GROUPS, its (it / GROUPS)-th chunk
+    auto stage_of = [&](long long it) -> int { return int(it % GROUPS) * SPG + int((it / GROUPS) % SPG); };
 
     if (warp == 0) {
         // ---------------- producer ----------------
         const long long pre = count < STAGES ? count : STAGES;
         for (long long it = 0; it < pre; ++it) {
+            const int s = stage_of(it);
             const R* src = p.u + chunk_base(it);
-            if (lane == 0) mbar_arrive_expect_tx(&full[it], IO::tx_bytes(src, contiguous));
+            if (lane == 0) mbar_arrive_expect_tx(&full[s], IO::tx_bytes(src, contiguous));
             __syncwarp();
-            IO::load(stage0 + it * S::STAGE_BYTES, src, p.group, contiguous, &full[it], lane);
+            IO::load(stage0 + size_t(s) * S::STAGE_BYTES, src, p.group, contiguous, &full[s], lane);
         }
         for (long long it = 0; it < count; ++it) {
-            const int s = int(it % STAGES);
+            const int s = stage_of(it);
             const uint32_t ph = uint32_t((it / STAGES) & 1);
             unsigned char* buf = stage0 + size_t(s) * S::STAGE_BYTES;
             mbar_wait_parity(&computed[s], ph);
@@ -99,25 +158,10 @@ __global__ void __launch_bounds__(PipeShape<R, DIM, M, NE, STAGES>::BS)
         return;
     }
 
-    // ---------------- consumers ----------------
-    // The stage loop is unrolled so that each stage's buffer is a compile-time
-    // offset into the __shared__ window (see lines_sweeps).
-    const int ct = tid - 32;
-    for (long long it0 = 0; it0 < count; it0 += STAGES) {
-        const uint32_t ph = uint32_t((it0 / STAGES) & 1);
-#pragma unroll
-        for (int s = 0; s < STAGES; ++s) {
-            const long long it = it0 + s;
-            if (it >= count) break;
-            const long long cb = chunk_base(it);
-            unsigned char* buf = smem_raw + S::HDR + size_t(s) * S::STAGE_BYTES;
-            mbar_wait_parity(&full[s], ph);
-            lines_sweeps_at<R, DIM, M, NE, SRC, 1, S::NCONS>(buf, IO::head_bytes(p.u + cb, contiguous), acc, p, ct);
-            fence_proxy_async_smem();
-            named_bar_sync(1, S::NCONS);
-            if (ct == 0) mbar_arrive(&computed[s]);
-        }
-    }
+    // ---------------- consumer groups ----------------
+    const int g = (tid - 32) / S::NCONS;
+    const int ct = (tid - 32) - g * S::NCONS;
+    pipe_consume<R, DIM, M, NE, STAGES, GROUPS, SRC>(smem_raw, full, computed, p, count, first, step, g, ct);
 }
 
 }  // namespace hfb

@@ -20,6 +20,7 @@
 // bank-conflict free (the banks.hpp:110-120 deconfliction, done statically).
 #pragma once
 
+#include "hf_chunk_io.cuh"
 #include "hf_common.cuh"
 
 namespace hfb {
@@ -162,6 +163,157 @@ __global__ void __launch_bounds__(PlanarShape<R, M, NE>::BS)
             }
         }
         if (i + 1 < M) __syncthreads();  // the next plane overwrites the buffer
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Managed planar (Method::PlanarManaged, codegen_planar.hpp:276-300 + the
+// generation-time MemoryManager, memory_manager.hpp:57-191).
+//
+// The reference's manager is a greedy allocator: with enough shared capacity
+// every operand the planar emitter requests -- the y-z plane slices (high
+// priority) and the x-line neighbours (low priority, load_x_value :229-240) --
+// ends up resident in shared memory, and global memory is read exactly once.
+// On B200 the per-CTA capacity (227 KB) holds whole element chunks, so the
+// managed kernel realises the manager's fixed point directly: the CTA's NE
+// elements are staged into shared memory with cp.async.bulk (hf_chunk_io.cuh),
+// and the planar algorithm (same thread mapping, same accumulation order, hence
+// bit-identical results to hf_planar_kernel) reads its y-line, x-line and
+// z-line operands from the staged chunk.  Outputs go straight to global memory
+// (coalesced over the element index), so the staged input stays intact for
+// the neighbouring threads.
+// ---------------------------------------------------------------------------------------------
+template <class R, int M, int NE>
+struct PlanarManagedShape {
+    static constexpr int NV = 13;
+    static constexpr int NP = M * M * M;
+    static constexpr int NT = NE * M;                // compute threads: (element, z-plane)
+    static constexpr int BS = ((NT + 31) / 32) * 32;  // whole warps: the bulk copies are split over 32 lanes
+    static constexpr int HDR = 128;
+    static constexpr int IN_BYTES = NE * NP * NV * int(sizeof(R));
+    using IO = ChunkIO<R, NE, NP * NV, IN_BYTES>;
+    static constexpr size_t SMEM = HDR + size_t(IO::BUF_BYTES);
+};
+
+template <class R, int M, int NE, bool SRC>
+__global__ void __launch_bounds__(PlanarManagedShape<R, M, NE>::BS)
+    hf_planar_managed_kernel(const __grid_constant__ Params<R> p) {
+    using S = PlanarManagedShape<R, M, NE>;
+    using IO = typename S::IO;
+    constexpr int NP = S::NP, NV = S::NV, BS = S::BS;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    unsigned char* buf = smem_raw + S::HDR;
+
+    const int tid = threadIdx.x;
+    const long long E0 = static_cast<long long>(blockIdx.x) * NE;
+    const long long grp = E0 / p.group;
+    const int el0 = static_cast<int>(E0 - grp * p.group);
+    const long long gbase = grp * p.group_words + el0;
+    const bool contiguous = (p.group == NE);
+    bool fast = p.fast_ok && E0 + NE <= p.n_elem;
+    if (fast && contiguous)  // the 16-byte superset must stay inside the allocation
+        fast = ((gbase + NE * NP * NV) * (long long)sizeof(R) + 15) / 16 * 16 <= p.total_words * (long long)sizeof(R);
+    const int head = fast ? IO::head_bytes(p.u + gbase, contiguous) : 0;
+
+    // ---------------- stage the chunk (the manager's resident set) ----------------
+    if (fast) {
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (tid < 32) {
+            if (tid == 0) mbar_arrive_expect_tx(bar, IO::tx_bytes(p.u + gbase, contiguous));
+            __syncwarp();
+            IO::load(buf, p.u + gbase, p.group, contiguous, bar, tid);
+        }
+        mbar_wait_parity(bar, 0);
+    } else {
+        R* s0 = reinterpret_cast<R*>(buf);
+        for (int idx = tid; idx < NE * NP * NV; idx += BS) {
+            const long long e = E0 + idx % NE;
+            R v = R(0);
+            if (e < p.n_elem) {
+                const long long ge = e / p.group;
+                v = ld_stream(p.u + ge * p.group_words + (e - ge * p.group) + static_cast<long long>(p.group) * (idx / NE));
+            }
+            s0[idx] = v;
+        }
+        __syncthreads();
+    }
+    const R* __restrict__ s = reinterpret_cast<const R*>(buf + head);
+    if (tid >= S::NT) return;  // padding lanes of the last warp only help staging
+
+    const int el = tid % NE;
+    const int kp = tid / NE;
+    const long long e = E0 + el;
+    const bool act = e < p.n_elem;
+    const long long ge = act ? e / p.group : 0;
+    R* __restrict__ ob = p.out + ge * p.group_words + (e - ge * p.group);
+    const long long G = p.group;
+    auto sofs = [&](int i, int j, int k, int v) -> int { return el + NE * (i + M * j + M * M * k + NP * v); };
+    auto gofs = [&](int i, int j, int k, int v) -> long long {
+        return G * static_cast<long long>(i + M * j + M * M * k + NP * v);
+    };
+
+    R rDz[M];
+#pragma unroll
+    for (int t = 0; t < M; ++t) rDz[t] = p.D[kp * M + t];
+
+#pragma unroll 1
+    for (int i = 0; i < M; ++i) {
+        R rY[M][NV];  // plane slice: y-line (i, *, kp) (high-priority request, :118-131)
+#pragma unroll
+        for (int j = 0; j < M; ++j)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) rY[j][v] = s[sofs(i, j, kp, v)];
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            R tx[13], ty[13], tz[13];
+#pragma unroll
+            for (int i2 = 0; i2 < M; ++i2) {  // x line: resident neighbours (load_x_value, :229-240)
+                R P, V[3], Gc[3];
+                P = s[sofs(i2, j, kp, 0)];
+#pragma unroll
+                for (int b = 0; b < 3; ++b) {
+                    V[b] = s[sofs(i2, j, kp, 1 + b)];
+                    Gc[b] = s[sofs(i2, j, kp, var_grad_c(3, b, 0))];
+                }
+                accumulate_column<R, 0>(tx, i2 == 0, p.D[i * M + i2], P, V, Gc, p);
+            }
+#pragma unroll
+            for (int j2 = 0; j2 < M; ++j2) {  // y line from registers
+                const R V[3] = {rY[j2][1], rY[j2][2], rY[j2][3]};
+                const R Gc[3] = {rY[j2][var_grad_c(3, 0, 1)], rY[j2][var_grad_c(3, 1, 1)],
+                                 rY[j2][var_grad_c(3, 2, 1)]};
+                accumulate_column<R, 1>(ty, j2 == 0, p.D[j * M + j2], rY[j2][0], V, Gc, p);
+            }
+#pragma unroll
+            for (int k2 = 0; k2 < M; ++k2) {  // z line from the resident plane
+                const R V[3] = {s[sofs(i, j, k2, 1)], s[sofs(i, j, k2, 2)], s[sofs(i, j, k2, 3)]};
+                const R Gc[3] = {s[sofs(i, j, k2, var_grad_c(3, 0, 2))], s[sofs(i, j, k2, var_grad_c(3, 1, 2))],
+                                 s[sofs(i, j, k2, var_grad_c(3, 2, 2))]};
+                accumulate_column<R, 2>(tz, k2 == 0, rDz[k2], s[sofs(i, j, k2, 0)], V, Gc, p);
+            }
+            if (act) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const bool hx = v <= 3 || (v >= 4 && (v - 4) % 3 == 0);
+                    const bool hy = v <= 3 || (v >= 4 && (v - 4) % 3 == 1);
+                    const bool hz = v <= 3 || (v >= 4 && (v - 4) % 3 == 2);
+                    R r = R(0);
+                    bool have = false;
+                    if (hx) { r = p.jac[0] * tx[v]; have = true; }
+                    if (hy) { r = have ? fma(p.jac[1], ty[v], r) : p.jac[1] * ty[v]; have = true; }
+                    if (hz) { r = have ? fma(p.jac[2], tz[v], r) : p.jac[2] * tz[v]; }
+                    R o = -r;
+                    if constexpr (SRC)
+                        if (v >= 4) o = fma(-p.invT, rY[j][v], o);
+                    ob[gofs(i, j, kp, v)] = o;
+                }
+            }
+        }
     }
 }
 

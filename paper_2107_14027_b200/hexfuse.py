@@ -50,6 +50,7 @@ class Method(enum.IntEnum):
     planar = _lib.HF_METHOD_PLANAR
     lines = _lib.HF_METHOD_LINES
     unfused = _lib.HF_METHOD_UNFUSED
+    planar_managed = _lib.HF_METHOD_PLANAR_MANAGED
 
 
 def n_vars(d: int) -> int:

@@ -56,6 +56,27 @@ int main() {
                                        oracle_divergence(U, par, {1, 1, 1}, false));
     std::printf("tgv p=4 err=%.3e %s\n", err, err <= 1e-12 ? "ok" : "FAIL");
     failures += err <= 1e-12 ? 0 : 1;
+    // every reference kernel method (layout.hpp:18) through method_of(): planar, managed planar, lines
+    for (Method m : {Method::PlanarUnmanaged, Method::PlanarManaged, Method::Lines}) {
+        for (Precision prec : {Precision::fp64, Precision::fp32}) {
+            for (int p : {2, 5}) {
+                ElementConfig c;
+                c.p = p;
+                c.n_elem = 97;
+                c.precision = prec;
+                c.method = m;
+                if (m == Method::Lines) c.block_threads = 2 * (p + 1) * (p + 1);  // layout.hpp: n*(p+1)^2
+                const StateField U = random_field(c, 99 + p);
+                const double e = field_rel_error(
+                    hexfuse_b200::fused_divergence_b200(U, par, {1.0, 2.0, 0.5}, true, hexfuse_b200::method_of(m)),
+                    oracle_divergence(U, par, {1.0, 2.0, 0.5}, true));
+                const double tol = prec == Precision::fp32 ? 1e-5 : 1e-12;
+                std::printf("method=%s %s p=%d err=%.3e %s\n", to_string(m), to_string(prec), p, e,
+                            e <= tol ? "ok" : "FAIL");
+                failures += e <= tol ? 0 : 1;
+            }
+        }
+    }
     // error mapping: invalid params -> std::invalid_argument, like the reference
     try {
         hexfuse_b200::fused_divergence_b200(U, PhysParams{-1.0, 2.5, 1.0}, {1, 1, 1}, false);

@@ -71,9 +71,14 @@ def test_validation_mirrors_reference_errors():
             hf.validate(pr)
     pr = hf.make_problem(2, 8, 10, 4, Precision.fp32, PhysParams())  # d=2 p=8 is supported (unpinned)
     hf.validate(pr)
-    pr = hf.make_problem(2, 3, 10, 4, Precision.fp32, PhysParams(), method=Method.planar)
-    with pytest.raises(HexfuseInvalid, match="planar"):
-        hf.validate(pr)  # the reference's planar generator rejects d=2 (codegen_planar.hpp:102)
+    for meth in (Method.planar, Method.planar_managed):
+        pr = hf.make_problem(2, 3, 10, 4, Precision.fp32, PhysParams(), method=meth)
+        with pytest.raises(HexfuseInvalid, match="planar"):
+            hf.validate(pr)  # the reference's planar generator rejects d=2 (codegen_planar.hpp:102)
+    pr = hf.make_problem(3, 3, 10, 4, Precision.fp32, PhysParams())
+    pr.method = 5  # past HF_METHOD_PLANAR_MANAGED: rejected at the C ABI
+    with pytest.raises(HexfuseInvalid, match="unknown method"):
+        hf.validate(pr)
 
 
 def test_derivative_matrix_bitexact_vs_oracle():

@@ -48,7 +48,7 @@ def test_nonunit_jac_fp64(cuda, p):
     par = PhysParams(3e-3, 2.5, 1.0)
     for t in range(3):
         U = _field(3, p, 37, 4, False, 100 + 10 * p + t)
-        for method in (Method.lines, Method.planar, Method.unfused):
+        for method in (Method.lines, Method.planar, Method.planar_managed, Method.unfused):
             check_parity(3, p, 37, 4, False, U, params=par, jac=(1.0, 0.5, 2.0), with_source=(t % 2 == 0),
                          method=method)
 
@@ -72,7 +72,7 @@ def test_lines_misaligned_pointer(cuda):
     check_parity(3, 2, 64, 16, False, U, method=Method.lines, offset_bytes=8)
 
 
-@pytest.mark.parametrize("variant", list(range(10)))
+@pytest.mark.parametrize("variant", list(range(16)))
 @pytest.mark.parametrize("d,p,fp32", [(3, 1, True), (3, 3, False), (3, 4, True), (3, 6, False), (3, 6, True),
                                       (2, 3, True), (2, 8, True)])
 def test_lines_variants(cuda, d, p, fp32, variant):
@@ -99,7 +99,7 @@ def test_pipe_many_chunks_per_cta(cuda):
     import paper_2107_14027_b200 as hf
     for fp32, p in [(False, 3), (True, 5)]:
         pr = hf.make_problem(3, p, 1, 1, int(not fp32), PAR)
-        for variant in (3, 4, 5, 6, 8, 9):
+        for variant in (3, 4, 5, 6, 8, 9, 10, 11, 12, 13, 14, 15):
             try:
                 g = hf.variant_info(pr, Method.lines, variant)["elems_per_cta"]
             except hf.HexfuseInvalid:
@@ -112,12 +112,32 @@ def test_pipe_many_chunks_per_cta(cuda):
 
 
 # ---------------------------------------------------------------- planar method (d = 3)
+@pytest.mark.parametrize("method", [Method.planar, Method.planar_managed])
 @pytest.mark.parametrize("fp32", [False, True])
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6])
-def test_planar_random(cuda, p, fp32):
+def test_planar_random(cuda, p, fp32, method):
     for t, src in enumerate([False, True]):
         U = _field(3, p, 45, 32, fp32, 2024 + t)
-        check_parity(3, p, 45, 32, fp32, U, with_source=src, method=Method.planar)
+        check_parity(3, p, 45, 32, fp32, U, with_source=src, method=method)
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6])
+def test_planar_managed_layouts(cuda, p, fp32):
+    """Managed planar (every operand resident in shared memory): bulk-staged chunks
+    (group == elements per CTA, any alignment), row-mode chunks, group 1 / 3 (guarded
+    staging), a partial last chunk, and the same numbers as the unmanaged planar kernel
+    (same accumulation order, codegen_planar.hpp:97-210)."""
+    import paper_2107_14027_b200 as hf
+    g = hf.variant_info(hf.make_problem(3, p, 1, 1, int(not fp32), PAR), Method.planar_managed, 0)["elems_per_cta"]
+    for n, group, src in [(3 * g + 1, g, True), (4 * g, 2 * g, False), (2 * g + 1, 1, True), (2 * g + 2, 3, False)]:
+        U = _field(3, p, n, group, fp32, 300 + n + group)
+        got = check_parity(3, p, n, group, fp32, U, with_source=src, method=Method.planar_managed)
+        assert got <= (1e-5 if fp32 else 1e-12)
+    U = _field(3, p, 2 * g, g, fp32, 17)
+    a = run_device(3, p, 2 * g, g, fp32, U, method=Method.planar_managed, with_source=True)
+    b = run_device(3, p, 2 * g, g, fp32, U, method=Method.planar, with_source=True)
+    assert O.field_rel_error(3, p, 2 * g, g, a, b) <= (1e-6 if fp32 else 1e-14)
 
 
 # ---------------------------------------------------------------- unfused comparator
@@ -137,7 +157,7 @@ def test_tgv_fixture(cuda, p, fp32):
     g = hf.preferred_group(hf.make_problem(3, p, 1, 1, int(not fp32), PAR))
     n = 64
     U = O.tgv_field(p, n, g, fp32)
-    for method in (Method.auto, Method.planar):
+    for method in (Method.auto, Method.planar, Method.planar_managed):
         check_parity(3, p, n, g, fp32, U, method=method)
 
 
@@ -150,7 +170,7 @@ def test_constant_field_zero_divergence(cuda):
         U[:, v, :, :] = 0.5 + 0.1 * v
     U = U.reshape(-1)
     real = padding_mask(d, p, n, g).reshape(-1, 13, 27, g)
-    for method in (Method.lines, Method.planar, Method.unfused):
+    for method in (Method.lines, Method.planar, Method.planar_managed, Method.unfused):
         got = run_device(d, p, n, g, False, U, method=method).reshape(-1, 13, 27, g)
         assert np.max(np.abs(got[real])) < 1e-12
         src = run_device(d, p, n, g, False, U, with_source=True, method=method).reshape(-1, 13, 27, g)
@@ -170,7 +190,7 @@ def test_linear_velocity_exact(cuda):
             for j in range(m):
                 for i in range(m):
                     U[i + m * j + m * m * k + m ** 3 * 1] = nodes[i]  # u = x
-        for method in (Method.lines, Method.planar, Method.unfused):
+        for method in (Method.lines, Method.planar, Method.planar_managed, Method.unfused):
             got = run_device(3, p, 1, 1, False, U, params=par, method=method)
             for k in range(m):
                 for j in range(m):
