@@ -23,11 +23,12 @@ int lines_variant(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, 
                        : int(launch_lines_pipe<R, DIM, M, NE, ST, GR, false>(prm, st, info, dry));
         }
     } else if constexpr (LinesShape<R, DIM, M, NE>::SMEM > size_t(kMaxSmemPerCta) ||
-                         LinesShape<R, DIM, M, NE>::BS > 1024) {
+                         LinesShape<R, DIM, M, NE, lines_per_thread<VARIANT>()>::BS > 1024) {
         return kUnsupported;
     } else {
-        return src ? int(launch_lines<R, DIM, M, NE, true>(prm, st, info, dry))
-                   : int(launch_lines<R, DIM, M, NE, false>(prm, st, info, dry));
+        constexpr int LPT = lines_per_thread<VARIANT>();
+        return src ? int(launch_lines<R, DIM, M, NE, true, LPT>(prm, st, info, dry))
+                   : int(launch_lines<R, DIM, M, NE, false, LPT>(prm, st, info, dry));
     }
 }
 

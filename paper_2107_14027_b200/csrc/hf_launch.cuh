@@ -55,10 +55,12 @@ constexpr int lines_ne_default() {
 //     8: (NE0/4, 3, 1)  9: (NE0/4, 4, 1)
 //    10: (NE0/2, 4, 2) 11: (NE0/2, 6, 3)  12: (NE0/4, 8, 4)  13: (NE0/4, 6, 2)
 //    14: (NE0, 4, 2)   15: (NE0/4, 6, 3)
+//   one chunk per CTA with several lines per thread, (elements, lines per thread):
+//    16: (2*NE0, 2)    17: (NE0, 2)       18: (4*NE0, 4)
 // The contiguous bulk path accepts any NE >= 1 (hf_chunk_io.cuh), so the small-NE
 // variants exist for every order; a variant whose shape does not fit (shared
 // memory, 1024 threads) reports unsupported.
-constexpr int kLinesVariants = 16;
+constexpr int kLinesVariants = 19;
 
 // The measured selection (tools/select_methods.py -> hf_select_table.inc).
 struct SelRow {
@@ -87,7 +89,7 @@ constexpr bool variant_built() {
 }
 template <int VARIANT>
 constexpr bool is_pipe_variant() {
-    return !(VARIANT == 0 || VARIANT == 1 || VARIANT == 2 || VARIANT == 7);
+    return !(VARIANT == 0 || VARIANT == 1 || VARIANT == 2 || VARIANT == 7 || VARIANT >= 16);
 }
 template <class R, int DIM, int M, int VARIANT>
 constexpr int variant_ne() {
@@ -95,7 +97,9 @@ constexpr int variant_ne() {
     constexpr int ne = (VARIANT == 0 || VARIANT == 3 || VARIANT == 6 || VARIANT == 14)     ? ne0
                        : (VARIANT == 1 || VARIANT == 4 || VARIANT == 5 || VARIANT == 10 ||
                           VARIANT == 11)                                                     ? ne0 / 2
-                       : (VARIANT == 2)                                                      ? ne0 * 2
+                       : (VARIANT == 2 || VARIANT == 16)                                     ? ne0 * 2
+                       : (VARIANT == 17)                                                     ? ne0
+                       : (VARIANT == 18)                                                     ? ne0 * 4
                                                                                              : ne0 / 4;
     return ne >= 1 ? ne : 0;
 }
@@ -108,6 +112,10 @@ constexpr int pipe_stages() {
         case 12: return 8;
         default: return 2;
     }
+}
+template <int VARIANT>
+constexpr int lines_per_thread() {
+    return VARIANT == 16 || VARIANT == 17 ? 2 : (VARIANT == 18 ? 4 : 1);
 }
 template <int VARIANT>
 constexpr int pipe_groups() {
@@ -166,10 +174,10 @@ inline void fill_regs(K kernel, KInfo* info) {
 inline const char* prec_name(size_t w) { return w == 4 ? "fp32" : "fp64"; }
 
 // Launch (or, with dry = true, only describe) the lines kernel.
-template <class R, int DIM, int M, int NE, bool SRC>
+template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1>
 cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
-    using S = LinesShape<R, DIM, M, NE>;
-    auto kernel = hf_lines_kernel<R, DIM, M, NE, SRC>;
+    using S = LinesShape<R, DIM, M, NE, LPT>;
+    auto kernel = hf_lines_kernel<R, DIM, M, NE, SRC, LPT>;
     const long long grid = (p.n_elem + NE - 1) / NE;
     const bool fast_layout = bulk_layout<R, NE>(p.group);
     if (info) {
@@ -179,8 +187,12 @@ cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
         info->shared_bytes = int(S::SMEM);
         info->grid = grid;
         info->bulk_path = fast_layout ? 1 : 0;
-        std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d%s", DIM, M - 1, prec_name(sizeof(R)),
-                      NE, SRC ? "_src" : "");
+        if (LPT == 1)
+            std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d%s", DIM, M - 1,
+                          prec_name(sizeof(R)), NE, SRC ? "_src" : "");
+        else
+            std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d_l%d%s", DIM, M - 1,
+                          prec_name(sizeof(R)), NE, LPT, SRC ? "_src" : "");
         if (dry) fill_regs(kernel, info);
     }
     if (dry || p.n_elem == 0) return cudaSuccess;

@@ -44,12 +44,17 @@
 
 namespace hfb {
 
-template <class R, int DIM, int M, int NE>
+// LPT: lines per thread of the one-chunk-per-CTA kernel (block = LINES / LPT
+// threads): larger chunks per block without more threads, for the low-order
+// cases whose per-line work is small and whose bytes in flight per SM are
+// limited by the thread count.
+template <class R, int DIM, int M, int NE, int LPT = 1>
 struct LinesShape {
     static constexpr int NV = n_vars_c(DIM);
     static constexpr int NP = ipow_c(M, DIM);
     static constexpr int LINES = NE * ipow_c(M, DIM - 1);
-    static constexpr int BS = ((LINES + 31) / 32) * 32 < 64 ? 64 : ((LINES + 31) / 32) * 32;
+    static constexpr int TL = (LINES + LPT - 1) / LPT;
+    static constexpr int BS = ((TL + 31) / 32) * 32 < 64 ? 64 : ((TL + 31) / 32) * 32;
     static constexpr int NACC = 1 + DIM;  // continuity + d momentum partials
     static constexpr int IN_WORDS = NE * NP * NV;
     static constexpr int ACC_WORDS = NE * NP * NACC;
@@ -339,10 +344,10 @@ __device__ __forceinline__ void lines_sweeps_at(unsigned char* buf, int head, R*
     }
 }
 
-template <class R, int DIM, int M, int NE, bool SRC>
-__global__ void __launch_bounds__(LinesShape<R, DIM, M, NE>::BS)
+template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1>
+__global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT>::BS)
     hf_lines_kernel(const __grid_constant__ Params<R> p) {
-    using S = LinesShape<R, DIM, M, NE>;
+    using S = LinesShape<R, DIM, M, NE, LPT>;
     constexpr int BS = S::BS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     using IO = typename S::IO;

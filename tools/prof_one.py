@@ -22,7 +22,7 @@ def main():
     ap.add_argument("--p", type=int, default=3)
     ap.add_argument("--prec", default="fp64")
     ap.add_argument("--method", default="lines")
-    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--variant", type=int, default=0, help="lines variant; -1 = the selected kernel (method auto)")
     ap.add_argument("--points", type=float, default=1e7)
     ap.add_argument("--launches", type=int, default=3)
     ap.add_argument("--src", action="store_true")
@@ -31,7 +31,11 @@ def main():
     method = Method[a.method]
     par = PhysParams(1.0 / 1600.0, 2.5, 1.0)
     pr0 = hf.make_problem(a.d, a.p, 1, 1, prec, par)
-    g = hf.variant_info(pr0, method, a.variant)["elems_per_cta"] if method != Method.unfused else 32
+    if a.variant < 0:
+        method = Method.auto
+        g = hf.preferred_group(pr0)
+    else:
+        g = hf.variant_info(pr0, method, a.variant)["elems_per_cta"] if method != Method.unfused else 32
     npt = (a.p + 1) ** a.d
     n = max(g, int(a.points / npt) // g * g)
     pr = hf.make_problem(a.d, a.p, n, g, prec, par, with_source=a.src, method=method)
@@ -44,10 +48,13 @@ def main():
     for _ in range(a.launches):
         if ws is not None:
             hf.unfused_divergence_device(pr, u, o, ws)
+        elif a.variant < 0:
+            hf.fused_divergence_device(pr, u, o)
         else:
             hf.fused_divergence_variant(pr, method, a.variant, u, o)
     torch.cuda.synchronize()
-    print(hf.variant_info(pr, method, a.variant) if ws is None else "unfused", n, "elements")
+    print(hf.kernel_info(pr) if a.variant < 0 else
+          (hf.variant_info(pr, method, a.variant) if ws is None else "unfused"), n, "elements")
 
 
 if __name__ == "__main__":

@@ -120,7 +120,7 @@ def main():
     ap.add_argument("--write-table", action="store_true")
     ap.add_argument("--no-unfused", action="store_true")
     ap.add_argument("--ps", default=None, help="comma list of orders (default: all)")
-    ap.add_argument("--variants", default=None, help="comma list of lines variants (default: 0..15)")
+    ap.add_argument("--variants", default=None, help="comma list of lines variants (default: 0..18)")
     ap.add_argument("--no-planar", action="store_true")
     ap.add_argument("--from-files", nargs="*", default=None, help="write the table from saved jsonl rows")
     args = ap.parse_args()
@@ -133,7 +133,7 @@ def main():
         pmax = 6 if d == 3 else 8
         for prec in (Precision.fp32, Precision.fp64):
             for p in ([int(x) for x in args.ps.split(",")] if args.ps else range(1, pmax + 1)):
-                vs = [int(x) for x in args.variants.split(",")] if args.variants else range(16)
+                vs = [int(x) for x in args.variants.split(",")] if args.variants else range(19)
                 cands = [(Method.lines, v) for v in vs]
                 if d == 3 and not args.no_planar:
                     cands.append((Method.planar, 0))
@@ -168,7 +168,8 @@ def write_table(rows, points, raw="profiles/select_r01_*.jsonl"):
                 "// lines variants (hf_launch.cuh): 0/1/2/7 = one chunk per CTA with NE0, NE0/2, 2*NE0, NE0/4\n"
                 "// elements; 3..6, 8..15 = persistent TMA-ring kernel, (elements, stages, consumer groups):\n"
                 "// 3 (NE0,2,1) 4 (NE0/2,3,1) 5 (NE0/2,2,1) 6 (NE0,3,1) 8 (NE0/4,3,1) 9 (NE0/4,4,1)\n"
-                "// 10 (NE0/2,4,2) 11 (NE0/2,6,3) 12 (NE0/4,8,4) 13 (NE0/4,6,2) 14 (NE0,4,2) 15 (NE0/4,6,3).\n"
+                "// 10 (NE0/2,4,2) 11 (NE0/2,6,3) 12 (NE0/4,8,4) 13 (NE0/4,6,2) 14 (NE0,4,2) 15 (NE0/4,6,3);\n"
+                "// 16/17/18 = one chunk per CTA with (2*NE0, 2), (NE0, 2), (4*NE0, 4) (elements, lines per thread).\n"
                 "// Generated by tools/select_methods.py from on-GPU measurements (achieved\n"
                 f"// HBM GB/s, median of 20 launches at ~{points:.0e} points per configuration;\n"
                 f"// raw rows in {raw}).\n")
