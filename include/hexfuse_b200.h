@@ -114,6 +114,22 @@ HF_API int hf_fused_divergence(const hf_problem* pr, const void* u_dev, void* di
 HF_API size_t hf_unfused_workspace_bytes(const hf_problem* pr); /* d*n_v words per padded point */
 HF_API int hf_unfused_divergence(const hf_problem* pr, const void* u_dev, void* divf_dev, void* ws_dev, void* stream);
 
+/* ---- extension: elements with a non-constant Jacobian ----
+ * Beyond the reference, which fixes a constant per-axis Jacobian (oracle.hpp:47):
+ * (bi/tri)linear elements given by their 2^d corners ("linear elements, for which
+ * only the element corners need to be loaded").  Conservative FR
+ * form out = -(1/|J|) sum_a D_a(sum_b adj(J)_ab F_b) (+ source) at the solution
+ * points; pr->jac and pr->method are ignored.  geom_dev: hf_geometry_words(pr)
+ * words of the problem's precision, AoSoA with the field's group:
+ *   word (e, c, x) = (e/group)*group*2^d*d + e%group + group*(x + d*c),
+ * corner c at reference point (bit k of c ? +1 : -1) along xi_k.  For an
+ * axis-aligned box of half-widths h this equals hf_fused_divergence with
+ * jac = 1/h.  Asynchronous like hf_fused_divergence. */
+HF_API int64_t hf_geometry_words(const hf_problem* pr);
+HF_API int hf_fused_divergence_mapped(const hf_problem* pr, const void* u_dev, const void* geom_dev, void* divf_dev,
+                                      void* stream);
+HF_API int hf_mapped_kernel_info(const hf_problem* pr, hf_kernel_info* out);
+
 /* ---- host-buffer entry point (the (b1) replacement) ----
  * u_host / divf_host: host arrays of hf_field_words(pr) words of the problem's
  * precision (float for HF_FP32, double for HF_FP64).  Pinned memory is used

@@ -85,6 +85,14 @@ def lib() -> C.CDLL:
         L.hfo_verify_tolerance.argtypes = [C.c_int]
         L.hfo_verify_tolerance.restype = C.c_double
         L.hfo_io_model.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(_i64), C.POINTER(_i64)]
+        L.hfo_geometry_words.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.hfo_geometry_words.restype = _i64
+        L.hfo_mapped_jacobian.argtypes = [C.c_int, _dp, _dp, _dp]
+        L.hfo_mapped_jacobian.restype = None
+        L.hfo_adjugate.argtypes = [C.c_int, _dp, _dp]
+        L.hfo_adjugate.restype = C.c_double
+        L.hfo_oracle_divergence_mapped.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, C.c_double,
+                                                   C.c_double, C.c_double, C.c_int]
         _lib = L
     return _lib
 
@@ -209,6 +217,55 @@ def oracle_divergence_elements(d: int, p: int, group: int, U: np.ndarray, out: n
                                            int(with_source), e_begin, e_end)
     if rc != 0:
         raise ValueError("oracle_divergence_range: invalid arguments")
+
+
+# ---- extension: (bi/tri)linear elements with a non-constant Jacobian (hexfuse_oracle.c)
+def geometry_words(d: int, n_elem: int, group: int) -> int:
+    return int(lib().hfo_geometry_words(d, n_elem, group))
+
+
+def geom_offset(d: int, group: int, e: int, c: int, x: int) -> int:
+    """AoSoA word of corner c (bit k = +xi_k side), coordinate x, of element e."""
+    nc = 1 << d
+    return (e // group) * group * nc * d + e % group + group * (x + d * c)
+
+
+def box_geometry(d: int, n_elem: int, group: int, h, origin=None) -> np.ndarray:
+    """Axis-aligned boxes of half-widths h (element e shifted by 2*h_0*e along x)."""
+    G = np.zeros(geometry_words(d, n_elem, group))
+    for e in range(n_elem):
+        for c in range(1 << d):
+            for x in range(d):
+                s = 1.0 if (c >> x) & 1 else -1.0
+                base = (origin[x] if origin is not None else 0.0) + (2.0 * h[0] * e if x == 0 else 0.0)
+                G[geom_offset(d, group, e, c, x)] = base + s * h[x]
+    return G
+
+
+def random_geometry(d: int, n_elem: int, group: int, seed: int, h=(0.5, 0.7, 0.9), amp: float = 0.15,
+                    fp32: bool = False) -> np.ndarray:
+    """Boxes of half-widths h with every corner displaced by U(-amp, amp) * h (curved trilinear
+    elements, positive Jacobian for amp < 1/3); quantised to float for FP32 problems."""
+    rng = np.random.default_rng(seed)
+    G = box_geometry(d, n_elem, group, h)
+    for e in range(n_elem):
+        for c in range(1 << d):
+            for x in range(d):
+                G[geom_offset(d, group, e, c, x)] += rng.uniform(-amp, amp) * h[x]
+    if fp32:
+        G = G.astype(np.float32).astype(np.float64)
+    return G
+
+
+def oracle_divergence_mapped(d: int, p: int, n_elem: int, group: int, U: np.ndarray, G: np.ndarray, nu: float,
+                             zeta: float, T: float, with_source: bool = False) -> np.ndarray:
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    assert U.size == field_words(d, p, n_elem, group) and G.size == geometry_words(d, n_elem, group)
+    out = np.zeros_like(U)
+    if lib().hfo_oracle_divergence_mapped(d, p, n_elem, group, U, G, out, nu, zeta, T, int(with_source)) != 0:
+        raise ValueError("oracle_divergence_mapped: invalid arguments")
+    return out
 
 
 def field_rel_error(d: int, p: int, n_elem: int, group: int, got: np.ndarray, ref_: np.ndarray) -> float:

@@ -22,6 +22,9 @@ from .hexfuse import (  # noqa: F401
     field_words,
     fused_divergence,
     fused_divergence_device,
+    fused_divergence_mapped_device,
+    geometry_words,
+    mapped_kernel_info,
     fused_divergence_variant,
     import_blob,
     kernel_info,

@@ -53,6 +53,7 @@ EXPORTED = [
     "hf_algorithmic_bytes_per_point", "hf_selected_method", "hf_preferred_group", "hf_kernel_info_get",
     "hf_fused_divergence", "hf_unfused_workspace_bytes", "hf_unfused_divergence", "hf_context_create",
     "hf_context_destroy", "hf_fused_divergence_host", "hf_partition", "hf_last_error", "hf_version",
+    "hf_geometry_words", "hf_fused_divergence_mapped", "hf_mapped_kernel_info",
 ]
 
 _lib = None
@@ -103,6 +104,10 @@ def load() -> C.CDLL:
     L.hf_version.restype = C.c_char_p
     L.hf_fused_divergence_variant.argtypes = [P, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                               C.POINTER(hf_kernel_info)]
+    L.hf_geometry_words.argtypes = [P]
+    L.hf_geometry_words.restype = C.c_int64
+    L.hf_fused_divergence_mapped.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.hf_mapped_kernel_info.argtypes = [P, C.POINTER(hf_kernel_info)]
     _lib = L
     return L
 

@@ -88,12 +88,16 @@ void derivative_matrix(int m, const double* x, double* D) {
 
 struct OpCache {
     double D[10][hfb::kMaxM * hfb::kMaxM];
+    double x[10][hfb::kMaxM];
     bool ok[10];
     OpCache() {
         for (int m = 0; m < 10; ++m) {
-            double x[16];
-            ok[m] = gl_nodes(m, x);
-            if (ok[m]) derivative_matrix(m, x, D[m]);
+            double xs[16];
+            ok[m] = gl_nodes(m, xs);
+            if (ok[m]) {
+                derivative_matrix(m, xs, D[m]);
+                for (int i = 0; i < m && i < hfb::kMaxM; ++i) x[m][i] = xs[i];
+            }
         }
     }
 };
@@ -153,6 +157,7 @@ hfb::Params<R> make_params(const hf_problem* pr, const void* u, void* out, void*
     const int m = pr->p + 1;
     const double* D = ops().D[m];
     for (int i = 0; i < m * m; ++i) p.D[i] = R(D[i]);
+    for (int i = 0; i < m; ++i) p.xg[i] = R(ops().x[m][i]);
     const int h = m / 2;
     for (int i = 0; i <= h && i < hfb::kMaxH; ++i) {
         for (int t = 0; t < h; ++t) {
@@ -298,6 +303,57 @@ int hf_fused_divergence(const hf_problem* pr, const void* u_dev, void* divf_dev,
 size_t hf_unfused_workspace_bytes(const hf_problem* pr) {
     if (validate(pr)) return 0;
     return size_t(hf_field_words(pr)) * size_t(pr->d) * word_bytes(pr);
+}
+
+int64_t hf_geometry_words(const hf_problem* pr) {
+    if (!pr || pr->group < 1 || (pr->d != 2 && pr->d != 3) || pr->n_elem < 0) return -1;
+    const int64_t ng = (pr->n_elem + pr->group - 1) / pr->group;
+    return ng * pr->group * (int64_t(1) << pr->d) * pr->d;
+}
+
+int hf_fused_divergence_mapped(const hf_problem* pr, const void* u_dev, const void* geom_dev, void* divf_dev,
+                               void* stream) {
+    if (int rc = validate(pr)) return rc;
+    if (pr->n_elem > 0 && (!u_dev || !divf_dev || !geom_dev))
+        return fail(HF_EINVAL, "hf_fused_divergence_mapped: null buffer");
+    if (u_dev == divf_dev && pr->n_elem > 0)
+        return fail(HF_EINVAL, "hf_fused_divergence_mapped: in-place not supported");
+    const bool src = pr->with_source != 0;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int rc;
+    if (pr->precision == HF_FP32) {
+        auto prm = make_params<float>(pr, u_dev, divf_dev, nullptr);
+        prm.geo = static_cast<const float*>(geom_dev);
+        rc = hfb::mapped_f32(pr->d, pr->p, src, prm, st, nullptr, false);
+    } else {
+        auto prm = make_params<double>(pr, u_dev, divf_dev, nullptr);
+        prm.geo = static_cast<const double*>(geom_dev);
+        rc = hfb::mapped_f64(pr->d, pr->p, src, prm, st, nullptr, false);
+    }
+    if (rc == hfb::kUnsupported) return fail(HF_EINVAL, "no mapped kernel for this (d, p)");
+    if (rc != 0) return cuda_fail(cudaError_t(rc), "mapped kernel launch");
+    return HF_OK;
+}
+
+int hf_mapped_kernel_info(const hf_problem* pr, hf_kernel_info* out) {
+    if (int rc = validate(pr)) return rc;
+    if (!out) return fail(HF_EINVAL, "hf_mapped_kernel_info: null output");
+    hfb::KInfo ki;
+    const auto dummy_f = make_params<float>(pr, nullptr, nullptr, nullptr);
+    const auto dummy_d = make_params<double>(pr, nullptr, nullptr, nullptr);
+    const int rc = pr->precision == HF_FP32 ? hfb::mapped_f32(pr->d, pr->p, pr->with_source != 0, dummy_f, nullptr, &ki, true)
+                                            : hfb::mapped_f64(pr->d, pr->p, pr->with_source != 0, dummy_d, nullptr, &ki, true);
+    if (rc == hfb::kUnsupported) return fail(HF_EINVAL, "no mapped kernel for this (d, p)");
+    out->method = ki.method;
+    out->elems_per_cta = ki.elems_per_cta;
+    out->block_threads = ki.block_threads;
+    out->shared_bytes = ki.shared_bytes;
+    out->registers = ki.registers;
+    out->grid = ki.grid;
+    out->bulk_path = ki.bulk_path;
+    out->blocks_per_sm = ki.blocks_per_sm;
+    std::memcpy(out->name, ki.name, sizeof(out->name));
+    return HF_OK;
 }
 
 int hf_unfused_divergence(const hf_problem* pr, const void* u_dev, void* divf_dev, void* ws_dev, void* stream) {

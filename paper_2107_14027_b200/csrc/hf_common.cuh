@@ -33,9 +33,11 @@ struct Params {
     R nu, zeta, invT;    // PhysParams (equations.hpp:14-24), 1/T precomputed
     R jac[3];            // constant per-axis metric (oracle.hpp:47)
     R jac_invT[3];       // jac[a] / T : gradient-row scale
+    R xg[kMaxM];         // Gauss-Legendre nodes (mapped elements: the reference point of each node)
     const R* __restrict__ u;  // input field, AoSoA (layout.hpp:128-134)
     R* __restrict__ out;      // divergence, same layout
     R* __restrict__ ws;       // unfused only: flux workspace
+    const R* __restrict__ geo;  // mapped elements only: 2^d corners per element (hf_mapped.cuh)
     long long n_elem;
     long long group_words;    // group * m^d * n_v
     long long total_words;    // n_groups * group_words (allocation size of u and out)

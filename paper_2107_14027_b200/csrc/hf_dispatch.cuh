@@ -110,6 +110,44 @@ int run_planar_managed_impl(int p, bool src, const Params<R>& prm, cudaStream_t 
     }
 }
 
+template <class R, int DIM, int M>
+int mapped_m(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
+    constexpr int NE = mapped_ne<R, DIM, M>();
+    if constexpr (MappedShape<R, DIM, M, NE>::SMEM > size_t(kMaxSmemPerCta)) {
+        return kUnsupported;
+    } else {
+        return src ? int(launch_mapped<R, DIM, M, NE, true>(prm, st, info, dry))
+                   : int(launch_mapped<R, DIM, M, NE, false>(prm, st, info, dry));
+    }
+}
+
+template <class R>
+int run_mapped_impl(int d, int p, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
+    if (d == 3) {
+        switch (p) {
+            case 1: return mapped_m<R, 3, 2>(src, prm, st, info, dry);
+            case 2: return mapped_m<R, 3, 3>(src, prm, st, info, dry);
+            case 3: return mapped_m<R, 3, 4>(src, prm, st, info, dry);
+            case 4: return mapped_m<R, 3, 5>(src, prm, st, info, dry);
+            case 5: return mapped_m<R, 3, 6>(src, prm, st, info, dry);
+            case 6: return mapped_m<R, 3, 7>(src, prm, st, info, dry);
+            case 7: return mapped_m<R, 3, 8>(src, prm, st, info, dry);
+            default: return kUnsupported;
+        }
+    }
+    switch (p) {
+        case 1: return mapped_m<R, 2, 2>(src, prm, st, info, dry);
+        case 2: return mapped_m<R, 2, 3>(src, prm, st, info, dry);
+        case 3: return mapped_m<R, 2, 4>(src, prm, st, info, dry);
+        case 4: return mapped_m<R, 2, 5>(src, prm, st, info, dry);
+        case 5: return mapped_m<R, 2, 6>(src, prm, st, info, dry);
+        case 6: return mapped_m<R, 2, 7>(src, prm, st, info, dry);
+        case 7: return mapped_m<R, 2, 8>(src, prm, st, info, dry);
+        case 8: return mapped_m<R, 2, 9>(src, prm, st, info, dry);
+        default: return kUnsupported;
+    }
+}
+
 template <class R>
 int run_unfused_impl(int d, int p, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
     if (d == 3) {
@@ -155,6 +193,8 @@ int planar_f32(int p, bool src, const Params<float>&, cudaStream_t, KInfo*, bool
 int planar_f64(int p, bool src, const Params<double>&, cudaStream_t, KInfo*, bool);
 int planar_managed_f32(int p, bool src, const Params<float>&, cudaStream_t, KInfo*, bool);
 int planar_managed_f64(int p, bool src, const Params<double>&, cudaStream_t, KInfo*, bool);
+int mapped_f32(int d, int p, bool src, const Params<float>&, cudaStream_t, KInfo*, bool);
+int mapped_f64(int d, int p, bool src, const Params<double>&, cudaStream_t, KInfo*, bool);
 int unfused_f32(int d, int p, bool src, const Params<float>&, cudaStream_t, KInfo*, bool);
 int unfused_f64(int d, int p, bool src, const Params<double>&, cudaStream_t, KInfo*, bool);
 

@@ -16,6 +16,7 @@
 #include "hf_common.cuh"
 #include "hf_lines.cuh"
 #include "hf_lines_pipe.cuh"
+#include "hf_mapped.cuh"
 #include "hf_planar.cuh"
 #include "hf_unfused.cuh"
 
@@ -318,6 +319,44 @@ cudaError_t launch_planar_managed(Params<R> p, cudaStream_t st, KInfo* info, boo
         info->grid = grid;
         info->bulk_path = fast_layout ? 1 : 0;
         std::snprintf(info->name, sizeof(info->name), "hf_planar_managed_d3_p%d_%s_ne%d%s", M - 1,
+                      prec_name(sizeof(R)), NE, SRC ? "_src" : "");
+        if (dry) fill_regs(kernel, info);
+    }
+    if (dry || p.n_elem == 0) return cudaSuccess;
+    p.fast_ok = fast_layout && aligned16(p.u) && aligned16(p.out);
+    if (int e = set_smem_attr(kernel, S::SMEM)) return cudaError_t(e);
+    kernel<<<dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st>>>(p);
+    return cudaGetLastError();
+}
+
+// Mapped elements: the largest power-of-two chunk (<= 64 / 128 elements) with
+// <= 100 KB of shared memory (two CTAs per SM) and <= 512 lines.
+template <class R, int DIM, int M>
+constexpr int mapped_ne() {
+    int ne = (DIM == 2) ? 128 : 64;
+    while (ne > 1 && (MappedShape<R, DIM, M, 1>::HDR + 48 + size_t(ne) * ipow_c(M, DIM) *
+                                                               (2 * n_vars_c(DIM) + DIM * DIM + 1) * sizeof(R) +
+                          size_t(ne) * (1 << DIM) * DIM * sizeof(R) >
+                      size_t(100 * 1024) ||
+                      ne * ipow_c(M, DIM - 1) > 512))
+        ne /= 2;
+    return ne;
+}
+
+template <class R, int DIM, int M, int NE, bool SRC>
+cudaError_t launch_mapped(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
+    using S = MappedShape<R, DIM, M, NE>;
+    auto kernel = hf_mapped_kernel<R, DIM, M, NE, SRC>;
+    const long long grid = (p.n_elem + NE - 1) / NE;
+    const bool fast_layout = bulk_layout<R, NE>(p.group);
+    if (info) {
+        info->method = 2;
+        info->elems_per_cta = NE;
+        info->block_threads = S::BS;
+        info->shared_bytes = int(S::SMEM);
+        info->grid = grid;
+        info->bulk_path = fast_layout ? 1 : 0;
+        std::snprintf(info->name, sizeof(info->name), "hf_mapped_d%d_p%d_%s_ne%d%s", DIM, M - 1,
                       prec_name(sizeof(R)), NE, SRC ? "_src" : "");
         if (dry) fill_regs(kernel, info);
     }

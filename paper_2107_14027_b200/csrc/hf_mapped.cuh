@@ -1,0 +1,298 @@
+// hf_mapped.cuh -- fused flux + divergence on elements with a non-constant
+// Jacobian (bi/trilinear "linear" elements given by their 2^d corners).
+//
+// EXTENSION beyond the reference, which fixes a constant per-axis Jacobian
+// (oracle.hpp:47).  PAPER.md:1111 names the next step:
+// "linear elements, for which only the locations of the element corners need
+// to be loaded".  Conservative FR form, collocated at the solution points
+// (oracle: hfo_oracle_divergence_mapped, oracle/hexfuse_oracle.c):
+//
+//     out = -(1/|J|) sum_a D_a ( sum_b S_ab F_b )  (+ source),   S = adj(J) = |J| J^-1.
+//
+// With G_a = sum_b S_ab F_b (the contravariant flux) the rows are, per point,
+//     continuity     zeta * W_a,                       W_a = sum_b S_ab V_b
+//     momentum c     V_c W_a + S_ac P - nu sum_b S_ab g(c,b)
+//     gradient (c,b) -S_ab V_c / T
+// so unlike the constant-Jacobian kernel every output row receives a
+// contribution from every sweep, and the metric varies along the line.
+//
+// One CTA per chunk of NE elements (hf_lines.cuh's staging):
+//   1. U chunk -> shared (cp.async.bulk), the chunk's corners -> shared;
+//   2. metric pass: S and 1/|J| at every point into shared ((d^2+1) words/pt);
+//   3. d sweeps, thread per a-line (bank-conflict-free LineMap order): batch 0
+//      contracts the 1+d continuity/momentum lines, then d batches of d
+//      gradient lines S_ab V_c; partial sums of all n_v rows accumulate in a
+//      shared region (n_v words/pt);
+//   4. final pass: out = -acc/|J| (+ -g/T) written over the staged input, bulk store.
+// HBM traffic stays n_v words in + n_v out per point plus 2^d d words per
+// element of geometry.
+#pragma once
+
+#include "hf_lines.cuh"
+
+namespace hfb {
+
+template <class R, int DIM, int M, int NE>
+struct MappedShape {
+    using L = LinesShape<R, DIM, M, NE>;
+    static constexpr int NV = n_vars_c(DIM);
+    static constexpr int NP = ipow_c(M, DIM);
+    static constexpr int NC = 1 << DIM;  // corners
+    static constexpr int NMET = DIM * DIM + 1;
+    static constexpr int BS = L::BS;
+    static constexpr int HDR = 128;
+    static constexpr size_t ACC_OFF = HDR + size_t(L::BUF_BYTES);
+    static constexpr size_t MET_OFF = ACC_OFF + size_t(NV) * NP * NE * sizeof(R);
+    static constexpr size_t GEO_OFF = MET_OFF + size_t(NMET) * NP * NE * sizeof(R);
+    static constexpr size_t SMEM = GEO_OFF + size_t(NC) * DIM * NE * sizeof(R);
+};
+
+// adj(J) (row-major) and det(J) of the map at one point.
+template <class R, int DIM>
+__device__ __forceinline__ R mapped_adjugate(const R (&J)[DIM * DIM], R (&S)[DIM * DIM]) {
+    if constexpr (DIM == 2) {
+        S[0] = J[3];
+        S[1] = -J[1];
+        S[2] = -J[2];
+        S[3] = J[0];
+        return J[0] * J[3] - J[1] * J[2];
+    } else {
+        S[0] = J[4] * J[8] - J[5] * J[7];
+        S[1] = J[2] * J[7] - J[1] * J[8];
+        S[2] = J[1] * J[5] - J[2] * J[4];
+        S[3] = J[5] * J[6] - J[3] * J[8];
+        S[4] = J[0] * J[8] - J[2] * J[6];
+        S[5] = J[2] * J[3] - J[0] * J[5];
+        S[6] = J[3] * J[7] - J[4] * J[6];
+        S[7] = J[1] * J[6] - J[0] * J[7];
+        S[8] = J[0] * J[4] - J[1] * J[3];
+        return J[0] * S[0] + J[1] * S[3] + J[2] * S[6];
+    }
+}
+
+// Accumulate d = D * Y (line rows of one batch) into the shared partial sums.
+template <class R, int M, int NE, int STRIDE, int NROW>
+__device__ __forceinline__ void mapped_contract(const Params<R>& p, const R (&Y)[NROW][M], R* __restrict__ acc_line,
+                                                const int (&rows)[NROW], R scale, bool first) {
+    constexpr int NP_STRIDE = NE * STRIDE;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+#pragma unroll
+        for (int r = 0; r < NROW; ++r) {
+            R s = p.D[i * M] * Y[r][0];
+#pragma unroll
+            for (int t = 1; t < M; ++t) s = fma(p.D[i * M + t], Y[r][t], s);
+            R* q = acc_line + rows[r] + NP_STRIDE * i;
+            *q = first ? scale * s : fma(scale, s, *q);
+        }
+    }
+}
+
+// One sweep along axis A for the line whose first point is word `o` of the chunk.
+template <class R, int DIM, int M, int NE, int A>
+__device__ __forceinline__ void mapped_sweep(const R* __restrict__ s, R* __restrict__ acc, const R* __restrict__ met,
+                                             const Params<R>& p, int o) {
+    constexpr int NP = ipow_c(M, DIM);
+    constexpr int VS = NE * NP;  // word stride between variables (and metric entries)
+    constexpr int STRIDE = (A == 0) ? 1 : (A == 1) ? M : M * M;
+    constexpr int NV = n_vars_c(DIM);
+    const bool first = (A == 0);
+    const R* sb = s + o;
+    const R* mb = met + o;
+
+    // batch 0: continuity + momentum rows
+    {
+        R Y[1 + DIM][M];
+#pragma unroll
+        for (int t = 0; t < M; ++t) {
+            const int q = NE * STRIDE * t;
+            R Sa[DIM], V[DIM];
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) Sa[b] = mb[q + VS * (A * DIM + b)];
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) V[b] = sb[q + VS * (1 + b)];
+            const R P = sb[q];
+            R W = Sa[0] * V[0];
+#pragma unroll
+            for (int b = 1; b < DIM; ++b) W = fma(Sa[b], V[b], W);
+            Y[0][t] = p.zeta * W;
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+                R vg = Sa[0] * sb[q + VS * var_grad_c(DIM, c, 0)];
+#pragma unroll
+                for (int b = 1; b < DIM; ++b) vg = fma(Sa[b], sb[q + VS * var_grad_c(DIM, c, b)], vg);
+                Y[1 + c][t] = fma(V[c], W, fma(Sa[c], P, -p.nu * vg));
+            }
+        }
+        int rows[1 + DIM];
+#pragma unroll
+        for (int r = 0; r <= DIM; ++r) rows[r] = VS * r;
+        mapped_contract<R, M, NE, STRIDE, 1 + DIM>(p, Y, acc + o, rows, R(1), first);
+    }
+    // batches 1..d: gradient rows g(c, b) <- D (S_ab V_c) * (-1/T)
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+        R Y[DIM][M];
+#pragma unroll
+        for (int t = 0; t < M; ++t) {
+            const int q = NE * STRIDE * t;
+            const R Vc = sb[q + VS * (1 + c)];
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) Y[b][t] = mb[q + VS * (A * DIM + b)] * Vc;
+        }
+        int rows[DIM];
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) rows[b] = VS * var_grad_c(DIM, c, b);
+        mapped_contract<R, M, NE, STRIDE, DIM>(p, Y, acc + o, rows, -p.invT, first);
+    }
+    (void)NV;
+}
+
+template <class R, int DIM, int M, int NE, bool SRC>
+__global__ void __launch_bounds__(MappedShape<R, DIM, M, NE>::BS)
+    hf_mapped_kernel(const __grid_constant__ Params<R> p) {
+    using S = MappedShape<R, DIM, M, NE>;
+    using L = LinesShape<R, DIM, M, NE>;
+    using IO = typename L::IO;
+    constexpr int BS = S::BS, NP = S::NP, NV = S::NV, NC = S::NC;
+    constexpr int VS = NE * NP;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    unsigned char* buf = smem_raw + S::HDR;
+    R* acc = reinterpret_cast<R*>(smem_raw + S::ACC_OFF);
+    R* met = reinterpret_cast<R*>(smem_raw + S::MET_OFF);
+    R* geo = reinterpret_cast<R*>(smem_raw + S::GEO_OFF);  // [c][x][el]
+
+    const int tid = threadIdx.x;
+    const long long E0 = static_cast<long long>(blockIdx.x) * NE;
+    const long long grp = E0 / p.group;
+    const int el0 = static_cast<int>(E0 - grp * p.group);
+    const long long gbase = grp * p.group_words + el0;
+    const bool contiguous = (p.group == NE);
+    const bool fast = chunk_bulk_ok<R, L::IN_WORDS>(p, gbase, E0 + NE <= p.n_elem, contiguous);
+    const int head = fast ? IO::head_bytes(p.u + gbase, contiguous) : 0;
+
+    // ---------------- stage the chunk and its corners ----------------
+    if (fast) {
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (tid < 32) {
+            if (tid == 0) mbar_arrive_expect_tx(bar, IO::tx_bytes(p.u + gbase, contiguous));
+            __syncwarp();
+            IO::load(buf, p.u + gbase, p.group, contiguous, bar, tid);
+        }
+    } else {
+        R* s0 = reinterpret_cast<R*>(buf);
+        for (int idx = tid; idx < L::IN_WORDS; idx += BS) {
+            const long long e = E0 + idx % NE;
+            R v = R(0);
+            if (e < p.n_elem) {
+                const long long ge = e / p.group;
+                v = ld_stream(p.u + ge * p.group_words + (e - ge * p.group) + static_cast<long long>(p.group) * (idx / NE));
+            }
+            s0[idx] = v;
+        }
+    }
+    for (int idx = tid; idx < NC * DIM * NE; idx += BS) {
+        const int el = idx % NE;
+        const int cx = idx / NE;  // x + DIM * c
+        const long long e = E0 + el;
+        R v = R(0);
+        if (e < p.n_elem) {
+            const long long ge = e / p.group;
+            v = p.geo[ge * p.group * NC * DIM + (e - ge * p.group) + static_cast<long long>(p.group) * cx];
+        }
+        geo[idx] = v;
+    }
+    __syncthreads();
+
+    // ---------------- metric pass: S = adj(J), 1/|J| at every point ----------------
+    for (int idx = tid; idx < NE * NP; idx += BS) {
+        const int el = idx % NE;
+        const int pt = idx / NE;
+        R xi[3];
+        xi[0] = p.xg[pt % M];
+        xi[1] = p.xg[(pt / M) % M];
+        xi[2] = DIM == 3 ? p.xg[pt / (M * M)] : R(0);
+        R J[DIM * DIM];
+#pragma unroll
+        for (int q = 0; q < DIM * DIM; ++q) J[q] = R(0);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) {
+                R dn = R(0.5) * ((c >> j) & 1 ? R(1) : R(-1));  // dN_c / dxi_j
+#pragma unroll
+                for (int k = 0; k < DIM; ++k)
+                    if (k != j) dn *= R(0.5) * (R(1) + ((c >> k) & 1 ? xi[k] : -xi[k]));
+#pragma unroll
+                for (int i = 0; i < DIM; ++i) J[i * DIM + j] = fma(geo[el + NE * (i + DIM * c)], dn, J[i * DIM + j]);
+            }
+        }
+        R Sm[DIM * DIM];
+        const R det = mapped_adjugate<R, DIM>(J, Sm);
+#pragma unroll
+        for (int q = 0; q < DIM * DIM; ++q) met[idx + VS * q] = Sm[q];
+        met[idx + VS * DIM * DIM] = R(1) / det;
+    }
+    if (fast) mbar_wait_parity(bar, 0);
+    __syncthreads();
+
+    // ---------------- d sweeps ----------------
+    R* s = reinterpret_cast<R*>(buf + head);
+    auto sweep = [&](auto a_tag) {
+        constexpr int A = decltype(a_tag)::value;
+        using LM = LineMap<R, DIM, M, NE, A, BS>;
+        const unsigned short* map = kLineMap<R, DIM, M, NE, A, BS>.off;
+#pragma unroll 1
+        for (int k = 0; k < LM::ITERS; ++k) {
+            const int o = map[k * BS + tid];
+            if (o != 0xFFFF) mapped_sweep<R, DIM, M, NE, A>(s, acc, met, p, o);
+        }
+    };
+    sweep(std::integral_constant<int, 0>{});
+    __syncthreads();
+    sweep(std::integral_constant<int, 1>{});
+    if constexpr (DIM == 3) {
+        __syncthreads();
+        sweep(std::integral_constant<int, 2>{});
+    }
+    __syncthreads();
+
+    // ---------------- out = -acc / |J| (+ source), over the staged input ----------------
+    for (int idx = tid; idx < NE * NP; idx += BS) {
+        const R inv = met[idx + VS * DIM * DIM];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            R o = -acc[idx + VS * v] * inv;
+            if constexpr (SRC)
+                if (v >= 1 + DIM) o = fma(-p.invT, s[idx + VS * v], o);
+            s[idx + VS * v] = o;
+        }
+    }
+
+    // ---------------- write the finished chunk ----------------
+    if (fast) {
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid < 32) {
+            IO::store(p.out + gbase, buf, p.group, contiguous, tid);
+            bulk_wait_read_all();
+        }
+    } else {
+        __syncthreads();
+        const R* s0 = reinterpret_cast<const R*>(buf);
+        for (int idx = tid; idx < L::IN_WORDS; idx += BS) {
+            const long long e = E0 + idx % NE;
+            if (e < p.n_elem) {
+                const long long ge = e / p.group;
+                p.out[ge * p.group_words + (e - ge * p.group) + static_cast<long long>(p.group) * (idx / NE)] = s0[idx];
+            }
+        }
+    }
+}
+
+}  // namespace hfb

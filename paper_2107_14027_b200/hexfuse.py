@@ -342,6 +342,27 @@ def fused_divergence_device(pr: hf_problem, u, out, stream=None) -> None:
     check(_lib.load().hf_fused_divergence(C.byref(pr), _ptr(u), _ptr(out), _stream(stream)), "hf_fused_divergence")
 
 
+# ---- extension: elements with a non-constant Jacobian (include/hexfuse_b200.h)
+def geometry_words(pr: hf_problem) -> int:
+    """Words of the corner array: 2^d corners x d coordinates per element, AoSoA with the field's group."""
+    return int(_lib.load().hf_geometry_words(C.byref(pr)))
+
+
+def fused_divergence_mapped_device(pr: hf_problem, u, geom, out, stream=None) -> None:
+    """Fused divergence on (bi/tri)linear elements given by their corners: out = -(1/|J|) sum_a D_a(adj(J)_a. F)
+    (+ source); pr.jac and pr.method are ignored.  Device buffers, asynchronous on `stream`."""
+    check(_lib.load().hf_fused_divergence_mapped(C.byref(pr), _ptr(u), _ptr(geom), _ptr(out), _stream(stream)),
+          "hf_fused_divergence_mapped")
+
+
+def mapped_kernel_info(pr: hf_problem) -> dict:
+    ki = hf_kernel_info()
+    check(_lib.load().hf_mapped_kernel_info(C.byref(pr), C.byref(ki)), "hf_mapped_kernel_info")
+    return {"elems_per_cta": ki.elems_per_cta, "block_threads": ki.block_threads, "shared_bytes": ki.shared_bytes,
+            "registers": ki.registers, "grid": int(ki.grid), "bulk_path": bool(ki.bulk_path),
+            "blocks_per_sm": ki.blocks_per_sm, "name": ki.name.decode()}
+
+
 def fused_divergence_variant(pr: hf_problem, method: Method, variant: int, u, out, stream=None) -> None:
     """Tuning hook: launch a specific method/variant, bypassing the selection table."""
     check(_lib.load().hf_fused_divergence_variant(C.byref(pr), int(method), int(variant), _ptr(u), _ptr(out),
