@@ -130,6 +130,35 @@ HF_API int hf_fused_divergence_mapped(const hf_problem* pr, const void* u_dev, c
                                       void* stream);
 HF_API int hf_mapped_kernel_info(const hf_problem* pr, hf_kernel_info* out);
 
+/* ---- extension: the FR stages either side of the fused kernel ----
+ * PAPER.md Table 1 on a periodic structured mesh of dims[0] x dims[1] (x dims[2])
+ * elements, element e = ex + dims[0]*(ey + dims[1]*ez), the constant per-axis
+ * Jacobian pr->jac (the reference models these stages' I/O only):
+ *   hf_fr_project   stage 1: U_f = every a-line extrapolated to xi_a = -1, +1;
+ *   hf_fr_correct   stages 4+5: Rusanov common flux (wave speed
+ *                   |V_a| + sqrt(V_a^2 + zeta + nu/T)) and the DG correction
+ *                   -sum_a jac_a (g_L' jump_(-a) + g_R' jump_(+a)) added in place
+ *                   to divf_dev, which holds hf_fused_divergence's result;
+ *   hf_fr_residual  the whole right-hand side on one device (2+3+6, 1, 4+5).
+ * Face layout (AoSoA, the field's group, L = m^(d-1), l = transverse indices,
+ * s = 0 at xi = -1, 1 at +1):
+ *   word (e, a, s, l, v) = (e/group)*group*2*d*L*n_v + e%group + group*(l + L*(s + 2*(a + d*v))).
+ * Partitions (multi-GPU): whole element layers (layer = dims[0]*dims[1], d = 3;
+ * dims[0], d = 2), pr->n_elem = mesh->n_local, ghost_lo / ghost_hi = the face
+ * arrays (same layout) of the layer below / above the partition (periodic). */
+typedef struct hf_mesh {
+    int dims[3];
+    int64_t e_begin;  /* first element of the partition            */
+    int64_t n_local;  /* its elements (== pr->n_elem)               */
+    int64_t layer;    /* elements per ghost layer (partitions only) */
+} hf_mesh;
+HF_API int64_t hf_face_words(const hf_problem* pr);
+HF_API int hf_fr_project(const hf_problem* pr, const void* u_dev, void* uf_dev, void* stream);
+HF_API int hf_fr_correct(const hf_problem* pr, const hf_mesh* mesh, const void* uf_dev, const void* ghost_lo,
+                         const void* ghost_hi, void* divf_dev, void* stream);
+HF_API int hf_fr_residual(const hf_problem* pr, const int* dims, const void* u_dev, void* uf_dev, void* divf_dev,
+                          void* stream);
+
 /* ---- host-buffer entry point (the (b1) replacement) ----
  * u_host / divf_host: host arrays of hf_field_words(pr) words of the problem's
  * precision (float for HF_FP32, double for HF_FP64).  Pinned memory is used

@@ -93,6 +93,19 @@ def lib() -> C.CDLL:
         L.hfo_adjugate.restype = C.c_double
         L.hfo_oracle_divergence_mapped.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, C.c_double,
                                                    C.c_double, C.c_double, C.c_int]
+        L.hfo_face_words.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+        L.hfo_face_words.restype = _i64
+        L.hfo_face_interp.argtypes = [C.c_int, _dp, _dp]
+        L.hfo_correction_derivs.argtypes = [C.c_int, _dp, _dp]
+        L.hfo_max_wavespeed.argtypes = [C.c_int, _dp, C.c_int, C.c_double, C.c_double, C.c_double]
+        L.hfo_max_wavespeed.restype = C.c_double
+        L.hfo_common_flux.argtypes = [C.c_int, _dp, _dp, C.c_int, C.c_double, C.c_double, C.c_double, _dp]
+        L.hfo_common_flux.restype = None
+        L.hfo_project_faces.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_int, C.c_int]
+        L.hfo_fr_correct.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), _dp, _dp, C.c_double, C.c_double,
+                                     C.c_double, _dp, C.c_int, C.c_int]
+        L.hfo_fr_residual.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int), C.c_int, _dp, _dp, C.c_double,
+                                      C.c_double, C.c_double, _dp, C.c_int]
         _lib = L
     return _lib
 
@@ -123,6 +136,8 @@ def ref() -> C.CDLL:
         R.ref_time_oracle_mt.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_double,
                                          C.c_double, C.c_double, _dp, C.c_int, C.c_int]
         R.ref_time_oracle_mt.restype = C.c_double
+        R.ref_max_abs_eigenvalue.argtypes = [C.c_int, _dp, C.c_int, C.c_double, C.c_double, C.c_double]
+        R.ref_max_abs_eigenvalue.restype = C.c_double
         _ref = R
     return _ref
 
@@ -266,6 +281,67 @@ def oracle_divergence_mapped(d: int, p: int, n_elem: int, group: int, U: np.ndar
     if lib().hfo_oracle_divergence_mapped(d, p, n_elem, group, U, G, out, nu, zeta, T, int(with_source)) != 0:
         raise ValueError("oracle_divergence_mapped: invalid arguments")
     return out
+
+
+# ---- extension: the adjacent FR stages 1/4/5 on a periodic structured mesh
+def face_words(d: int, p: int, n_elem: int, group: int) -> int:
+    return int(lib().hfo_face_words(d, p, n_elem, group))
+
+
+def face_interp(m: int):
+    lm, lp = np.zeros(m), np.zeros(m)
+    lib().hfo_face_interp(m, lm, lp)
+    return lm, lp
+
+
+def correction_derivs(m: int):
+    gl, gr = np.zeros(m), np.zeros(m)
+    lib().hfo_correction_derivs(m, gl, gr)
+    return gl, gr
+
+
+def max_wavespeed(d: int, s, a: int, nu: float, zeta: float, T: float) -> float:
+    return float(lib().hfo_max_wavespeed(d, np.ascontiguousarray(s, dtype=np.float64), a, nu, zeta, T))
+
+
+def common_flux(d: int, UL, UR, a: int, nu: float, zeta: float, T: float) -> np.ndarray:
+    out = np.zeros(1 + d + d * d)
+    lib().hfo_common_flux(d, np.ascontiguousarray(UL, dtype=np.float64), np.ascontiguousarray(UR, dtype=np.float64),
+                          a, nu, zeta, T, out)
+    return out
+
+
+def project_faces(d: int, p: int, n_elem: int, group: int, U: np.ndarray) -> np.ndarray:
+    Uf = np.zeros(face_words(d, p, n_elem, group))
+    lib().hfo_project_faces(d, p, group, np.ascontiguousarray(U, dtype=np.float64), Uf, 0, n_elem)
+    return Uf
+
+
+def fr_correct(d: int, p: int, group: int, dims, Uf: np.ndarray, out: np.ndarray, nu: float, zeta: float, T: float,
+               jac, e_begin: int, e_end: int) -> None:
+    """Stages 4+5 in place on ``out`` for elements [e_begin, e_end) of the whole-mesh arrays."""
+    dims3 = (C.c_int * 3)(*(list(dims) + [1] * (3 - len(dims))))
+    if lib().hfo_fr_correct(d, p, group, dims3, Uf, out, nu, zeta, T, np.array(jac, dtype=np.float64),
+                            e_begin, e_end) != 0:
+        raise ValueError("fr_correct: invalid arguments")
+
+
+def fr_residual(d: int, p: int, dims, group: int, U: np.ndarray, nu: float, zeta: float, T: float,
+                jac=(1.0, 1.0, 1.0), with_source: bool = False) -> np.ndarray:
+    """Stages 1-6 of PAPER.md Table 1 on the periodic nx x ny (x nz) mesh."""
+    dims3 = (C.c_int * 3)(*(list(dims) + [1] * (3 - len(dims))))
+    n = int(np.prod(dims[:d]))
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    assert U.size == field_words(d, p, n, group)
+    out = np.zeros_like(U)
+    if lib().hfo_fr_residual(d, p, dims3, group, U, out, nu, zeta, T, np.array(jac, dtype=np.float64),
+                             int(with_source)) != 0:
+        raise ValueError("fr_residual: invalid arguments")
+    return out
+
+
+def ref_max_abs_eigenvalue(d: int, s, a: int, nu: float, zeta: float, T: float) -> float:
+    return float(ref().ref_max_abs_eigenvalue(d, np.ascontiguousarray(s, dtype=np.float64), a, nu, zeta, T))
 
 
 def field_rel_error(d: int, p: int, n_elem: int, group: int, got: np.ndarray, ref_: np.ndarray) -> float:

@@ -536,3 +536,191 @@ HFO_EXPORT int hfo_oracle_divergence_mapped(int d, int p, int n_elem, int group,
     memset(out, 0, sizeof(double) * (size_t)hfo_field_words(d, p, n_elem, group));
     return hfo_oracle_divergence_mapped_range(d, p, group, U, G, out, nu, zeta, T, with_source, 0, n_elem);
 }
+
+/* ===========================================================================
+ * EXTENSION beyond the reference: the adjacent FR stages around the fused
+ * kernel (Table 1, stages 1, 4, 5).  The reference
+ * models only their I/O; restated here from the paper's FR
+ * formulation on a periodic structured mesh of nx x ny (x nz) elements with
+ * the constant per-axis Jacobian of the reference, element
+ * e = ex + nx*(ey + ny*ez):
+ *
+ *   stage 1 (M)  U_f = the a-lines of every element extrapolated to xi_a = -1, +1
+ *                (Lagrange basis on the Gauss-Legendre nodes at +-1);
+ *   stage 4 (I)  Rusanov common flux at every face point, normal +x_a:
+ *                F^I = (F_a(UL) + F_a(UR))/2 - lambda (UR - UL)/2,
+ *                lambda = max over UL, UR of |V_a| + sqrt(V_a^2 + zeta + nu/T)
+ *                (the spectral radius of flux_jacobian, equations.hpp:112-140;
+ *                pinned against the reference's own eigenvalues, eig.hpp);
+ *   stage 5 (M)  DG correction: div^c = div^D + sum_a jac_a (g_L'(xi) (F^I - F^D)_(-a face)
+ *                                              + g_R'(xi) (F^I - F^D)_(+a face)),
+ *                g_L = (-1)^m/2 (P_m - P_{m-1}) (right Radau), g_R(x) = g_L(-x);
+ *   stage 6      out = -div^c (+ source), as the fused kernel.
+ *
+ * Face layout (AoSoA, the field's group; L = m^(d-1) lines per axis, l = the
+ * line's transverse indices in increasing axis order, s = 0 (xi = -1) / 1 (+1)):
+ *     word (e, a, s, l, v) = (e/group)*group*2*d*L*nv + e%group + group*(l + L*(s + 2*(a + d*v))).
+ * =========================================================================== */
+static inline int64_t face_offset(int d, int m, int group, int e, int a, int s, int l, int v) {
+    const int nv = 1 + d + d * d;
+    const int L = (d == 3) ? m * m : m;
+    return (int64_t)(e / group) * group * 2 * d * L * nv + e % group + (int64_t)group * (l + L * (s + 2 * (a + d * v)));
+}
+
+HFO_EXPORT int64_t hfo_face_words(int d, int p, int n_elem, int group) {
+    const int m = p + 1, nv = 1 + d + d * d, L = (d == 3) ? m * m : m;
+    const int64_t ng = (n_elem + group - 1) / group;
+    return ng * group * 2 * d * L * nv;
+}
+
+/* (i, j, k) of point t on line l of axis a */
+static inline void line_point(int d, int m, int a, int l, int t, int *i, int *j, int *k) {
+    const int t0 = l % m, t1 = l / m;
+    if (a == 0) { *i = t; *j = t0; *k = (d == 3) ? t1 : 0; }
+    else if (a == 1) { *i = t0; *j = t; *k = (d == 3) ? t1 : 0; }
+    else { *i = t0; *j = t1; *k = t; }
+}
+
+/* Lagrange basis of the Gauss-Legendre nodes at xi = -1 (side 0) and +1 (side 1). */
+HFO_EXPORT int hfo_face_interp(int m, double *lm, double *lp) {
+    double x[16];
+    if (hfo_gauss_legendre_points(m, x) != 0) return -1;
+    for (int t = 0; t < m; ++t) {
+        double a = 1.0, b = 1.0;
+        for (int q = 0; q < m; ++q) {
+            if (q == t) continue;
+            a *= (-1.0 - x[q]) / (x[t] - x[q]);
+            b *= (1.0 - x[q]) / (x[t] - x[q]);
+        }
+        lm[t] = a;
+        lp[t] = b;
+    }
+    return 0;
+}
+
+/* g_L'(x_i), g_R'(x_i) of the DG correction functions at the Gauss-Legendre nodes. */
+HFO_EXPORT int hfo_correction_derivs(int m, double *gl, double *gr) {
+    double x[16];
+    if (hfo_gauss_legendre_points(m, x) != 0) return -1;
+    for (int i = 0; i < m; ++i) {
+        for (int side = 0; side < 2; ++side) {
+            const double xx = side == 0 ? x[i] : -x[i];
+            /* Legendre P_n and P_n' by the three-term recurrence */
+            double p0 = 1.0, p1 = xx, d0 = 0.0, d1 = 1.0;
+            double pm1 = p0, dm1 = d0;  /* P_{m-1}, P_{m-1}' */
+            if (m - 1 == 1) { pm1 = p1; dm1 = d1; }
+            for (int n = 2; n <= m; ++n) {
+                const double p2 = ((2.0 * n - 1.0) * xx * p1 - (n - 1.0) * p0) / n;
+                const double d2 = d0 + (2.0 * n - 1.0) * p1;  /* P_n' = P_{n-2}' + (2n-1) P_{n-1} */
+                p0 = p1; p1 = p2; d0 = d1; d1 = d2;
+                if (n == m - 1) { pm1 = p1; dm1 = d1; }
+            }
+            (void)pm1;
+            const double sgn = (m % 2 == 0) ? 0.5 : -0.5;  /* (-1)^m / 2 */
+            const double gp = sgn * (d1 - dm1);             /* g_L'(xx) */
+            if (side == 0) gl[i] = gp;
+            else gr[i] = -gp;                               /* g_R'(x) = -g_L'(-x) */
+        }
+    }
+    return 0;
+}
+
+/* |V_a| + sqrt(V_a^2 + zeta + nu/T): spectral radius of the normal flux Jacobian. */
+HFO_EXPORT double hfo_max_wavespeed(int d, const double *s, int a, double nu, double zeta, double T) {
+    (void)d;
+    const double u = s[1 + a];
+    return fabs(u) + sqrt(u * u + zeta + nu / T);
+}
+
+/* Rusanov common flux, normal +x_a (all n_v rows). */
+HFO_EXPORT void hfo_common_flux(int d, const double *UL, const double *UR, int a, double nu, double zeta, double T,
+                                double *FI) {
+    const int nv = 1 + d + d * d;
+    double fl[3 * 13], fr[3 * 13];
+    hfo_flux(d, UL, nu, zeta, T, fl);
+    hfo_flux(d, UR, nu, zeta, T, fr);
+    const double ll = hfo_max_wavespeed(d, UL, a, nu, zeta, T), lr = hfo_max_wavespeed(d, UR, a, nu, zeta, T);
+    const double lam = ll > lr ? ll : lr;
+    for (int v = 0; v < nv; ++v) FI[v] = 0.5 * (fl[a * nv + v] + fr[a * nv + v]) - 0.5 * lam * (UR[v] - UL[v]);
+}
+
+/* Stage 1 over elements [e_begin, e_end). */
+HFO_EXPORT int hfo_project_faces(int d, int p, int group, const double *U, double *Uf, int e_begin, int e_end) {
+    const int m = p + 1, nv = 1 + d + d * d, L = (d == 3) ? m * m : m;
+    double lm[16], lp[16];
+    if (hfo_face_interp(m, lm, lp) != 0) return -1;
+    for (int e = e_begin; e < e_end; ++e)
+        for (int a = 0; a < d; ++a)
+            for (int l = 0; l < L; ++l)
+                for (int v = 0; v < nv; ++v) {
+                    double sm = 0.0, sp = 0.0;
+                    for (int t = 0; t < m; ++t) {
+                        int i, j, k;
+                        line_point(d, m, a, l, t, &i, &j, &k);
+                        const double u = U[field_offset(d, m, group, e, i, j, k, v)];
+                        sm += lm[t] * u;
+                        sp += lp[t] * u;
+                    }
+                    Uf[face_offset(d, m, group, e, a, 0, l, v)] = sm;
+                    Uf[face_offset(d, m, group, e, a, 1, l, v)] = sp;
+                }
+    return 0;
+}
+
+static inline int mesh_neighbor(int d, const int *dims, int e, int a, int dir) {
+    int c[3] = {e % dims[0], (e / dims[0]) % dims[1], (d == 3) ? e / (dims[0] * dims[1]) : 0};
+    c[a] = (c[a] + dir + dims[a]) % dims[a];
+    return c[0] + dims[0] * (c[1] + dims[1] * c[2]);
+}
+
+/* Stages 4 + 5 on elements [e_begin, e_end): out (holding -div^D (+src)) -= sum_a jac_a (...). */
+HFO_EXPORT int hfo_fr_correct(int d, int p, int group, const int *dims, const double *Uf, double *out, double nu,
+                              double zeta, double T, const double *jac, int e_begin, int e_end) {
+    const int m = p + 1, nv = 1 + d + d * d, L = (d == 3) ? m * m : m;
+    double gl[16], gr[16];
+    if (hfo_correction_derivs(m, gl, gr) != 0) return -1;
+    double UL[13], UR[13], FI[13], f[3 * 13], dm[13], dp[13];
+    for (int e = e_begin; e < e_end; ++e)
+        for (int a = 0; a < d; ++a) {
+            const int en = mesh_neighbor(d, dims, e, a, +1), ep = mesh_neighbor(d, dims, e, a, -1);
+            for (int l = 0; l < L; ++l) {
+                /* +a face: this element's +1 side against the +a neighbour's -1 side */
+                for (int v = 0; v < nv; ++v) {
+                    UL[v] = Uf[face_offset(d, m, group, e, a, 1, l, v)];
+                    UR[v] = Uf[face_offset(d, m, group, en, a, 0, l, v)];
+                }
+                hfo_common_flux(d, UL, UR, a, nu, zeta, T, FI);
+                hfo_flux(d, UL, nu, zeta, T, f);
+                for (int v = 0; v < nv; ++v) dp[v] = FI[v] - f[a * nv + v];
+                /* -a face: the -a neighbour's +1 side against this element's -1 side */
+                for (int v = 0; v < nv; ++v) {
+                    UL[v] = Uf[face_offset(d, m, group, ep, a, 1, l, v)];
+                    UR[v] = Uf[face_offset(d, m, group, e, a, 0, l, v)];
+                }
+                hfo_common_flux(d, UL, UR, a, nu, zeta, T, FI);
+                hfo_flux(d, UR, nu, zeta, T, f);
+                for (int v = 0; v < nv; ++v) dm[v] = FI[v] - f[a * nv + v];
+                for (int t = 0; t < m; ++t) {
+                    int i, j, k;
+                    line_point(d, m, a, l, t, &i, &j, &k);
+                    for (int v = 0; v < nv; ++v)
+                        out[field_offset(d, m, group, e, i, j, k, v)] -= jac[a] * (gl[t] * dm[v] + gr[t] * dp[v]);
+                }
+            }
+        }
+    return 0;
+}
+
+/* The full FR right-hand side on the periodic mesh: stages 1-6. */
+HFO_EXPORT int hfo_fr_residual(int d, int p, const int *dims, int group, const double *U, double *out, double nu,
+                               double zeta, double T, const double *jac, int with_source) {
+    const int n = dims[0] * dims[1] * ((d == 3) ? dims[2] : 1);
+    if (hfo_oracle_divergence(d, p, n, group, U, out, nu, zeta, T, jac, with_source) != 0) return -1;
+    const int64_t fw = hfo_face_words(d, p, n, group);
+    double *Uf = (double *)calloc((size_t)fw, sizeof(double));
+    if (!Uf) return -1;
+    int rc = hfo_project_faces(d, p, group, U, Uf, 0, n);
+    if (rc == 0) rc = hfo_fr_correct(d, p, group, dims, Uf, out, nu, zeta, T, jac, 0, n);
+    free(Uf);
+    return rc;
+}

@@ -15,8 +15,12 @@
 //   ref_gl_derivative      -> gauss_legendre_points + derivative_matrix (operators.hpp:17-74)
 //   ref_time_oracle_mt     -> oracle_divergence on T group-aligned sub-fields, one
 //                             std::thread each (the function is pure)
+//   ref_max_abs_eigenvalue -> max |eigenvalues(flux_jacobian(s, params, e_a))|
+//                             (equations.hpp:112-130, eig.hpp:15): pins the Rusanov
+//                             wave speed of the FR interface stage (hexfuse_oracle.c)
 #include <hexfuse/oracle.hpp>
 #include <hexfuse/verify.hpp>
+#include <hexfuse/eig.hpp>
 
 #include <algorithm>
 #include <chrono>
@@ -162,6 +166,20 @@ double ref_time_oracle_mt(int d, int p, int n_elem, int group, int fp32, const d
         g_err = e.what();
         return -1.0;
     }
+}
+
+double ref_max_abs_eigenvalue(int d, const double* s, int a, double nu, double zeta, double T) {
+    double r = -1.0;
+    guarded([&] {
+        AcmHdState st(d);
+        for (int v = 0; v < n_vars(d); ++v) st.v[static_cast<std::size_t>(v)] = s[v];
+        PhysParams par{nu, zeta, T};
+        std::vector<double> dir(static_cast<std::size_t>(d), 0.0);
+        dir[static_cast<std::size_t>(a)] = 1.0;
+        r = 0.0;
+        for (const auto& ev : eigenvalues(flux_jacobian(st, par, dir))) r = std::max(r, std::abs(ev));
+    });
+    return r;
 }
 
 }  // extern "C"

@@ -23,6 +23,11 @@ from .hexfuse import (  # noqa: F401
     fused_divergence,
     fused_divergence_device,
     fused_divergence_mapped_device,
+    face_words,
+    fr_correct_device,
+    fr_project_device,
+    fr_residual_device,
+    make_mesh,
     geometry_words,
     mapped_kernel_info,
     fused_divergence_variant,

@@ -54,7 +54,12 @@ EXPORTED = [
     "hf_fused_divergence", "hf_unfused_workspace_bytes", "hf_unfused_divergence", "hf_context_create",
     "hf_context_destroy", "hf_fused_divergence_host", "hf_partition", "hf_last_error", "hf_version",
     "hf_geometry_words", "hf_fused_divergence_mapped", "hf_mapped_kernel_info",
+    "hf_face_words", "hf_fr_project", "hf_fr_correct", "hf_fr_residual",
 ]
+
+
+class hf_mesh(C.Structure):
+    _fields_ = [("dims", C.c_int * 3), ("e_begin", C.c_int64), ("n_local", C.c_int64), ("layer", C.c_int64)]
 
 _lib = None
 
@@ -108,6 +113,11 @@ def load() -> C.CDLL:
     L.hf_geometry_words.restype = C.c_int64
     L.hf_fused_divergence_mapped.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     L.hf_mapped_kernel_info.argtypes = [P, C.POINTER(hf_kernel_info)]
+    L.hf_face_words.argtypes = [P]
+    L.hf_face_words.restype = C.c_int64
+    L.hf_fr_project.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.hf_fr_correct.argtypes = [P, C.POINTER(hf_mesh), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.hf_fr_residual.argtypes = [P, C.POINTER(C.c_int), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     _lib = L
     return L
 

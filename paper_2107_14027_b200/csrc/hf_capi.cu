@@ -14,6 +14,7 @@
 
 #include "../../include/hexfuse_b200.h"
 #include "hf_dispatch.cuh"
+#include "hf_fr.cuh"
 
 namespace {
 
@@ -184,6 +185,55 @@ hfb::Params<R> make_params(const hf_problem* pr, const void* u, void* out, void*
     return p;
 }
 
+// FR stage parameters: Lagrange basis at -1/+1 and the DG correction-function
+// derivatives g_L'(x_i), g_R'(x_i) (g_L = (-1)^m/2 (P_m - P_{m-1}), g_R(x) = g_L(-x)).
+template <class R>
+hfb::FrParams<R> make_fr_params(const hf_problem* pr, const hf_mesh* mesh, const void* uf, const void* glo,
+                                const void* ghi) {
+    hfb::FrParams<R> f;
+    std::memset(&f, 0, sizeof(f));
+    const int m = pr->p + 1;
+    const double* x = ops().x[m];
+    for (int t = 0; t < m; ++t) {
+        double a = 1.0, b = 1.0;
+        for (int q = 0; q < m; ++q) {
+            if (q == t) continue;
+            a *= (-1.0 - x[q]) / (x[t] - x[q]);
+            b *= (1.0 - x[q]) / (x[t] - x[q]);
+        }
+        f.lm[t] = R(a);
+        f.lp[t] = R(b);
+    }
+    auto gl_deriv = [m](double xx) {
+        double p0 = 1.0, p1 = xx, d0 = 0.0, d1 = 1.0, dm1 = 1.0;  // P_n, P_n' recurrences
+        for (int n = 2; n <= m; ++n) {
+            const double p2 = ((2.0 * n - 1.0) * xx * p1 - (n - 1.0) * p0) / n;
+            const double d2 = d0 + (2.0 * n - 1.0) * p1;
+            p0 = p1;
+            p1 = p2;
+            d0 = d1;
+            d1 = d2;
+            if (n == m - 1) dm1 = d1;
+        }
+        return ((m % 2 == 0) ? 0.5 : -0.5) * (d1 - dm1);
+    };
+    for (int i = 0; i < m; ++i) {
+        f.gl[i] = R(gl_deriv(x[i]));
+        f.gr[i] = R(-gl_deriv(-x[i]));
+    }
+    if (mesh) {
+        for (int a = 0; a < 3; ++a) f.mesh.dims[a] = mesh->dims[a];
+        if (pr->d == 2) f.mesh.dims[2] = 1;
+        f.mesh.e_begin = mesh->e_begin;
+        f.mesh.n_local = mesh->n_local;
+        f.mesh.layer = mesh->layer;
+    }
+    f.uf = static_cast<const R*>(uf);
+    f.ghost_lo = static_cast<const R*>(glo);
+    f.ghost_hi = static_cast<const R*>(ghi);
+    return f;
+}
+
 // Resolve + launch (dry: describe only).  ws only for the unfused method.
 int dispatch(const hf_problem* pr, const void* u, void* out, void* ws, cudaStream_t st, hfb::KInfo* info, bool dry,
              int force_method = -1, int force_variant = -1) {
@@ -305,6 +355,13 @@ size_t hf_unfused_workspace_bytes(const hf_problem* pr) {
     return size_t(hf_field_words(pr)) * size_t(pr->d) * word_bytes(pr);
 }
 
+int64_t hf_face_words(const hf_problem* pr) {
+    if (!pr || pr->group < 1 || (pr->d != 2 && pr->d != 3) || pr->n_elem < 0) return -1;
+    const int m = pr->p + 1;
+    const int64_t ng = (pr->n_elem + pr->group - 1) / pr->group;
+    return ng * pr->group * 2 * pr->d * ipow64(m, pr->d - 1) * (1 + pr->d + pr->d * pr->d);
+}
+
 int64_t hf_geometry_words(const hf_problem* pr) {
     if (!pr || pr->group < 1 || (pr->d != 2 && pr->d != 3) || pr->n_elem < 0) return -1;
     const int64_t ng = (pr->n_elem + pr->group - 1) / pr->group;
@@ -354,6 +411,71 @@ int hf_mapped_kernel_info(const hf_problem* pr, hf_kernel_info* out) {
     out->blocks_per_sm = ki.blocks_per_sm;
     std::memcpy(out->name, ki.name, sizeof(out->name));
     return HF_OK;
+}
+
+int hf_fr_project(const hf_problem* pr, const void* u_dev, void* uf_dev, void* stream) {
+    if (int rc = validate(pr)) return rc;
+    if (pr->n_elem > 0 && (!u_dev || !uf_dev)) return fail(HF_EINVAL, "hf_fr_project: null buffer");
+    int rc;
+    if (pr->precision == HF_FP32) {
+        const auto prm = make_params<float>(pr, u_dev, nullptr, nullptr);
+        const auto fp = make_fr_params<float>(pr, nullptr, nullptr, nullptr, nullptr);
+        rc = hfb::fr_f32(1, pr->d, pr->p, prm, fp, static_cast<float*>(uf_dev), static_cast<cudaStream_t>(stream));
+    } else {
+        const auto prm = make_params<double>(pr, u_dev, nullptr, nullptr);
+        const auto fp = make_fr_params<double>(pr, nullptr, nullptr, nullptr, nullptr);
+        rc = hfb::fr_f64(1, pr->d, pr->p, prm, fp, static_cast<double*>(uf_dev), static_cast<cudaStream_t>(stream));
+    }
+    if (rc < 0) return fail(HF_EINVAL, "hf_fr_project: unsupported (d, p)");
+    if (rc != 0) return cuda_fail(cudaError_t(rc), "hf_fr_project launch");
+    return HF_OK;
+}
+
+int hf_fr_correct(const hf_problem* pr, const hf_mesh* mesh, const void* uf_dev, const void* ghost_lo,
+                  const void* ghost_hi, void* divf_dev, void* stream) {
+    if (int rc = validate(pr)) return rc;
+    if (!mesh) return fail(HF_EINVAL, "hf_fr_correct: null mesh");
+    const int64_t nz = pr->d == 3 ? mesh->dims[2] : 1;
+    if (mesh->dims[0] < 1 || mesh->dims[1] < 1 || nz < 1) return fail(HF_EINVAL, "hf_fr_correct: bad mesh dims");
+    const int64_t n_mesh = int64_t(mesh->dims[0]) * mesh->dims[1] * nz;
+    if (mesh->n_local != pr->n_elem || mesh->e_begin < 0 || mesh->e_begin + mesh->n_local > n_mesh)
+        return fail(HF_EINVAL, "hf_fr_correct: partition must be n_elem elements inside the mesh");
+    if (mesh->n_local < n_mesh) {
+        const int64_t layer = pr->d == 3 ? int64_t(mesh->dims[0]) * mesh->dims[1] : mesh->dims[0];
+        if (mesh->layer != layer || mesh->e_begin % layer || mesh->n_local % layer || !ghost_lo || !ghost_hi)
+            return fail(HF_EINVAL, "hf_fr_correct: a partition must be whole element layers with both ghost layers");
+    }
+    if (pr->n_elem > 0 && (!uf_dev || !divf_dev)) return fail(HF_EINVAL, "hf_fr_correct: null buffer");
+    int rc;
+    if (pr->precision == HF_FP32) {
+        const auto prm = make_params<float>(pr, nullptr, divf_dev, nullptr);
+        const auto fp = make_fr_params<float>(pr, mesh, uf_dev, ghost_lo, ghost_hi);
+        rc = hfb::fr_f32(2, pr->d, pr->p, prm, fp, nullptr, static_cast<cudaStream_t>(stream));
+    } else {
+        const auto prm = make_params<double>(pr, nullptr, divf_dev, nullptr);
+        const auto fp = make_fr_params<double>(pr, mesh, uf_dev, ghost_lo, ghost_hi);
+        rc = hfb::fr_f64(2, pr->d, pr->p, prm, fp, nullptr, static_cast<cudaStream_t>(stream));
+    }
+    if (rc < 0) return fail(HF_EINVAL, "hf_fr_correct: unsupported (d, p)");
+    if (rc != 0) return cuda_fail(cudaError_t(rc), "hf_fr_correct launch");
+    return HF_OK;
+}
+
+int hf_fr_residual(const hf_problem* pr, const int* dims, const void* u_dev, void* uf_dev, void* divf_dev,
+                   void* stream) {
+    if (!dims) return fail(HF_EINVAL, "hf_fr_residual: null dims");
+    hf_mesh ms{};
+    ms.dims[0] = dims[0];
+    ms.dims[1] = dims[1];
+    ms.dims[2] = pr && pr->d == 3 ? dims[2] : 1;
+    ms.e_begin = 0;
+    ms.n_local = pr ? pr->n_elem : 0;
+    ms.layer = 0;
+    if (pr && int64_t(ms.dims[0]) * ms.dims[1] * ms.dims[2] != pr->n_elem)
+        return fail(HF_EINVAL, "hf_fr_residual: n_elem must equal the mesh's element count");
+    if (int rc = hf_fused_divergence(pr, u_dev, divf_dev, stream)) return rc;  // stages 2+3+6
+    if (int rc = hf_fr_project(pr, u_dev, uf_dev, stream)) return rc;        // stage 1
+    return hf_fr_correct(pr, &ms, uf_dev, nullptr, nullptr, divf_dev, stream);  // stages 4+5
 }
 
 int hf_unfused_divergence(const hf_problem* pr, const void* u_dev, void* divf_dev, void* ws_dev, void* stream) {

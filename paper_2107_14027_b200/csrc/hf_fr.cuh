@@ -1,0 +1,361 @@
+// hf_fr.cuh -- the FR stages either side of the fused kernel (Table 1,
+// stages 1, 4, 5), on a periodic structured mesh with the
+// reference's constant per-axis Jacobian.  EXTENSION beyond the reference,
+// which models only their I/O; oracle: hfo_project_faces /
+// hfo_fr_correct / hfo_fr_residual (oracle/hexfuse_oracle.c).
+//
+//   stage 1  hf_fr_project_kernel: each CTA stages a chunk of NE elements
+//            (bulk copy, as the lines kernel) and extrapolates every a-line of
+//            every variable to xi_a = -1, +1 (Lagrange basis at +-1) -> U_f.
+//   stage 4+5 hf_fr_correct_kernel: per element, the Rusanov common flux at
+//            both ends of every line (own U_f against the neighbour's, wave
+//            speed |V_a| + sqrt(V_a^2 + zeta + nu/T)), the jumps
+//            F^I - F_a(U_f) into shared memory, then per solution point
+//            out -= sum_a jac_a (g_L'(xi) jump_(-a) + g_R'(xi) jump_(+a)) over the
+//            fused kernel's -div^D (+ source) in place.
+//
+// Face layout (AoSoA, the field's group; L = m^(d-1)):
+//     word (e, a, s, l, v) = (e/group)*group*2*d*L*n_v + e%group + group*(l + L*(s + 2*(a + d*v))).
+// Multi-GPU: a rank owns whole element layers (ex, ey planes of the mesh);
+// the faces of the layers just below / above its slab arrive as ghost arrays
+// (same layout, one layer each) through NCCL (multi_gpu.FrSlab).
+#pragma once
+
+#include "hf_lines.cuh"
+
+namespace hfb {
+
+struct FrMesh {
+    int dims[3];         // elements per axis (dims[2] = 1 for d = 2)
+    long long e_begin;   // first (global) element of this partition
+    long long n_local;   // elements of this partition (whole layers unless single-partition)
+    long long layer;     // elements per ghost layer (dims[0] * dims[1] for d = 3, dims[0] for d = 2)
+};
+
+template <class R>
+struct FrParams {
+    R lm[kMaxM], lp[kMaxM];  // Lagrange basis at xi = -1, +1
+    R gl[kMaxM], gr[kMaxM];  // g_L'(x_i), g_R'(x_i) of the DG correction functions
+    FrMesh mesh;
+    const R* __restrict__ uf;       // local faces
+    const R* __restrict__ ghost_lo;  // faces of the layer below the partition (or nullptr)
+    const R* __restrict__ ghost_hi;  // faces of the layer above
+};
+
+template <int DIM, int M>
+__host__ __device__ constexpr int fr_lines() {
+    return ipow_c(M, DIM - 1);
+}
+
+__device__ __forceinline__ long long face_word(int dim, int m, long long group, long long e, int a, int s, int l,
+                                               int v) {
+    const int nv = 1 + dim + dim * dim;
+    const int L = dim == 3 ? m * m : m;
+    return (e / group) * group * 2 * dim * L * nv + e % group + group * (l + (long long)L * (s + 2 * (a + dim * v)));
+}
+
+// line l of axis a, point t -> point index i + m j + m^2 k
+template <int DIM, int M>
+__device__ __forceinline__ int fr_line_point(int a, int l, int t) {
+    const int t0 = l % M, t1 = l / M;
+    if (a == 0) return t + M * t0 + M * M * (DIM == 3 ? t1 : 0);
+    if (a == 1) return t0 + M * t + M * M * (DIM == 3 ? t1 : 0);
+    return t0 + M * t1 + M * M * t;
+}
+
+// ---------------------------------------------------------------------------------------------
+// stage 1
+// ---------------------------------------------------------------------------------------------
+template <class R, int DIM, int M, int NE>
+struct FrProjShape {
+    using L = LinesShape<R, DIM, M, NE>;
+    static constexpr int NV = n_vars_c(DIM);
+    static constexpr int BS = L::BS;
+    static constexpr int HDR = 128;
+    static constexpr size_t SMEM = HDR + size_t(L::BUF_BYTES);
+};
+
+template <class R, int DIM, int M, int NE>
+__global__ void __launch_bounds__(FrProjShape<R, DIM, M, NE>::BS)
+    hf_fr_project_kernel(const __grid_constant__ Params<R> p, const __grid_constant__ FrParams<R> f, R* __restrict__ uf) {
+    using S = FrProjShape<R, DIM, M, NE>;
+    using L = typename S::L;
+    using IO = typename L::IO;
+    constexpr int BS = S::BS, NV = S::NV, NP = L::NP, LN = fr_lines<DIM, M>();
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    unsigned char* buf = smem_raw + S::HDR;
+    const int tid = threadIdx.x;
+    const long long E0 = static_cast<long long>(blockIdx.x) * NE;
+    const long long grp = E0 / p.group;
+    const long long gbase = grp * p.group_words + (E0 - grp * p.group);
+    const bool contiguous = (p.group == NE);
+    const bool fast = chunk_bulk_ok<R, L::IN_WORDS>(p, gbase, E0 + NE <= p.n_elem, contiguous);
+    const int head = fast ? IO::head_bytes(p.u + gbase, contiguous) : 0;
+    if (fast) {
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (tid < 32) {
+            if (tid == 0) mbar_arrive_expect_tx(bar, IO::tx_bytes(p.u + gbase, contiguous));
+            __syncwarp();
+            IO::load(buf, p.u + gbase, p.group, contiguous, bar, tid);
+        }
+        mbar_wait_parity(bar, 0);
+    } else {
+        R* s0 = reinterpret_cast<R*>(buf);
+        for (int idx = tid; idx < L::IN_WORDS; idx += BS) {
+            const long long e = E0 + idx % NE;
+            R v = R(0);
+            if (e < p.n_elem) {
+                const long long ge = e / p.group;
+                v = ld_stream(p.u + ge * p.group_words + (e - ge * p.group) + static_cast<long long>(p.group) * (idx / NE));
+            }
+            s0[idx] = v;
+        }
+        __syncthreads();
+    }
+    const R* s = reinterpret_cast<const R*>(buf + head);
+    // one task = (element, axis, line, variable): both ends of the line, coalesced over the element
+    for (int task = tid; task < NE * DIM * LN * NV; task += BS) {
+        const int el = task % NE;
+        int r = task / NE;
+        const int l = r % LN;
+        r /= LN;
+        const int a = r % DIM;
+        const int v = r / DIM;
+        const long long e = E0 + el;
+        if (e >= p.n_elem) continue;
+        R sm = R(0), sp = R(0);
+#pragma unroll
+        for (int t = 0; t < M; ++t) {
+            const R u = s[el + NE * (fr_line_point<DIM, M>(a, l, t) + NP * v)];
+            sm = fma(f.lm[t], u, sm);
+            sp = fma(f.lp[t], u, sp);
+        }
+        uf[face_word(DIM, M, p.group, e, a, 0, l, v)] = sm;
+        uf[face_word(DIM, M, p.group, e, a, 1, l, v)] = sp;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// stages 4 + 5
+// ---------------------------------------------------------------------------------------------
+// Locate the faces of global element eg: local buffer, or a ghost layer.
+template <class R>
+__device__ __forceinline__ const R* fr_faces_of(const FrParams<R>& f, long long eg, long long n_mesh, long long* e_loc) {
+    const FrMesh& ms = f.mesh;
+    long long rel = eg - ms.e_begin;
+    if (rel < 0) rel += n_mesh;
+    if (rel < ms.n_local) {
+        *e_loc = rel;
+        return f.uf;
+    }
+    if (rel < ms.n_local + ms.layer) {  // the layer above the partition
+        *e_loc = rel - ms.n_local;
+        return f.ghost_hi;
+    }
+    *e_loc = rel - (n_mesh - ms.layer);  // the layer below (wrapped)
+    return f.ghost_lo;
+}
+
+template <class R, int DIM, int M, int NE>
+struct FrCorrShape {
+    static constexpr int NV = n_vars_c(DIM);
+    static constexpr int LN = fr_lines<DIM, M>();
+    static constexpr int TASKS = NE * DIM * LN;  // (element, axis, line)
+    static constexpr int BS = ((TASKS + 31) / 32) * 32 < 64 ? 64 : (((TASKS + 31) / 32) * 32 > 256 ? 256 : ((TASKS + 31) / 32) * 32);
+    static constexpr size_t SMEM = size_t(TASKS) * 2 * NV * sizeof(R);  // jumps [v][s][a][l][el]
+};
+
+template <class R, int DIM>
+__device__ __forceinline__ void fr_flux_normal(const R (&U)[n_vars_c(DIM)], int a, const Params<R>& p,
+                                               R (&F)[n_vars_c(DIM)]) {
+    constexpr int NV = n_vars_c(DIM);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) F[v] = R(0);
+    R Va = U[1];
+#pragma unroll
+    for (int b = 1; b < DIM; ++b)
+        if (a == b) Va = U[1 + b];
+    F[0] = p.zeta * Va;
+#pragma unroll
+    for (int b = 0; b < DIM; ++b) {
+        R g = R(0);
+#pragma unroll
+        for (int c = 0; c < DIM; ++c)
+            if (c == a) g = U[var_grad_c(DIM, b, c)];
+        R mom = U[1 + b] * Va - p.nu * g;  // equations.hpp:70-83
+        if (a == b) mom += U[0];
+        F[1 + b] = mom;
+#pragma unroll
+        for (int c = 0; c < DIM; ++c)
+            if (c == a) F[var_grad_c(DIM, b, c)] = -U[1 + b] * p.invT;
+    }
+}
+
+template <class R, int DIM>
+__device__ __forceinline__ R fr_wavespeed(const R (&U)[n_vars_c(DIM)], int a, const Params<R>& p) {
+    R Va = U[1];
+#pragma unroll
+    for (int b = 1; b < DIM; ++b)
+        if (a == b) Va = U[1 + b];
+    return fabs(Va) + sqrt(Va * Va + p.zeta + p.nu * p.invT);
+}
+
+template <class R, int DIM, int M, int NE>
+__global__ void __launch_bounds__(FrCorrShape<R, DIM, M, NE>::BS)
+    hf_fr_correct_kernel(const __grid_constant__ Params<R> p, const __grid_constant__ FrParams<R> f) {
+    using S = FrCorrShape<R, DIM, M, NE>;
+    constexpr int NV = S::NV, LN = S::LN, BS = S::BS, NP = ipow_c(M, DIM);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    R* jump = reinterpret_cast<R*>(smem_raw);  // [v][s][a][l][el]
+    auto jidx = [](int el, int a, int s, int l, int v) { return el + NE * (l + LN * (a + DIM * (s + 2 * v))); };
+    const int tid = threadIdx.x;
+    const long long E0 = static_cast<long long>(blockIdx.x) * NE;
+    const long long n_mesh = (long long)f.mesh.dims[0] * f.mesh.dims[1] * (DIM == 3 ? f.mesh.dims[2] : 1);
+
+    // ---- stage 4: common fluxes and jumps at both ends of every line
+    for (int task = tid; task < S::TASKS; task += BS) {
+        const int el = task % NE;
+        const int l = (task / NE) % LN;
+        const int a = task / (NE * LN);
+        const long long e = E0 + el;  // local element
+        if (e >= p.n_elem) continue;
+        const long long eg = f.mesh.e_begin + e;
+        int c[3] = {int(eg % f.mesh.dims[0]), int((eg / f.mesh.dims[0]) % f.mesh.dims[1]),
+                    DIM == 3 ? int(eg / ((long long)f.mesh.dims[0] * f.mesh.dims[1])) : 0};
+        for (int s = 0; s < 2; ++s) {
+            // side s = 1: this element's +a face vs the +a neighbour's -1 side; s = 0: the -a face
+            int cn[3] = {c[0], c[1], c[2]};
+            cn[a] = (cn[a] + (s ? 1 : -1) + f.mesh.dims[a]) % f.mesh.dims[a];
+            const long long en = cn[0] + (long long)f.mesh.dims[0] * (cn[1] + (long long)f.mesh.dims[1] * cn[2]);
+            long long enl;
+            const R* nb = fr_faces_of(f, en, n_mesh, &enl);
+            R Uo[NV], Un[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                Uo[v] = f.uf[face_word(DIM, M, p.group, e, a, s, l, v)];
+                Un[v] = nb[face_word(DIM, M, p.group, enl, a, 1 - s, l, v)];
+            }
+            R Fo[NV], Fn[NV];
+            fr_flux_normal<R, DIM>(Uo, a, p, Fo);
+            fr_flux_normal<R, DIM>(Un, a, p, Fn);
+            const R lam = fmax(fr_wavespeed<R, DIM>(Uo, a, p), fr_wavespeed<R, DIM>(Un, a, p));
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                // UL / UR in the +x_a orientation of the face
+                const R ul = s ? Uo[v] : Un[v], ur = s ? Un[v] : Uo[v];
+                const R fl = s ? Fo[v] : Fn[v], fr = s ? Fn[v] : Fo[v];
+                const R FI = R(0.5) * (fl + fr) - R(0.5) * lam * (ur - ul);
+                jump[jidx(el, a, s, l, v)] = FI - Fo[v];
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- stage 5: corrections at every solution point, over the fused kernel's result
+    for (int task = tid; task < NE * NP; task += BS) {
+        const int el = task % NE;
+        const int pt = task / NE;
+        const long long e = E0 + el;
+        if (e >= p.n_elem) continue;
+        const int i = pt % M, j = (pt / M) % M, k = pt / (M * M);
+        const long long ge = e / p.group;
+        R* ob = p.out + ge * p.group_words + (e - ge * p.group);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            R corr = R(0);
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                const int t = a == 0 ? i : (a == 1 ? j : k);
+                const int l = a == 0 ? (j + M * k) : (a == 1 ? (i + M * k) : (i + M * j));
+                corr = fma(p.jac[a], fma(f.gl[t], jump[jidx(el, a, 0, l, v)], f.gr[t] * jump[jidx(el, a, 1, l, v)]), corr);
+            }
+            R* q = ob + static_cast<long long>(p.group) * (pt + NP * v);
+            *q = *q - corr;
+        }
+    }
+}
+
+}  // namespace hfb
+
+// ---------------------------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------------------------
+namespace hfb {
+
+template <class R, int DIM, int M>
+constexpr int fr_proj_ne() {
+    int ne = 32;  // <= 72 KB of staged chunk, a multiple of the row alignment not required (any NE)
+    while (ne > 1 && (size_t(ne) * ipow_c(M, DIM) * n_vars_c(DIM) * sizeof(R) > size_t(72 * 1024) ||
+                      ne * ipow_c(M, DIM - 1) > 512))
+        ne /= 2;
+    return ne;
+}
+
+template <class R, int DIM, int M>
+constexpr int fr_corr_ne() {
+    int ne = 32;
+    while (ne > 1 && size_t(ne) * DIM * ipow_c(M, DIM - 1) * 2 * n_vars_c(DIM) * sizeof(R) > size_t(48 * 1024)) ne /= 2;
+    return ne;
+}
+
+template <class R, int DIM, int M>
+int fr_stage(int which, const Params<R>& prm, const FrParams<R>& fp, R* uf, cudaStream_t st) {
+    if (prm.n_elem == 0) return 0;
+    if (which == 1) {
+        constexpr int NE = fr_proj_ne<R, DIM, M>();
+        using S = FrProjShape<R, DIM, M, NE>;
+        auto kernel = hf_fr_project_kernel<R, DIM, M, NE>;
+        Params<R> p = prm;
+        p.fast_ok = (p.group == NE || (p.group % NE == 0 && (NE * sizeof(R)) % 16 == 0 &&
+                                       ((long long)p.group * sizeof(R)) % 16 == 0)) &&
+                    (reinterpret_cast<uintptr_t>(p.u) & 15u) == 0;
+        if (S::SMEM > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM));
+            if (e != cudaSuccess) return int(e);
+        }
+        kernel<<<unsigned((p.n_elem + NE - 1) / NE), S::BS, S::SMEM, st>>>(p, fp, uf);
+    } else {
+        constexpr int NE = fr_corr_ne<R, DIM, M>();
+        using S = FrCorrShape<R, DIM, M, NE>;
+        auto kernel = hf_fr_correct_kernel<R, DIM, M, NE>;
+        kernel<<<unsigned((prm.n_elem + NE - 1) / NE), S::BS, S::SMEM, st>>>(prm, fp);
+    }
+    return int(cudaGetLastError());
+}
+
+template <class R>
+int run_fr_impl(int which, int d, int p, const Params<R>& prm, const FrParams<R>& fp, R* uf, cudaStream_t st) {
+    if (d == 3) {
+        switch (p) {
+            case 1: return fr_stage<R, 3, 2>(which, prm, fp, uf, st);
+            case 2: return fr_stage<R, 3, 3>(which, prm, fp, uf, st);
+            case 3: return fr_stage<R, 3, 4>(which, prm, fp, uf, st);
+            case 4: return fr_stage<R, 3, 5>(which, prm, fp, uf, st);
+            case 5: return fr_stage<R, 3, 6>(which, prm, fp, uf, st);
+            case 6: return fr_stage<R, 3, 7>(which, prm, fp, uf, st);
+            case 7: return fr_stage<R, 3, 8>(which, prm, fp, uf, st);
+            default: return -1;
+        }
+    }
+    switch (p) {
+        case 1: return fr_stage<R, 2, 2>(which, prm, fp, uf, st);
+        case 2: return fr_stage<R, 2, 3>(which, prm, fp, uf, st);
+        case 3: return fr_stage<R, 2, 4>(which, prm, fp, uf, st);
+        case 4: return fr_stage<R, 2, 5>(which, prm, fp, uf, st);
+        case 5: return fr_stage<R, 2, 6>(which, prm, fp, uf, st);
+        case 6: return fr_stage<R, 2, 7>(which, prm, fp, uf, st);
+        case 7: return fr_stage<R, 2, 8>(which, prm, fp, uf, st);
+        case 8: return fr_stage<R, 2, 9>(which, prm, fp, uf, st);
+        default: return -1;
+    }
+}
+
+int fr_f32(int which, int d, int p, const Params<float>&, const FrParams<float>&, float*, cudaStream_t);
+int fr_f64(int which, int d, int p, const Params<double>&, const FrParams<double>&, double*, cudaStream_t);
+
+}  // namespace hfb

@@ -363,6 +363,43 @@ def mapped_kernel_info(pr: hf_problem) -> dict:
             "blocks_per_sm": ki.blocks_per_sm, "name": ki.name.decode()}
 
 
+# ---- extension: FR stages 1 / 4+5 around the fused kernel (include/hexfuse_b200.h)
+def face_words(pr: hf_problem) -> int:
+    """Words of the face array U_f: 2 d m^(d-1) n_v per element, AoSoA with the field's group."""
+    return int(_lib.load().hf_face_words(C.byref(pr)))
+
+
+def make_mesh(dims, d: int, e_begin: int = 0, n_local: int | None = None, layer: int = 0):
+    ms = _lib.hf_mesh()
+    for a in range(3):
+        ms.dims[a] = int(dims[a]) if a < len(dims) else 1
+    if d == 2:
+        ms.dims[2] = 1
+    n_mesh = ms.dims[0] * ms.dims[1] * ms.dims[2]
+    ms.e_begin, ms.n_local, ms.layer = int(e_begin), int(n_mesh if n_local is None else n_local), int(layer)
+    return ms
+
+
+def fr_project_device(pr: hf_problem, u, uf, stream=None) -> None:
+    """Stage 1: every a-line extrapolated to xi_a = -1, +1 into the face array."""
+    check(_lib.load().hf_fr_project(C.byref(pr), _ptr(u), _ptr(uf), _stream(stream)), "hf_fr_project")
+
+
+def fr_correct_device(pr: hf_problem, mesh, uf, out, ghost_lo=None, ghost_hi=None, stream=None) -> None:
+    """Stages 4+5 in place on `out` (which holds the fused kernel's result)."""
+    check(_lib.load().hf_fr_correct(C.byref(pr), C.byref(mesh), _ptr(uf),
+                                    _ptr(ghost_lo) if ghost_lo is not None else None,
+                                    _ptr(ghost_hi) if ghost_hi is not None else None, _ptr(out), _stream(stream)),
+          "hf_fr_correct")
+
+
+def fr_residual_device(pr: hf_problem, dims, u, uf, out, stream=None) -> None:
+    """The FR right-hand side (stages 1-6) on the periodic dims mesh, one device."""
+    d3 = (C.c_int * 3)(*(list(dims) + [1] * (3 - len(dims))))
+    check(_lib.load().hf_fr_residual(C.byref(pr), d3, _ptr(u), _ptr(uf), _ptr(out), _stream(stream)),
+          "hf_fr_residual")
+
+
 def fused_divergence_variant(pr: hf_problem, method: Method, variant: int, u, out, stream=None) -> None:
     """Tuning hook: launch a specific method/variant, bypassing the selection table."""
     check(_lib.load().hf_fused_divergence_variant(C.byref(pr), int(method), int(variant), _ptr(u), _ptr(out),

@@ -93,3 +93,104 @@ def partitioned_divergence(U: "H.StateField", params: "H.PhysParams", jac=(1.0, 
     if full is None:
         return None
     return H.StateField(U.d, U.p, U.n_elem, U.group, U.precision, full)
+
+
+# ------------------------------------------------------------------------------------------------
+# The FR right-hand side on a layer-partitioned periodic mesh: the
+# first place the path has a real exchange step.  Stage 4 (the common interface
+# flux) reads the neighbouring element's face values, so a rank that owns a slab
+# of whole element layers needs the faces of the layer just below and just above
+# it -- the ghost layers.  They travel as point-to-point NCCL messages (NVLink /
+# NVSwitch on one node; gloo on CPU in the tests), overlapped with the fused
+# divergence kernel, which needs no halo.
+# ------------------------------------------------------------------------------------------------
+@dataclass
+class FrSlab:
+    rank: int
+    world: int
+    d: int
+    dims: tuple
+    layer: int           # elements per layer
+    l_begin: int         # first layer of the slab
+    l_end: int
+    e_begin: int
+    n_elem: int
+    problem: object      # hf_problem of the slab (the global problem's d, p, group, params)
+    face_layer_words: int  # face words of one layer
+
+    @property
+    def n_layers(self) -> int:
+        return self.l_end - self.l_begin
+
+
+def make_fr_slab(pr, dims, world: int, rank: int) -> FrSlab:
+    """Rank `rank`'s contiguous run of whole element layers (the last mesh axis).
+    Layers must be whole AoSoA groups (layer % group == 0) and every rank needs at
+    least one layer."""
+    d = pr.d
+    dims = tuple(int(x) for x in dims[:d])
+    layer = dims[0] * dims[1] if d == 3 else dims[0]
+    n_layers = dims[-1]
+    if layer % pr.group:
+        raise H.HexfuseInvalid("FrSlab: an element layer must be a whole number of AoSoA groups")
+    if world > n_layers:
+        raise H.HexfuseInvalid("FrSlab: more ranks than element layers")
+    l0 = (n_layers * rank) // world
+    l1 = (n_layers * (rank + 1)) // world
+    sp = H.make_problem(d, pr.p, (l1 - l0) * layer, pr.group, pr.precision,
+                        H.PhysParams(pr.nu, pr.zeta, pr.T), tuple(pr.jac), bool(pr.with_source))
+    one = H.make_problem(d, pr.p, layer, pr.group, pr.precision, H.PhysParams(pr.nu, pr.zeta, pr.T))
+    return FrSlab(rank, world, d, dims, layer, l0, l1, l0 * layer, (l1 - l0) * layer, sp, H.face_words(one))
+
+
+def exchange_ghost_layers(sl: FrSlab, uf, ghost_lo, ghost_hi, dist=None):
+    """Send this slab's first face layer to rank-1 (its ghost_hi) and its last to
+    rank+1 (its ghost_lo); receive ours.  Periodic ring; non-blocking (returns the
+    request list).  uf / ghost_* are 1-D tensors (CUDA for NCCL, CPU for gloo)."""
+    if dist is None:
+        import torch.distributed as dist
+    w = sl.face_layer_words
+    lo_rank, hi_rank = (sl.rank - 1) % sl.world, (sl.rank + 1) % sl.world
+    first = uf[:w].contiguous()
+    last = uf[(sl.n_layers - 1) * w: sl.n_layers * w].contiguous()
+    # Message order = matching order per peer (NCCL has no tags): with two ranks both
+    # neighbours are the same peer, whose first layer is our ghost_hi and last our ghost_lo,
+    # so every rank posts "first layer -> ghost_hi" before "last layer -> ghost_lo".
+    ops = [dist.P2POp(dist.isend, first, lo_rank, tag=0), dist.P2POp(dist.isend, last, hi_rank, tag=1),
+           dist.P2POp(dist.irecv, ghost_hi, hi_rank, tag=0), dist.P2POp(dist.irecv, ghost_lo, lo_rank, tag=1)]
+    return dist.batch_isend_irecv(ops)
+
+
+class FrOps:
+    """The per-rank kernels of the FR right-hand side: the B200 library by default.
+    Tests substitute CPU stand-ins (oracle) to exercise the partition and halo logic."""
+
+    @staticmethod
+    def divergence(sp, u, out):
+        H.fused_divergence_device(sp, u, out)
+
+    @staticmethod
+    def project(sp, u, uf):
+        H.fr_project_device(sp, u, uf)
+
+    @staticmethod
+    def correct(sp, mesh, uf, out, ghost_lo, ghost_hi):
+        H.fr_correct_device(sp, mesh, uf, out, ghost_lo, ghost_hi)
+
+
+def fr_residual_slab(sl: FrSlab, u, out, uf, ghost_lo, ghost_hi, dist=None, ops=FrOps):
+    """Stages 1-6 on one rank's slab: project the faces, start the ghost-layer
+    exchange, run the fused divergence while it is in flight, then the interface
+    corrections.  With world == 1 the mesh wraps onto itself and no message is sent."""
+    ops.project(sl.problem, u, uf)
+    reqs = []
+    if sl.world > 1:
+        if hasattr(u, "is_cuda") and u.is_cuda:
+            import torch
+            torch.cuda.current_stream().synchronize()  # faces complete before NCCL reads them
+        reqs = exchange_ghost_layers(sl, uf, ghost_lo, ghost_hi, dist)
+    ops.divergence(sl.problem, u, out)
+    for r in reqs:
+        r.wait()
+    mesh = H.make_mesh(sl.dims, sl.d, sl.e_begin, sl.n_elem, sl.layer if sl.world > 1 else 0)
+    ops.correct(sl.problem, mesh, uf, out, ghost_lo if sl.world > 1 else None, ghost_hi if sl.world > 1 else None)

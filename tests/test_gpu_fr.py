@@ -1,0 +1,139 @@
+"""GPU parity of the FR stages around the fused kernel (PAPER.md
+Table 1 stages 1, 4, 5): hf_fr_project / hf_fr_correct / hf_fr_residual vs the
+CPU oracle's restatement (oracle/hexfuse_oracle.c: hfo_project_faces,
+hfo_fr_correct, hfo_fr_residual), whose pieces are pinned to the reference
+(element divergence, wave speed vs the reference's eigenvalues) and checked by
+known answers (constant state, conservation, vanishing corrections for smooth
+fields) in tests/test_oracle.py.  1e-12 FP64 / 1e-5 FP32."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from gpu_util import PAR
+
+pytestmark = pytest.mark.gpu
+
+
+def _t(x, fp32):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(torch.float32 if fp32 else torch.float64).cuda()
+
+
+def _pr(d, p, n, g, fp32, params=PAR, jac=(1.0, 1.0, 1.0), src=False):
+    import paper_2107_14027_b200 as hf
+    from paper_2107_14027_b200 import Precision
+    return hf.make_problem(d, p, n, g, Precision.fp32 if fp32 else Precision.fp64, params, jac, src)
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+@pytest.mark.parametrize("d,p", [(3, 1), (3, 3), (3, 5), (3, 7), (2, 2), (2, 8)])
+def test_project_faces(cuda, d, p, fp32):
+    import paper_2107_14027_b200 as hf
+    for n, g in [(37, 4), (20, 1), (33, 3)]:
+        U = O.random_field(d, p, n, g, fp32, 50 + n)
+        pr = _pr(d, p, n, g, fp32)
+        uf = torch.full((hf.face_words(pr),), 7.25, dtype=torch.float32 if fp32 else torch.float64, device="cuda")
+        hf.fr_project_device(pr, _t(U, fp32), uf)
+        torch.cuda.synchronize()
+        ref = O.project_faces(d, p, n, g, U)
+        real = ref != 0.0
+        got = uf.double().cpu().numpy()
+        scale = max(1.0, np.max(np.abs(ref)))
+        assert np.max(np.abs(got[real] - ref[real])) / scale <= (1e-6 if fp32 else 1e-13)
+
+
+MESHES = [(3, (3, 4, 2), 4), (3, (2, 2, 5), 2), (2, (5, 3), 3), (2, (4, 4), 8)]
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 6])
+@pytest.mark.parametrize("d,dims,g", MESHES)
+def test_fr_residual_random(cuda, d, dims, g, p, fp32):
+    import paper_2107_14027_b200 as hf
+    n = int(np.prod(dims))
+    jac = (1.0, 2.0, 0.5)
+    for t, src in enumerate([False, True]):
+        U = O.random_field(d, p, n, g, fp32, 600 + p + t)
+        pr = _pr(d, p, n, g, fp32, jac=jac, src=src)
+        dt = torch.float32 if fp32 else torch.float64
+        out = torch.zeros(hf.field_words(pr), dtype=dt, device="cuda")
+        uf = torch.zeros(hf.face_words(pr), dtype=dt, device="cuda")
+        hf.fr_residual_device(pr, dims, _t(U, fp32), uf, out)
+        torch.cuda.synchronize()
+        ref = O.fr_residual(d, p, dims, g, U, PAR.nu, PAR.zeta, PAR.T, jac, src)
+        err = O.field_rel_error(d, p, n, g, out.double().cpu().numpy(), ref)
+        assert err <= (1e-5 if fp32 else 1e-12), (d, dims, p, fp32, src, err)
+
+
+def test_fr_tgv_periodic_box(cuda):
+    """The vortex on the periodic [0, 2 pi]^3 box of 4 x 4 x 4 elements, p = 5 FP64."""
+    import paper_2107_14027_b200 as hf
+    d, p, g, n = 3, 5, 4, 64
+    width = 2.0 * np.pi / 4
+    jac = (2.0 / width,) * 3
+    U = O.tgv_field(p, n, g, False, width=width)
+    pr = _pr(d, p, n, g, False, jac=jac)
+    out = torch.zeros(hf.field_words(pr), dtype=torch.float64, device="cuda")
+    uf = torch.zeros(hf.face_words(pr), dtype=torch.float64, device="cuda")
+    hf.fr_residual_device(pr, (4, 4, 4), _t(U, False), uf, out)
+    torch.cuda.synchronize()
+    ref = O.fr_residual(d, p, (4, 4, 4), g, U, PAR.nu, PAR.zeta, PAR.T, jac, False)
+    assert O.field_rel_error(d, p, n, g, out.double().cpu().numpy(), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("parts", [2, 3])
+@pytest.mark.parametrize("d,dims,g", [(3, (4, 2, 6), 4), (2, (8, 6), 4)])
+def test_fr_layer_partitions_with_ghosts(cuda, d, dims, g, parts):
+    """Whole-layer partitions, each corrected with ghost face layers cut from the
+    neighbours' face arrays (what the NCCL exchange of multi_gpu.FrSlab delivers),
+    reproduce the single-partition residual."""
+    import paper_2107_14027_b200 as hf
+    p, fp32 = 3, False
+    n = int(np.prod(dims))
+    layer = dims[0] * dims[1] if d == 3 else dims[0]
+    n_layers = n // layer
+    U = O.random_field(d, p, n, g, fp32, 17)
+    ref = O.fr_residual(d, p, dims, g, U, PAR.nu, PAR.zeta, PAR.T, (1.0, 1.0, 1.0), True)
+    pr_all = _pr(d, p, n, g, fp32, src=True)
+    gw = hf.field_words(pr_all) // (n // g)  # words per group
+    fw = hf.face_words(pr_all) // (n // g)
+    uf_all = torch.zeros(hf.face_words(pr_all), dtype=torch.float64, device="cuda")
+    hf.fr_project_device(pr_all, _t(U, fp32), uf_all)
+    got = np.zeros_like(U)
+    bounds = np.linspace(0, n_layers, parts + 1).astype(int)
+    for r in range(parts):
+        l0, l1 = bounds[r], bounds[r + 1]
+        e0, ne = l0 * layer, (l1 - l0) * layer
+        pr = _pr(d, p, ne, g, fp32, src=True)
+        u = _t(U[e0 // g * gw:(e0 + ne) // g * gw], fp32)
+        out = torch.zeros(hf.field_words(pr), dtype=torch.float64, device="cuda")
+        uf = torch.zeros(hf.face_words(pr), dtype=torch.float64, device="cuda")
+        hf.fused_divergence_device(pr, u, out)
+        hf.fr_project_device(pr, u, uf)
+        lo = ((l0 - 1) % n_layers) * layer
+        hi = (l1 % n_layers) * layer
+        ghost_lo = uf_all[lo // g * fw:(lo + layer) // g * fw].clone()
+        ghost_hi = uf_all[hi // g * fw:(hi + layer) // g * fw].clone()
+        ms = hf.make_mesh(dims, d, e0, ne, layer)
+        hf.fr_correct_device(pr, ms, uf, out, ghost_lo, ghost_hi)
+        torch.cuda.synchronize()
+        got[e0 // g * gw:(e0 + ne) // g * gw] = out.cpu().numpy()
+    assert O.field_rel_error(d, p, n, g, got, ref) <= 1e-12
+
+
+def test_fr_slab_driver_single_rank(cuda):
+    """multi_gpu.fr_residual_slab with world = 1 (the mesh wraps onto itself, no message)."""
+    import paper_2107_14027_b200 as hf
+    from paper_2107_14027_b200.multi_gpu import fr_residual_slab, make_fr_slab
+    d, p, dims, g = 3, 4, (2, 4, 3), 4
+    n = int(np.prod(dims))
+    U = O.random_field(d, p, n, g, False, 5)
+    pr = _pr(d, p, n, g, False, src=True)
+    sl = make_fr_slab(pr, dims, 1, 0)
+    u = _t(U, False)
+    out = torch.zeros_like(u)
+    uf = torch.zeros(hf.face_words(pr), dtype=torch.float64, device="cuda")
+    fr_residual_slab(sl, u, out, uf, None, None)
+    torch.cuda.synchronize()
+    ref = O.fr_residual(d, p, dims, g, U, PAR.nu, PAR.zeta, PAR.T, (1.0, 1.0, 1.0), True)
+    assert O.field_rel_error(d, p, n, g, out.cpu().numpy(), ref) <= 1e-12

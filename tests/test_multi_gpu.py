@@ -88,3 +88,89 @@ def test_slices_tile_the_field():
         assert max(s.word_end for s in sls) == hf.field_words(pr)
         sizes = [s.n_elem for s in sls if s.n_elem]
         assert max(sizes) - min(sizes) <= g  # balanced to within one group
+
+
+# ---------------------------------------------------------------- FR right-hand side: layer slabs + ghost exchange
+def _fr_worker(rank, world, port, cases, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    import paper_2107_14027_b200 as hf
+    from paper_2107_14027_b200 import PhysParams, Precision
+    from paper_2107_14027_b200.multi_gpu import fr_residual_slab, make_fr_slab
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    par = PhysParams(1.0 / 1600.0, 2.5, 1.0)
+    ok = []
+    for (d, p, dims, g, src) in cases:
+        n = int(np.prod(dims))
+        U = O.random_field(d, p, n, g, False, 31 + n)
+        pr = hf.make_problem(d, p, n, g, Precision.fp64, par, with_source=src)
+        sl = make_fr_slab(pr, dims, world, rank)
+        gw = hf.field_words(pr) // (n // g)
+        fw = hf.face_words(pr) // (n // g)
+        e0, e1 = sl.e_begin, sl.e_begin + sl.n_elem
+        jac = (1.0, 1.0, 1.0)
+
+        class CpuOps:  # oracle stand-ins for the three device kernels (test infrastructure)
+            @staticmethod
+            def divergence(sp, u, out):
+                out[:] = torch.from_numpy(O.oracle_divergence(d, p, sp.n_elem, g, u.numpy(), par.nu, par.zeta, par.T,
+                                                              jac, src))
+
+            @staticmethod
+            def project(sp, u, uf):
+                uf[:] = torch.from_numpy(O.project_faces(d, p, sp.n_elem, g, u.numpy()))
+
+            @staticmethod
+            def correct(sp, mesh, uf, out, glo, ghi):
+                Ufg = np.zeros(hf.face_words(pr))
+                Ufg[e0 // g * fw:e1 // g * fw] = uf.numpy()
+                if glo is not None:
+                    lo = (e0 - sl.layer) % n
+                    hi = e1 % n
+                    Ufg[lo // g * fw:(lo + sl.layer) // g * fw] = glo.numpy()
+                    Ufg[hi // g * fw:(hi + sl.layer) // g * fw] = ghi.numpy()
+                outg = np.zeros(hf.field_words(pr))
+                outg[e0 // g * gw:e1 // g * gw] = out.numpy()
+                O.fr_correct(d, p, g, dims, Ufg, outg, par.nu, par.zeta, par.T, jac, e0, e1)
+                out[:] = torch.from_numpy(outg[e0 // g * gw:e1 // g * gw])
+
+        u = torch.from_numpy(U[e0 // g * gw:e1 // g * gw].copy())
+        out = torch.zeros_like(u)
+        uf = torch.zeros(hf.face_words(sl.problem), dtype=torch.float64)
+        glo = torch.zeros(sl.face_layer_words, dtype=torch.float64)
+        ghi = torch.zeros(sl.face_layer_words, dtype=torch.float64)
+        fr_residual_slab(sl, u, out, uf, glo, ghi, dist=dist, ops=CpuOps)
+        parts = [None] * world
+        dist.all_gather_object(parts, (e0, e1, out.numpy()))
+        if rank == 0:
+            full = np.zeros(hf.field_words(pr))
+            for a, b, arr in parts:
+                full[a // g * gw:b // g * gw] = arr
+            ref = O.fr_residual(d, p, dims, g, U, par.nu, par.zeta, par.T, jac, src)
+            ok.append(float(np.max(np.abs(full - ref))))
+    dist.barrier()
+    dist.destroy_process_group()
+    q.put((rank, ok))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fr_slabs_with_ghost_exchange_gloo(world):
+    cases = [(3, 2, (2, 2, 6), 4, True), (3, 3, (3, 2, 3), 2, False), (2, 4, (4, 6), 4, True)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fr_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for pr_ in procs:
+        pr_.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for pr_ in procs:
+        pr_.join(timeout=60)
+    assert len(res[0]) == len(cases) and max(res[0]) == 0.0, res
