@@ -170,39 +170,42 @@ struct FrCorrShape {
     static constexpr size_t SMEM = size_t(TASKS) * 2 * NV * sizeof(R);  // jumps [v][s][a][l][el]
 };
 
-template <class R, int DIM>
-__device__ __forceinline__ void fr_flux_normal(const R (&U)[n_vars_c(DIM)], int a, const Params<R>& p,
-                                               R (&F)[n_vars_c(DIM)]) {
-    constexpr int NV = n_vars_c(DIM);
-#pragma unroll
-    for (int v = 0; v < NV; ++v) F[v] = R(0);
-    R Va = U[1];
-#pragma unroll
-    for (int b = 1; b < DIM; ++b)
-        if (a == b) Va = U[1 + b];
-    F[0] = p.zeta * Va;
-#pragma unroll
-    for (int b = 0; b < DIM; ++b) {
-        R g = R(0);
-#pragma unroll
-        for (int c = 0; c < DIM; ++c)
-            if (c == a) g = U[var_grad_c(DIM, b, c)];
-        R mom = U[1 + b] * Va - p.nu * g;  // equations.hpp:70-83
-        if (a == b) mom += U[0];
-        F[1 + b] = mom;
-#pragma unroll
-        for (int c = 0; c < DIM; ++c)
-            if (c == a) F[var_grad_c(DIM, b, c)] = -U[1 + b] * p.invT;
+// Row V of the normal flux F_A (equations.hpp:70-83): zeta V_A on P,
+// V_b V_A - nu g(b,A) (+P if b == A) on momentum b, -V_b/T on g(b,A), 0 elsewhere.
+template <class R, int DIM, int A, int V>
+__device__ __forceinline__ R fr_flux_row(const R (&U)[n_vars_c(DIM)], const Params<R>& p) {
+    if constexpr (V == 0) {
+        return p.zeta * U[1 + A];
+    } else if constexpr (V <= DIM) {
+        constexpr int b = V - 1;
+        const R mom = U[1 + b] * U[1 + A] - p.nu * U[var_grad_c(DIM, b, A)];
+        return (b == A) ? mom + U[0] : mom;
+    } else {
+        constexpr int b = (V - 1 - DIM) / DIM, c = (V - 1 - DIM) % DIM;
+        if constexpr (c == A) return -U[1 + b] * p.invT;
+        else return R(0);
     }
 }
 
-template <class R, int DIM>
-__device__ __forceinline__ R fr_wavespeed(const R (&U)[n_vars_c(DIM)], int a, const Params<R>& p) {
-    R Va = U[1];
-#pragma unroll
-    for (int b = 1; b < DIM; ++b)
-        if (a == b) Va = U[1 + b];
+template <class R, int DIM, int A>
+__device__ __forceinline__ R fr_wavespeed(const R (&U)[n_vars_c(DIM)], const Params<R>& p) {
+    const R Va = U[1 + A];
     return fabs(Va) + sqrt(Va * Va + p.zeta + p.nu * p.invT);
+}
+
+// Jumps F^I - F_A(U_own) at both ends of one A-line, into the shared jump array.
+template <class R, int DIM, int M, int NE, int A, int V = 0>
+__device__ __forceinline__ void fr_jump_rows(const R (&Uo)[n_vars_c(DIM)], const R (&Un)[n_vars_c(DIM)], R lam,
+                                             int s, const Params<R>& p, R* __restrict__ jrow) {
+    if constexpr (V < n_vars_c(DIM)) {
+        constexpr int LN = fr_lines<DIM, M>();
+        const R fo = fr_flux_row<R, DIM, A, V>(Uo, p), fn = fr_flux_row<R, DIM, A, V>(Un, p);
+        // U_L / U_R in the +x_A orientation of the face: own state is U_L on the +A face (s = 1)
+        const R du = s ? (Un[V] - Uo[V]) : (Uo[V] - Un[V]);
+        const R FI = R(0.5) * (fo + fn) - R(0.5) * lam * du;
+        jrow[NE * LN * DIM * 2 * V] = FI - fo;
+        fr_jump_rows<R, DIM, M, NE, A, V + 1>(Uo, Un, lam, s, p, jrow);
+    }
 }
 
 template <class R, int DIM, int M, int NE>
@@ -217,43 +220,36 @@ __global__ void __launch_bounds__(FrCorrShape<R, DIM, M, NE>::BS)
     const long long E0 = static_cast<long long>(blockIdx.x) * NE;
     const long long n_mesh = (long long)f.mesh.dims[0] * f.mesh.dims[1] * (DIM == 3 ? f.mesh.dims[2] : 1);
 
-    // ---- stage 4: common fluxes and jumps at both ends of every line
-    for (int task = tid; task < S::TASKS; task += BS) {
-        const int el = task % NE;
-        const int l = (task / NE) % LN;
-        const int a = task / (NE * LN);
-        const long long e = E0 + el;  // local element
-        if (e >= p.n_elem) continue;
-        const long long eg = f.mesh.e_begin + e;
-        int c[3] = {int(eg % f.mesh.dims[0]), int((eg / f.mesh.dims[0]) % f.mesh.dims[1]),
-                    DIM == 3 ? int(eg / ((long long)f.mesh.dims[0] * f.mesh.dims[1])) : 0};
-        for (int s = 0; s < 2; ++s) {
-            // side s = 1: this element's +a face vs the +a neighbour's -1 side; s = 0: the -a face
-            int cn[3] = {c[0], c[1], c[2]};
-            cn[a] = (cn[a] + (s ? 1 : -1) + f.mesh.dims[a]) % f.mesh.dims[a];
-            const long long en = cn[0] + (long long)f.mesh.dims[0] * (cn[1] + (long long)f.mesh.dims[1] * cn[2]);
+    // ---- stage 4: common fluxes and jumps at both ends of every line (axis unrolled)
+    auto stage4 = [&](auto a_tag) {
+        constexpr int A = decltype(a_tag)::value;
+        for (int task = tid; task < NE * LN * 2; task += BS) {
+            const int el = task % NE;
+            const int l = (task / NE) % LN;
+            const int s = task / (NE * LN);
+            const long long e = E0 + el;  // local element
+            if (e >= p.n_elem) continue;
+            const long long eg = f.mesh.e_begin + e;
+            int c[3] = {int(eg % f.mesh.dims[0]), int((eg / f.mesh.dims[0]) % f.mesh.dims[1]),
+                        DIM == 3 ? int(eg / ((long long)f.mesh.dims[0] * f.mesh.dims[1])) : 0};
+            // side s = 1: this element's +A face vs the +A neighbour's -1 side; s = 0: the -A face
+            c[A] = (c[A] + (s ? 1 : -1) + f.mesh.dims[A]) % f.mesh.dims[A];
+            const long long en = c[0] + (long long)f.mesh.dims[0] * (c[1] + (long long)f.mesh.dims[1] * c[2]);
             long long enl;
             const R* nb = fr_faces_of(f, en, n_mesh, &enl);
             R Uo[NV], Un[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
-                Uo[v] = f.uf[face_word(DIM, M, p.group, e, a, s, l, v)];
-                Un[v] = nb[face_word(DIM, M, p.group, enl, a, 1 - s, l, v)];
+                Uo[v] = f.uf[face_word(DIM, M, p.group, e, A, s, l, v)];
+                Un[v] = nb[face_word(DIM, M, p.group, enl, A, 1 - s, l, v)];
             }
-            R Fo[NV], Fn[NV];
-            fr_flux_normal<R, DIM>(Uo, a, p, Fo);
-            fr_flux_normal<R, DIM>(Un, a, p, Fn);
-            const R lam = fmax(fr_wavespeed<R, DIM>(Uo, a, p), fr_wavespeed<R, DIM>(Un, a, p));
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                // UL / UR in the +x_a orientation of the face
-                const R ul = s ? Uo[v] : Un[v], ur = s ? Un[v] : Uo[v];
-                const R fl = s ? Fo[v] : Fn[v], fr = s ? Fn[v] : Fo[v];
-                const R FI = R(0.5) * (fl + fr) - R(0.5) * lam * (ur - ul);
-                jump[jidx(el, a, s, l, v)] = FI - Fo[v];
-            }
+            const R lam = fmax(fr_wavespeed<R, DIM, A>(Uo, p), fr_wavespeed<R, DIM, A>(Un, p));
+            fr_jump_rows<R, DIM, M, NE, A>(Uo, Un, lam, s, p, jump + jidx(el, A, s, l, 0));
         }
-    }
+    };
+    stage4(std::integral_constant<int, 0>{});
+    stage4(std::integral_constant<int, 1>{});
+    if constexpr (DIM == 3) stage4(std::integral_constant<int, 2>{});
     __syncthreads();
 
     // ---- stage 5: corrections at every solution point, over the fused kernel's result
@@ -289,7 +285,7 @@ namespace hfb {
 
 template <class R, int DIM, int M>
 constexpr int fr_proj_ne() {
-    int ne = 32;  // <= 72 KB of staged chunk, a multiple of the row alignment not required (any NE)
+    int ne = 32;  // power of two, <= 72 KB of staged chunk
     while (ne > 1 && (size_t(ne) * ipow_c(M, DIM) * n_vars_c(DIM) * sizeof(R) > size_t(72 * 1024) ||
                       ne * ipow_c(M, DIM - 1) > 512))
         ne /= 2;
@@ -303,28 +299,40 @@ constexpr int fr_corr_ne() {
     return ne;
 }
 
+template <class R, int DIM, int M, int NE>
+int fr_project_launch(const Params<R>& prm, const FrParams<R>& fp, R* uf, cudaStream_t st) {
+    using S = FrProjShape<R, DIM, M, NE>;
+    auto kernel = hf_fr_project_kernel<R, DIM, M, NE>;
+    Params<R> p = prm;
+    p.fast_ok = (p.group == NE || (p.group % NE == 0 && (NE * sizeof(R)) % 16 == 0 &&
+                                   ((long long)p.group * sizeof(R)) % 16 == 0)) &&
+                (reinterpret_cast<uintptr_t>(p.u) & 15u) == 0;
+    if (S::SMEM > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM));
+        if (e != cudaSuccess) return int(e);
+    }
+    kernel<<<unsigned((p.n_elem + NE - 1) / NE), S::BS, S::SMEM, st>>>(p, fp, uf);
+    return int(cudaGetLastError());
+}
+
+// Stage 1 stages whole chunks with bulk copies when the chunk is the AoSoA group
+// (or whole 16-byte rows of it): the chunk size follows the caller's group.
+template <class R, int DIM, int M, int NE = fr_proj_ne<R, DIM, M>()>
+int fr_project_dispatch(const Params<R>& prm, const FrParams<R>& fp, R* uf, cudaStream_t st) {
+    if constexpr (NE > 1) {
+        if (prm.group != NE && prm.group % NE != 0) return fr_project_dispatch<R, DIM, M, NE / 2>(prm, fp, uf, st);
+    }
+    return fr_project_launch<R, DIM, M, NE>(prm, fp, uf, st);
+}
+
 template <class R, int DIM, int M>
 int fr_stage(int which, const Params<R>& prm, const FrParams<R>& fp, R* uf, cudaStream_t st) {
     if (prm.n_elem == 0) return 0;
-    if (which == 1) {
-        constexpr int NE = fr_proj_ne<R, DIM, M>();
-        using S = FrProjShape<R, DIM, M, NE>;
-        auto kernel = hf_fr_project_kernel<R, DIM, M, NE>;
-        Params<R> p = prm;
-        p.fast_ok = (p.group == NE || (p.group % NE == 0 && (NE * sizeof(R)) % 16 == 0 &&
-                                       ((long long)p.group * sizeof(R)) % 16 == 0)) &&
-                    (reinterpret_cast<uintptr_t>(p.u) & 15u) == 0;
-        if (S::SMEM > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM));
-            if (e != cudaSuccess) return int(e);
-        }
-        kernel<<<unsigned((p.n_elem + NE - 1) / NE), S::BS, S::SMEM, st>>>(p, fp, uf);
-    } else {
-        constexpr int NE = fr_corr_ne<R, DIM, M>();
-        using S = FrCorrShape<R, DIM, M, NE>;
-        auto kernel = hf_fr_correct_kernel<R, DIM, M, NE>;
-        kernel<<<unsigned((prm.n_elem + NE - 1) / NE), S::BS, S::SMEM, st>>>(prm, fp);
-    }
+    if (which == 1) return fr_project_dispatch<R, DIM, M>(prm, fp, uf, st);
+    constexpr int NE = fr_corr_ne<R, DIM, M>();
+    using S = FrCorrShape<R, DIM, M, NE>;
+    auto kernel = hf_fr_correct_kernel<R, DIM, M, NE>;
+    kernel<<<unsigned((prm.n_elem + NE - 1) / NE), S::BS, S::SMEM, st>>>(prm, fp);
     return int(cudaGetLastError());
 }
 

@@ -340,6 +340,10 @@ constexpr int mapped_ne() {
                       size_t(100 * 1024) ||
                       ne * ipow_c(M, DIM - 1) > 512))
         ne /= 2;
+    // NE*m a multiple of the bank period puts every x-line of a warp in a few bank
+    // classes (e.g. p3 FP64, NE 4: 4 of 16); one element less spreads them
+    const int bank_words = sizeof(R) == 4 ? 32 : 16;
+    if (ne > 1 && (ne * M) % bank_words == 0) ne -= 1;
     return ne;
 }
 

@@ -43,7 +43,7 @@ struct MappedShape {
     static constexpr int HDR = 128;
     static constexpr size_t ACC_OFF = HDR + size_t(L::BUF_BYTES);
     static constexpr size_t MET_OFF = ACC_OFF + size_t(NV) * NP * NE * sizeof(R);
-    static constexpr size_t GEO_OFF = MET_OFF + size_t(NMET) * NP * NE * sizeof(R);
+    static constexpr size_t GEO_OFF = ((MET_OFF + size_t(NMET) * NP * NE * sizeof(R) + 15) / 16) * 16;
     static constexpr size_t SMEM = GEO_OFF + size_t(NC) * DIM * NE * sizeof(R);
 };
 
@@ -173,14 +173,26 @@ __global__ void __launch_bounds__(MappedShape<R, DIM, M, NE>::BS)
     const int head = fast ? IO::head_bytes(p.u + gbase, contiguous) : 0;
 
     // ---------------- stage the chunk and its corners ----------------
+    // With group == NE the chunk's corners are one contiguous, 16-byte-multiple
+    // range (2^d d words per element): a second bulk copy on its own mbarrier,
+    // so the metric pass starts while the field chunk is still in flight.
+    constexpr int GEO_WORDS = NC * DIM * NE;
+    const bool geo_bulk = fast && contiguous && (reinterpret_cast<uintptr_t>(p.geo) & 15u) == 0;
     if (fast) {
         if (tid == 0) {
             mbar_init(bar, 1);
+            mbar_init(bar + 1, 1);
             fence_mbar_init();
         }
         __syncthreads();
         if (tid < 32) {
-            if (tid == 0) mbar_arrive_expect_tx(bar, IO::tx_bytes(p.u + gbase, contiguous));
+            if (tid == 0) {
+                mbar_arrive_expect_tx(bar, IO::tx_bytes(p.u + gbase, contiguous));
+                if (geo_bulk) {
+                    mbar_arrive_expect_tx(bar + 1, uint32_t(GEO_WORDS * sizeof(R)));
+                    bulk_g2s(geo, p.geo + E0 * NC * DIM, GEO_WORDS * sizeof(R), bar + 1);
+                }
+            }
             __syncwarp();
             IO::load(buf, p.u + gbase, p.group, contiguous, bar, tid);
         }
@@ -196,18 +208,22 @@ __global__ void __launch_bounds__(MappedShape<R, DIM, M, NE>::BS)
             s0[idx] = v;
         }
     }
-    for (int idx = tid; idx < NC * DIM * NE; idx += BS) {
-        const int el = idx % NE;
-        const int cx = idx / NE;  // x + DIM * c
-        const long long e = E0 + el;
-        R v = R(0);
-        if (e < p.n_elem) {
-            const long long ge = e / p.group;
-            v = p.geo[ge * p.group * NC * DIM + (e - ge * p.group) + static_cast<long long>(p.group) * cx];
+    if (!geo_bulk) {
+        for (int idx = tid; idx < GEO_WORDS; idx += BS) {
+            const int el = idx % NE;
+            const int cx = idx / NE;  // x + DIM * c
+            const long long e = E0 + el;
+            R v = R(0);
+            if (e < p.n_elem) {
+                const long long ge = e / p.group;
+                v = p.geo[ge * p.group * NC * DIM + (e - ge * p.group) + static_cast<long long>(p.group) * cx];
+            }
+            geo[idx] = v;
         }
-        geo[idx] = v;
+        __syncthreads();
+    } else {
+        mbar_wait_parity(bar + 1, 0);
     }
-    __syncthreads();
 
     // ---------------- metric pass: S = adj(J), 1/|J| at every point ----------------
     for (int idx = tid; idx < NE * NP; idx += BS) {
