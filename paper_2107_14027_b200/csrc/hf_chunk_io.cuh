@@ -56,8 +56,17 @@ struct ChunkIO {
     // producer lane may refill its region as soon as its own store has read it.
     // PIECE is a multiple of the 128-byte line: when the chunk starts on a line,
     // no two bulk copies share a line or a 32-byte sector (split sectors in the
-    // bulk stores cost ~10% of HBM bandwidth, measured).
-    static constexpr int PIECE = ((BUF_BYTES / 32 + 127) / 128) * 128;
+    // bulk stores cost ~10% of HBM bandwidth, measured).  Few large copies beat
+    // many small ones: with pieces of at least 64 KB (one copy per chunk up to
+    // 64 KB) the selected kernels gained 0-6 % over 1/32-of-the-chunk pieces
+    // (p6: FP32 5.84 -> 6.20, FP64 6.09 -> 6.35 TB/s; profiles/select_r01d.jsonl
+    // vs select_r01c.jsonl) -- the bulk-copy engine's per-request cost, not the
+    // bytes, limited the small pieces.
+#ifndef HF_MIN_PIECE
+#define HF_MIN_PIECE 65536
+#endif
+    static constexpr int PIECE0 = ((BUF_BYTES / 32 + 127) / 128) * 128;
+    static constexpr int PIECE = PIECE0 > HF_MIN_PIECE ? PIECE0 : HF_MIN_PIECE;
 
     __device__ static void load(unsigned char* buf, const R* src, long long group, bool contiguous, uint64_t* bar,
                                 int lane) {
