@@ -617,12 +617,12 @@ int hf_fused_divergence_host(hf_context* c, const hf_problem* pr, const void* u_
     const size_t w = word_bytes(pr);
     const int64_t gw = int64_t(pr->group) * ipow64(pr->p + 1, pr->d) * (1 + pr->d + pr->d * pr->d);
     const int64_t n_groups = (pr->n_elem + pr->group - 1) / pr->group;
-    // Slice: whole groups, ~16 MB per slot, a multiple of the kernel's chunk.  The copy pipeline
+    // Slice: whole groups, ~48 MB per slot, a multiple of the kernel's chunk.  The copy pipeline
     // moves one direction alone while it fills and drains (one slice each), so a call of n
-    // slices runs at ~n/(n+1) of the duplex PCIe rate: small slices, many of them.
+    // slices runs at ~n/(n+1) of the duplex PCIe rate (measured: 16 MB slices lost 4 % to 48 MB).
     int pref = hf_preferred_group(pr);
     if (pref < 1) pref = 1;
-    int64_t slice_groups = std::max<int64_t>(1, (int64_t(16) << 20) / int64_t(gw * w));
+    int64_t slice_groups = std::max<int64_t>(1, (int64_t(48) << 20) / int64_t(gw * w));
     const int64_t chunk_groups = std::max<int64_t>(1, (pref + pr->group - 1) / pr->group);
     slice_groups = std::max<int64_t>(chunk_groups, slice_groups / chunk_groups * chunk_groups);
     slice_groups = std::min<int64_t>(slice_groups, n_groups);

@@ -150,6 +150,13 @@ def main():
         write_table(rows, args.points)
 
 
+# Measured exceptions to "fastest median wins" (tools/probe_p6.py): the one-chunk-per-CTA
+# p6 FP32 kernel with NE = 2 (chunk bytes not a multiple of 16, so two copies of the sweep
+# code alternate by chunk alignment) ran at 158 us in one context and 200 us in another on
+# the same box; the ring kernel is stable at 164 us.
+OVERRIDES = {(3, 6, "fp32"): 3}
+
+
 def write_table(rows, points, raw="profiles/select_r01_*.jsonl"):
     best = {}
     for r in rows:
@@ -158,6 +165,10 @@ def write_table(rows, points, raw="profiles/select_r01_*.jsonl"):
         key = (r["d"], r["p"], r["precision"])
         cur = best.get(key)
         score = r["alg_GBps"] * (1.02 if r["method"] == "lines" else 1.0)
+        if key in OVERRIDES:
+            if r["method"] == "lines" and r["variant"] == OVERRIDES[key]:
+                best[key] = (float("inf"), r)
+            continue
         if cur is None or score > cur[0]:
             best[key] = (score, r)
     path = os.path.join(ROOT, "paper_2107_14027_b200", "csrc", "hf_select_table.inc")
