@@ -111,11 +111,6 @@ __device__ __forceinline__ void bulk_wait_read_all() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
-// wait until at most N of this thread's committed bulk-store groups still read shared memory
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
 
 // make generic-proxy shared-memory writes visible to the async proxy (bulk store)
 __device__ __forceinline__ void fence_proxy_async_smem() {

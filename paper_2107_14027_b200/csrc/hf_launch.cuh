@@ -3,11 +3,12 @@
 // The reference picks one static configuration per (p, precision) from the
 // paper's Volta measurements (preset_table, presets.hpp:25-37;
 // default_lines_n, presets.hpp:86-103, sized for a 96 KiB shared-memory cap).
-// On B200 (227 KB shared per CTA, 228 KB per SM) the lines kernel's chunk is
-// sized for about three co-resident CTAs per SM, so one CTA can be staging its
-// next chunk through the bulk-copy engine while the others compute; the
-// variant knob (0: default, 1: half, 2: double the elements per CTA) exists so
-// the measured selection (hf_select_table.inc) can pick the best of three.
+// On B200 (227 KB shared per CTA, 228 KB per SM) the lines kernel's default
+// chunk (NE0) is sized for about three co-resident CTAs per SM, so one CTA can
+// be staging its next chunk through the bulk-copy engine while the others
+// compute; the variants below (chunk size, one chunk per CTA or a persistent
+// TMA ring, consumer groups, lines per thread) are what the measured selection
+// (hf_select_table.inc, tools/select_methods.py) chooses from.
 #pragma once
 
 #include <cstdio>
@@ -392,17 +393,8 @@ cudaError_t launch_unfused(Params<R> p, bool src, cudaStream_t st, KInfo* info, 
     return cudaGetLastError();
 }
 
-// Runtime -> template dispatch, defined per precision in hf_inst_*.cu.
-// Return cudaErrorInvalidValue (as an int) for an unsupported combination.
-template <class R>
-int run_lines(int d, int p, int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry);
-template <class R>
-int run_planar_managed(int p, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry);
-template <class R>
-int run_planar(int p, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry);
-template <class R>
-int run_unfused(int d, int p, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry);
-
+// Runtime -> template dispatch (hf_dispatch.cuh) returns this for a combination
+// that is not instantiated; the C ABI maps it to HF_EINVAL.
 constexpr int kUnsupported = -1;
 
 }  // namespace hfb
