@@ -261,6 +261,10 @@ __global__ void __launch_bounds__(FrCorrShape<R, DIM, M, NE>::BS)
         const int i = pt % M, j = (pt / M) % M, k = pt / (M * M);
         const long long ge = e / p.group;
         R* ob = p.out + ge * p.group_words + (e - ge * p.group);
+        // all n_v loads first (independent, in flight together), then the updates
+        R cur[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) cur[v] = ob[static_cast<long long>(p.group) * (pt + NP * v)];
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
             R corr = R(0);
@@ -270,8 +274,7 @@ __global__ void __launch_bounds__(FrCorrShape<R, DIM, M, NE>::BS)
                 const int l = a == 0 ? (j + M * k) : (a == 1 ? (i + M * k) : (i + M * j));
                 corr = fma(p.jac[a], fma(f.gl[t], jump[jidx(el, a, 0, l, v)], f.gr[t] * jump[jidx(el, a, 1, l, v)]), corr);
             }
-            R* q = ob + static_cast<long long>(p.group) * (pt + NP * v);
-            *q = *q - corr;
+            ob[static_cast<long long>(p.group) * (pt + NP * v)] = cur[v] - corr;
         }
     }
 }
