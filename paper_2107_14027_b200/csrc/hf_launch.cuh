@@ -331,14 +331,14 @@ cudaError_t launch_planar_managed(Params<R> p, cudaStream_t st, KInfo* info, boo
 }
 
 // Mapped elements: the largest power-of-two chunk (<= 64 / 128 elements) with
-// <= 100 KB of shared memory (two CTAs per SM) and <= 512 lines.
+// <= 64 KB of shared memory (three CTAs per SM) and <= 512 lines.
 template <class R, int DIM, int M>
 constexpr int mapped_ne() {
     int ne = (DIM == 2) ? 128 : 64;
     while (ne > 1 && (MappedShape<R, DIM, M, 1>::HDR + 48 + size_t(ne) * ipow_c(M, DIM) *
-                                                               (2 * n_vars_c(DIM) + DIM * DIM + 1) * sizeof(R) +
+                                                               (2 * n_vars_c(DIM)) * sizeof(R) +
                           size_t(ne) * (1 << DIM) * DIM * sizeof(R) >
-                      size_t(100 * 1024) ||
+                      size_t(64 * 1024) ||
                       ne * ipow_c(M, DIM - 1) > 512))
         ne /= 2;
     // NE*m a multiple of the bank period puts every x-line of a warp in a few bank

@@ -18,12 +18,12 @@
 //
 // One CTA per chunk of NE elements (hf_lines.cuh's staging):
 //   1. U chunk -> shared (cp.async.bulk), the chunk's corners -> shared;
-//   2. metric pass: S and 1/|J| at every point into shared ((d^2+1) words/pt);
-//   3. d sweeps, thread per a-line (bank-conflict-free LineMap order): batch 0
+//   2. d sweeps, thread per a-line (bank-conflict-free LineMap order); row a
+//      of S along the line from the corners (LineMetric: no stored metric); batch 0
 //      contracts the 1+d continuity/momentum lines, then d batches of d
 //      gradient lines S_ab V_c; partial sums of all n_v rows accumulate in a
 //      shared region (n_v words/pt);
-//   4. final pass: out = -acc/|J| (+ -g/T) written over the staged input, bulk store.
+//   3. final pass: out = -acc/|J| (+ -g/T) written over the staged input, bulk store.
 // HBM traffic stays n_v words in + n_v out per point plus 2^d d words per
 // element of geometry.
 #pragma once
@@ -38,12 +38,10 @@ struct MappedShape {
     static constexpr int NV = n_vars_c(DIM);
     static constexpr int NP = ipow_c(M, DIM);
     static constexpr int NC = 1 << DIM;  // corners
-    static constexpr int NMET = DIM * DIM + 1;
     static constexpr int BS = L::BS;
     static constexpr int HDR = 128;
     static constexpr size_t ACC_OFF = HDR + size_t(L::BUF_BYTES);
-    static constexpr size_t MET_OFF = ACC_OFF + size_t(NV) * NP * NE * sizeof(R);
-    static constexpr size_t GEO_OFF = ((MET_OFF + size_t(NMET) * NP * NE * sizeof(R) + 15) / 16) * 16;
+    static constexpr size_t GEO_OFF = ((ACC_OFF + size_t(NV) * NP * NE * sizeof(R) + 15) / 16) * 16;
     static constexpr size_t SMEM = GEO_OFF + size_t(NC) * DIM * NE * sizeof(R);
 };
 
@@ -70,6 +68,74 @@ __device__ __forceinline__ R mapped_adjugate(const R (&J)[DIM * DIM], R (&S)[DIM
     }
 }
 
+// Column j of J = dx/dxi at reference point xi, from the element's corners in
+// shared memory ([c][x][el] layout): sum_c X_c dN_c/dxi_j.
+template <class R, int DIM, int NE>
+__device__ __forceinline__ void mapped_jcol(const R* __restrict__ geo, int el, int j, const R (&xi)[3], R (&col)[DIM]) {
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) col[i] = R(0);
+#pragma unroll
+    for (int c = 0; c < (1 << DIM); ++c) {
+        R dn = R(0.5) * ((c >> j) & 1 ? R(1) : R(-1));
+#pragma unroll
+        for (int k = 0; k < DIM; ++k)
+            if (k != j) dn *= R(0.5) * (R(1) + ((c >> k) & 1 ? xi[k] : -xi[k]));
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) col[i] = fma(geo[el + NE * (i + DIM * c)], dn, col[i]);
+    }
+}
+
+// Row A of adj(J) along one A-line.  The J columns transverse to A are linear
+// in xi_A along the line (the map is (bi/tri)linear), so the thread evaluates
+// them at xi_A = 0 and 1 once (P, P + Q) and the row at line point t is a
+// cross product of P + xi_t Q terms: no per-point metric storage.
+template <class R, int DIM, int NE, int A>
+struct LineMetric {
+    R P[DIM - 1][DIM], Q[DIM - 1][DIM];
+    __device__ __forceinline__ LineMetric(const R* __restrict__ geo, int el, R (&xi)[3]) {
+#pragma unroll
+        for (int q = 0; q < DIM - 1; ++q) {
+            const int b = (A + 1 + q) % DIM;
+            R c0[DIM], c1[DIM];
+            xi[A] = R(0);
+            mapped_jcol<R, DIM, NE>(geo, el, b, xi, c0);
+            xi[A] = R(1);
+            mapped_jcol<R, DIM, NE>(geo, el, b, xi, c1);
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) {
+                P[q][i] = c0[i];
+                Q[q][i] = c1[i] - c0[i];
+            }
+        }
+    }
+    // S(A, .) at xi_A = x
+    __device__ __forceinline__ void row(R x, R (&Sa)[DIM]) const {
+        if constexpr (DIM == 3) {
+            R u[3], w[3];  // columns A+1, A+2: adj row A = col(A+1) x col(A+2)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                u[i] = fma(x, Q[0][i], P[0][i]);
+                w[i] = fma(x, Q[1][i], P[1][i]);
+            }
+            Sa[0] = u[1] * w[2] - u[2] * w[1];
+            Sa[1] = u[2] * w[0] - u[0] * w[2];
+            Sa[2] = u[0] * w[1] - u[1] * w[0];
+        } else {
+            R u[2];  // the other column
+#pragma unroll
+            for (int i = 0; i < 2; ++i) u[i] = fma(x, Q[0][i], P[0][i]);
+            // adj = [[J11, -J01], [-J10, J00]]: row 0 = (u1, -u0) with u = col 1; row 1 = (-u1, u0) with u = col 0
+            if constexpr (A == 0) {
+                Sa[0] = u[1];
+                Sa[1] = -u[0];
+            } else {
+                Sa[0] = -u[1];
+                Sa[1] = u[0];
+            }
+        }
+    }
+};
+
 // Accumulate d = D * Y (line rows of one batch) into the shared partial sums.
 template <class R, int M, int NE, int STRIDE, int NROW>
 __device__ __forceinline__ void mapped_contract(const Params<R>& p, const R (&Y)[NROW][M], R* __restrict__ acc_line,
@@ -90,7 +156,7 @@ __device__ __forceinline__ void mapped_contract(const Params<R>& p, const R (&Y)
 
 // One sweep along axis A for the line whose first point is word `o` of the chunk.
 template <class R, int DIM, int M, int NE, int A>
-__device__ __forceinline__ void mapped_sweep(const R* __restrict__ s, R* __restrict__ acc, const R* __restrict__ met,
+__device__ __forceinline__ void mapped_sweep(const R* __restrict__ s, R* __restrict__ acc, const R* __restrict__ geo,
                                              const Params<R>& p, int o) {
     constexpr int NP = ipow_c(M, DIM);
     constexpr int VS = NE * NP;  // word stride between variables (and metric entries)
@@ -98,7 +164,10 @@ __device__ __forceinline__ void mapped_sweep(const R* __restrict__ s, R* __restr
     constexpr int NV = n_vars_c(DIM);
     const bool first = (A == 0);
     const R* sb = s + o;
-    const R* mb = met + o;
+    const int el = o % NE;
+    const int bp = o / NE;  // the line's first point: its A index is 0
+    R xi[3] = {p.xg[bp % M], p.xg[(bp / M) % M], DIM == 3 ? p.xg[bp / (M * M)] : R(0)};
+    const LineMetric<R, DIM, NE, A> lm(geo, el, xi);
 
     // batch 0: continuity + momentum rows
     {
@@ -107,8 +176,7 @@ __device__ __forceinline__ void mapped_sweep(const R* __restrict__ s, R* __restr
         for (int t = 0; t < M; ++t) {
             const int q = NE * STRIDE * t;
             R Sa[DIM], V[DIM];
-#pragma unroll
-            for (int b = 0; b < DIM; ++b) Sa[b] = mb[q + VS * (A * DIM + b)];
+            lm.row(p.xg[t], Sa);
 #pragma unroll
             for (int b = 0; b < DIM; ++b) V[b] = sb[q + VS * (1 + b)];
             const R P = sb[q];
@@ -137,8 +205,10 @@ __device__ __forceinline__ void mapped_sweep(const R* __restrict__ s, R* __restr
         for (int t = 0; t < M; ++t) {
             const int q = NE * STRIDE * t;
             const R Vc = sb[q + VS * (1 + c)];
+            R Sa[DIM];
+            lm.row(p.xg[t], Sa);
 #pragma unroll
-            for (int b = 0; b < DIM; ++b) Y[b][t] = mb[q + VS * (A * DIM + b)] * Vc;
+            for (int b = 0; b < DIM; ++b) Y[b][t] = Sa[b] * Vc;
         }
         int rows[DIM];
 #pragma unroll
@@ -160,7 +230,6 @@ __global__ void __launch_bounds__(MappedShape<R, DIM, M, NE>::BS)
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
     unsigned char* buf = smem_raw + S::HDR;
     R* acc = reinterpret_cast<R*>(smem_raw + S::ACC_OFF);
-    R* met = reinterpret_cast<R*>(smem_raw + S::MET_OFF);
     R* geo = reinterpret_cast<R*>(smem_raw + S::GEO_OFF);  // [c][x][el]
 
     const int tid = threadIdx.x;
@@ -175,7 +244,7 @@ __global__ void __launch_bounds__(MappedShape<R, DIM, M, NE>::BS)
     // ---------------- stage the chunk and its corners ----------------
     // With group == NE the chunk's corners are one contiguous, 16-byte-multiple
     // range (2^d d words per element): a second bulk copy on its own mbarrier,
-    // so the metric pass starts while the field chunk is still in flight.
+    // so the sweeps' corner reads do not wait on a second round trip.
     constexpr int GEO_WORDS = NC * DIM * NE;
     const bool geo_bulk = fast && contiguous && (reinterpret_cast<uintptr_t>(p.geo) & 15u) == 0;
     if (fast) {
@@ -225,35 +294,6 @@ __global__ void __launch_bounds__(MappedShape<R, DIM, M, NE>::BS)
         mbar_wait_parity(bar + 1, 0);
     }
 
-    // ---------------- metric pass: S = adj(J), 1/|J| at every point ----------------
-    for (int idx = tid; idx < NE * NP; idx += BS) {
-        const int el = idx % NE;
-        const int pt = idx / NE;
-        R xi[3];
-        xi[0] = p.xg[pt % M];
-        xi[1] = p.xg[(pt / M) % M];
-        xi[2] = DIM == 3 ? p.xg[pt / (M * M)] : R(0);
-        R J[DIM * DIM];
-#pragma unroll
-        for (int q = 0; q < DIM * DIM; ++q) J[q] = R(0);
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-#pragma unroll
-            for (int j = 0; j < DIM; ++j) {
-                R dn = R(0.5) * ((c >> j) & 1 ? R(1) : R(-1));  // dN_c / dxi_j
-#pragma unroll
-                for (int k = 0; k < DIM; ++k)
-                    if (k != j) dn *= R(0.5) * (R(1) + ((c >> k) & 1 ? xi[k] : -xi[k]));
-#pragma unroll
-                for (int i = 0; i < DIM; ++i) J[i * DIM + j] = fma(geo[el + NE * (i + DIM * c)], dn, J[i * DIM + j]);
-            }
-        }
-        R Sm[DIM * DIM];
-        const R det = mapped_adjugate<R, DIM>(J, Sm);
-#pragma unroll
-        for (int q = 0; q < DIM * DIM; ++q) met[idx + VS * q] = Sm[q];
-        met[idx + VS * DIM * DIM] = R(1) / det;
-    }
     if (fast) mbar_wait_parity(bar, 0);
     __syncthreads();
 
@@ -266,7 +306,7 @@ __global__ void __launch_bounds__(MappedShape<R, DIM, M, NE>::BS)
 #pragma unroll 1
         for (int k = 0; k < LM::ITERS; ++k) {
             const int o = map[k * BS + tid];
-            if (o != 0xFFFF) mapped_sweep<R, DIM, M, NE, A>(s, acc, met, p, o);
+            if (o != 0xFFFF) mapped_sweep<R, DIM, M, NE, A>(s, acc, geo, p, o);
         }
     };
     sweep(std::integral_constant<int, 0>{});
@@ -280,7 +320,17 @@ __global__ void __launch_bounds__(MappedShape<R, DIM, M, NE>::BS)
 
     // ---------------- out = -acc / |J| (+ source), over the staged input ----------------
     for (int idx = tid; idx < NE * NP; idx += BS) {
-        const R inv = met[idx + VS * DIM * DIM];
+        const int el = idx % NE;
+        const int pt = idx / NE;
+        const R xi[3] = {p.xg[pt % M], p.xg[(pt / M) % M], DIM == 3 ? p.xg[pt / (M * M)] : R(0)};
+        R J[DIM * DIM], col[DIM], Sm[DIM * DIM];
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) {
+            mapped_jcol<R, DIM, NE>(geo, el, j, xi, col);
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) J[i * DIM + j] = col[i];
+        }
+        const R inv = R(1) / mapped_adjugate<R, DIM>(J, Sm);
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
             R o = -acc[idx + VS * v] * inv;
