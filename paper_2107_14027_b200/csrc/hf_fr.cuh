@@ -118,25 +118,32 @@ __global__ void __launch_bounds__(FrProjShape<R, DIM, M, NE>::BS)
         __syncthreads();
     }
     const R* s = reinterpret_cast<const R*>(buf + head);
-    // one task = (element, axis, line, variable): both ends of the line, coalesced over the element
-    for (int task = tid; task < NE * DIM * LN * NV; task += BS) {
+    // one task = (element, line, axis): both ends of the line for every variable (the
+    // index arithmetic is paid once per line), stores coalesced over the element
+    for (int task = tid; task < NE * LN * DIM; task += BS) {
         const int el = task % NE;
-        int r = task / NE;
-        const int l = r % LN;
-        r /= LN;
-        const int a = r % DIM;
-        const int v = r / DIM;
+        const int l = (task / NE) % LN;
+        const int a = task / (NE * LN);
         const long long e = E0 + el;
         if (e >= p.n_elem) continue;
-        R sm = R(0), sp = R(0);
+        int pt[M];
 #pragma unroll
-        for (int t = 0; t < M; ++t) {
-            const R u = s[el + NE * (fr_line_point<DIM, M>(a, l, t) + NP * v)];
-            sm = fma(f.lm[t], u, sm);
-            sp = fma(f.lp[t], u, sp);
+        for (int t = 0; t < M; ++t) pt[t] = el + NE * fr_line_point<DIM, M>(a, l, t);
+        const long long ge = e / p.group;
+        R* ub = uf + ge * p.group * 2 * DIM * LN * NV + (e - ge * p.group) + (long long)p.group * (l + LN * 2 * a);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            R sm = R(0), sp = R(0);
+#pragma unroll
+            for (int t = 0; t < M; ++t) {
+                const R u = s[pt[t] + NE * NP * v];
+                sm = fma(f.lm[t], u, sm);
+                sp = fma(f.lp[t], u, sp);
+            }
+            R* q = ub + (long long)p.group * LN * 2 * DIM * v;  // face_word(e, a, s, l, v)
+            q[0] = sm;
+            q[(long long)p.group * LN] = sp;
         }
-        uf[face_word(DIM, M, p.group, e, a, 0, l, v)] = sm;
-        uf[face_word(DIM, M, p.group, e, a, 1, l, v)] = sp;
     }
 }
 
