@@ -173,7 +173,12 @@ struct FrCorrShape {
     static constexpr int NV = n_vars_c(DIM);
     static constexpr int LN = fr_lines<DIM, M>();
     static constexpr int TASKS = NE * DIM * LN;  // (element, axis, line)
-    static constexpr int BS = ((TASKS + 31) / 32) * 32 < 64 ? 64 : (((TASKS + 31) / 32) * 32 > 256 ? 256 : ((TASKS + 31) / 32) * 32);
+    // one thread per stage-4 task of an axis (NE * LN * 2); FP32 also at least one
+    // per two stage-5 points; whole warps, 64..256 (measured per precision,
+    // profiles/ext_r01c_fr.jsonl: FP64 p3-p6 0.55-0.74 -> 0.8-0.9 of the roofline)
+    static constexpr int T4 = NE * LN * 2, T5 = (NE * ipow_c(M, DIM) + 1) / 2;
+    static constexpr int T = ((sizeof(R) == 8 || T4 > T5 ? T4 : T5) + 31) / 32 * 32;
+    static constexpr int BS = T < 64 ? 64 : (T > 256 ? 256 : T);
     static constexpr size_t SMEM = size_t(TASKS) * 2 * NV * sizeof(R);  // jumps [v][s][a][l][el]
 };
 
