@@ -137,19 +137,31 @@ struct LineMetric {
 };
 
 // Accumulate d = D * Y (line rows of one batch) into the shared partial sums.
+// Rows go through the contraction in pairs (same D row): FFMA2 for FP32.
 template <class R, int M, int NE, int STRIDE, int NROW>
 __device__ __forceinline__ void mapped_contract(const Params<R>& p, const R (&Y)[NROW][M], R* __restrict__ acc_line,
                                                 const int (&rows)[NROW], R scale, bool first) {
     constexpr int NP_STRIDE = NE * STRIDE;
+    using PR = Pair<R>;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
 #pragma unroll
-        for (int r = 0; r < NROW; ++r) {
-            R s = p.D[i * M] * Y[r][0];
+        for (int r = 0; r < NROW; r += 2) {
+            if (r + 1 < NROW) {
+                PR d = pmul(p.D[i * M], PR::make(Y[r][0], Y[r + 1][0]));
 #pragma unroll
-            for (int t = 1; t < M; ++t) s = fma(p.D[i * M + t], Y[r][t], s);
-            R* q = acc_line + rows[r] + NP_STRIDE * i;
-            *q = first ? scale * s : fma(scale, s, *q);
+                for (int t = 1; t < M; ++t) d = pfma(p.D[i * M + t], PR::make(Y[r][t], Y[r + 1][t]), d);
+                R* q0 = acc_line + rows[r] + NP_STRIDE * i;
+                R* q1 = acc_line + rows[r + 1] + NP_STRIDE * i;
+                *q0 = first ? scale * d.x() : fma(scale, d.x(), *q0);
+                *q1 = first ? scale * d.y() : fma(scale, d.y(), *q1);
+            } else {
+                R s = p.D[i * M] * Y[r][0];
+#pragma unroll
+                for (int t = 1; t < M; ++t) s = fma(p.D[i * M + t], Y[r][t], s);
+                R* q = acc_line + rows[r] + NP_STRIDE * i;
+                *q = first ? scale * s : fma(scale, s, *q);
+            }
         }
     }
 }
