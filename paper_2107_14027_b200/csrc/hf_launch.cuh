@@ -11,6 +11,7 @@
 // (hf_select_table.inc, tools/select_methods.py) chooses from.
 #pragma once
 
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 
@@ -228,15 +229,28 @@ cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dr
     // (whose superset could run past the end) for the guarded tail launch
     if (p.group == NE && n_full > 0 && n_full * NE == p.n_elem && (p.total_words * (long long)sizeof(R)) % 16 != 0)
         n_full -= 1;
-    static int blocks_per_sm = -1;
-    if (blocks_per_sm < 0 && !dry) {
+    // resident CTAs per SM: measured once per device (thread-safe: atomics), the
+    // shared-memory attribute set on every launch (it is per device)
+    static std::atomic<int> bps_cache[16];
+    int blocks_per_sm = 0;
+    if (!dry) {
         if (int e = set_smem_attr(kernel, S::SMEM)) return cudaError_t(e);
-        int b = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, S::BS, S::SMEM) != cudaSuccess || b < 1) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) {
             cudaGetLastError();
-            b = 1;
+            dev = 0;
         }
-        blocks_per_sm = b;
+        const int slot = dev & 15;
+        blocks_per_sm = bps_cache[slot].load(std::memory_order_relaxed);
+        if (blocks_per_sm < 1) {
+            int b = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, S::BS, S::SMEM) != cudaSuccess || b < 1) {
+                cudaGetLastError();
+                b = 1;
+            }
+            bps_cache[slot].store(b, std::memory_order_relaxed);
+            blocks_per_sm = b;
+        }
     }
     const long long slots = (long long)(blocks_per_sm > 0 ? blocks_per_sm : 1) * num_sms();
     const long long grid = n_full < slots ? n_full : slots;
