@@ -617,15 +617,42 @@ int hf_fused_divergence_host(hf_context* c, const hf_problem* pr, const void* u_
     const size_t w = word_bytes(pr);
     const int64_t gw = int64_t(pr->group) * ipow64(pr->p + 1, pr->d) * (1 + pr->d + pr->d * pr->d);
     const int64_t n_groups = (pr->n_elem + pr->group - 1) / pr->group;
-    // Slice: whole groups, ~48 MB per slot, a multiple of the kernel's chunk.  The copy pipeline
-    // moves one direction alone while it fills and drains (one slice each), so a call of n
-    // slices runs at ~n/(n+1) of the duplex PCIe rate (measured: 16 MB slices lost 4 % to 48 MB).
+    // Slices: whole groups, multiples of the kernel's chunk, at most ~48 MB (the slot size).
+    // The copy pipeline moves one direction alone while it fills (the first H2D) and drains
+    // (the last D2H), so the plan ramps up and down: b/8, b/4, b/2, b, ..., b, b/2, b/4, b/8.
     int pref = hf_preferred_group(pr);
     if (pref < 1) pref = 1;
-    int64_t slice_groups = std::max<int64_t>(1, (int64_t(48) << 20) / int64_t(gw * w));
     const int64_t chunk_groups = std::max<int64_t>(1, (pref + pr->group - 1) / pr->group);
-    slice_groups = std::max<int64_t>(chunk_groups, slice_groups / chunk_groups * chunk_groups);
-    slice_groups = std::min<int64_t>(slice_groups, n_groups);
+    auto rnd = [&](int64_t x) { return std::max<int64_t>(chunk_groups, x / chunk_groups * chunk_groups); };
+    const int64_t base = std::min<int64_t>(rnd((int64_t(48) << 20) / int64_t(gw * w)), n_groups);
+    std::vector<int64_t> plan;
+    {
+        const int64_t ramp[3] = {rnd(base / 8), rnd(base / 4), rnd(base / 2)};
+        const int64_t tail = ramp[0] + ramp[1] + ramp[2];
+        int64_t rem = n_groups;
+        if (rem <= 2 * tail + base) {  // small: ~6 equal slices
+            const int64_t q = rnd(std::max<int64_t>(1, rem / 6));
+            while (rem > 0) {
+                plan.push_back(std::min(q, rem));
+                rem -= plan.back();
+            }
+        } else {
+            for (int k = 0; k < 3; ++k) {
+                plan.push_back(ramp[k]);
+                rem -= ramp[k];
+            }
+            while (rem > tail + base) {
+                plan.push_back(base);
+                rem -= base;
+            }
+            const int64_t mid = (rem - tail) / chunk_groups * chunk_groups;  // whole chunks
+            if (mid > 0) plan.push_back(mid);
+            for (int k = 2; k >= 0; --k) plan.push_back(ramp[k]);
+            plan.back() += rem - tail - mid;  // the remainder rides in the final slice
+        }
+    }
+    int64_t slice_groups = 0;
+    for (int64_t q : plan) slice_groups = std::max(slice_groups, q);
     if (int rc = ctx_reserve(c, size_t(slice_groups * gw) * w)) return rc;
 
     // Pageable host memory is pinned for the duration of the call.
@@ -641,10 +668,10 @@ int hf_fused_divergence_host(hf_context* c, const hf_problem* pr, const void* u_
     }
 
     int rc = HF_OK;
-    int64_t s_idx = 0;
-    for (int64_t g0 = 0; g0 < n_groups && rc == HF_OK; g0 += slice_groups, ++s_idx) {
+    int64_t g0 = 0;
+    for (size_t s_idx = 0; s_idx < plan.size() && rc == HF_OK; g0 += plan[s_idx], ++s_idx) {
         const int slot = int(s_idx % hf_context::kSlots);
-        const int64_t ng = std::min<int64_t>(slice_groups, n_groups - g0);
+        const int64_t ng = plan[s_idx];
         const size_t bytes = size_t(ng * gw) * w;
         cudaStream_t st = c->stream[slot];
         const auto* src = static_cast<const unsigned char*>(u_host) + size_t(g0 * gw) * w;

@@ -1,0 +1,58 @@
+"""GPU: the host-buffer path (hf_fused_divergence_host, the (b1) replacement for
+oracle_divergence, oracle.hpp:20-62) on fields large enough for the sliced copy
+pipeline (ramped slices, three streams), pinned and pageable memory, partial last
+group: bit-identical to the device-buffer kernel on the same field, and equal to
+the CPU oracle on sampled elements (1e-12 FP64 / 1e-5 FP32)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from gpu_util import PAR
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("d,p,fp32,target_mb", [(3, 3, False, 400), (3, 6, True, 300), (2, 2, True, 60),
+                                                (3, 1, False, 5)])
+def test_host_path_matches_device_path(cuda, d, p, fp32, target_mb):
+    import paper_2107_14027_b200 as hf
+    from paper_2107_14027_b200 import Precision
+    prec = Precision.fp32 if fp32 else Precision.fp64
+    w = 4 if fp32 else 8
+    g = hf.preferred_group(hf.make_problem(d, p, 1, 1, prec, PAR))
+    nv, npt = O.n_vars(d), (p + 1) ** d
+    n = max(g, int(target_mb * 2 ** 20 / (nv * npt * w)) // g * g) + 1  # partial last group
+    pr = hf.make_problem(d, p, n, g, prec, PAR, with_source=True)
+    dt = torch.float32 if fp32 else torch.float64
+    gen = torch.Generator().manual_seed(5)
+    u = (torch.rand(hf.field_words(pr), generator=gen, dtype=torch.float64) * 2 - 1).to(dt)
+    # padding elements of the last group stay zero, as in a StateField
+    nwg = hf.field_words(pr) // ((n + g - 1) // g)
+    last = u[-nwg:].view(nv * npt, g)
+    last[:, n % g:] = 0
+    # device path
+    ud = u.cuda()
+    od = torch.zeros_like(ud)
+    hf.fused_divergence_device(pr, ud, od)
+    torch.cuda.synchronize()
+    ref = od.cpu()
+    ctx = hf.Context(0)
+    for pinned in (True, False):
+        src = u.pin_memory() if pinned else u.clone()
+        dst = torch.zeros_like(src)
+        if pinned:
+            dst = dst.pin_memory()
+        ctx.run(pr, src, dst)
+        assert torch.equal(dst, ref), f"host path differs from the device path (pinned={pinned})"
+    ctx.close()
+    # oracle on a sample: the first and the last (partial) group
+    U = u.double().numpy()
+    for e0, e1 in ((0, min(n, g)), ((n - 1) // g * g, n)):
+        out = np.zeros_like(U)
+        O.oracle_divergence_elements(d, p, g, U, out, PAR.nu, PAR.zeta, PAR.T, (1.0, 1.0, 1.0), True, e0, e1)
+        sl = slice(e0 // g * nwg, ((e1 + g - 1) // g) * nwg)
+        got = ref.double().numpy()[sl]
+        want = out[sl]
+        err = np.max(np.abs(got - want)) / max(1.0, np.max(np.abs(want)))
+        assert err <= (1e-5 if fp32 else 1e-12), err
