@@ -211,3 +211,33 @@ def test_config1_full_oracle(cuda):
     assert err <= 1e-12
     err = check_parity(3, 3, 32768, g, False, U, with_source=True)
     assert err <= 1e-12
+
+
+# ---------------------------------------------------------------- empty problems (n_elem = 0)
+def test_empty_problems_are_no_ops(cuda):
+    """n_elem = 0 on every entry point: success, nothing launched, nothing written
+    (the reference's oracle returns an empty field for an empty input)."""
+    import torch
+    import paper_2107_14027_b200 as hf
+    from paper_2107_14027_b200 import Method, Precision
+    for d, p in ((3, 3), (2, 5)):
+        for prec in (Precision.fp32, Precision.fp64):
+            pr = hf.make_problem(d, p, 0, 4, prec, PAR, with_source=True)
+            assert hf.field_words(pr) == 0
+            buf = torch.full((8,), 3.5, device="cuda", dtype=torch.float64)
+            hf.fused_divergence_device(pr, buf, buf[4:])
+            for meth in (Method.lines, Method.unfused) if d == 2 else (Method.lines, Method.planar,
+                                                                     Method.planar_managed, Method.unfused):
+                pr.method = int(meth)
+                if meth == Method.unfused:
+                    hf.unfused_divergence_device(pr, buf, buf[4:], buf[2:])
+                else:
+                    hf.fused_divergence_device(pr, buf, buf[4:])
+            pr.method = int(Method.auto)
+            hf.fused_divergence_mapped_device(pr, buf, buf[2:], buf[4:])
+            hf.fr_project_device(pr, buf, buf[4:])
+            torch.cuda.synchronize()
+            assert torch.all(buf == 3.5)
+            U = hf.StateField(d, p, 0, 4, prec)
+            out = hf.fused_divergence(U, PAR, with_source=True)
+            assert out.n_elem == 0 and out.data.size == 0
