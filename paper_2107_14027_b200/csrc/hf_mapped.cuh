@@ -179,7 +179,13 @@ __device__ __forceinline__ void mapped_sweep(const R* __restrict__ s, R* __restr
     const int el = o % NE;
     const int bp = o / NE;  // the line's first point: its A index is 0
     R xi[3] = {p.xg[bp % M], p.xg[(bp / M) % M], DIM == 3 ? p.xg[bp / (M * M)] : R(0)};
-    const LineMetric<R, DIM, NE, A> lm(geo, el, xi);
+    // row A of adj(J) at every point of the line, kept for all batches
+    R SL[M][DIM];
+    {
+        const LineMetric<R, DIM, NE, A> lm(geo, el, xi);
+#pragma unroll
+        for (int t = 0; t < M; ++t) lm.row(p.xg[t], SL[t]);
+    }
 
     // batch 0: continuity + momentum rows
     {
@@ -187,8 +193,8 @@ __device__ __forceinline__ void mapped_sweep(const R* __restrict__ s, R* __restr
 #pragma unroll
         for (int t = 0; t < M; ++t) {
             const int q = NE * STRIDE * t;
-            R Sa[DIM], V[DIM];
-            lm.row(p.xg[t], Sa);
+            const R(&Sa)[DIM] = SL[t];
+            R V[DIM];
 #pragma unroll
             for (int b = 0; b < DIM; ++b) V[b] = sb[q + VS * (1 + b)];
             const R P = sb[q];
@@ -217,10 +223,8 @@ __device__ __forceinline__ void mapped_sweep(const R* __restrict__ s, R* __restr
         for (int t = 0; t < M; ++t) {
             const int q = NE * STRIDE * t;
             const R Vc = sb[q + VS * (1 + c)];
-            R Sa[DIM];
-            lm.row(p.xg[t], Sa);
 #pragma unroll
-            for (int b = 0; b < DIM; ++b) Y[b][t] = Sa[b] * Vc;
+            for (int b = 0; b < DIM; ++b) Y[b][t] = SL[t][b] * Vc;
         }
         int rows[DIM];
 #pragma unroll
