@@ -159,6 +159,19 @@ HF_API int hf_fr_correct(const hf_problem* pr, const hf_mesh* mesh, const void* 
 HF_API int hf_fr_residual(const hf_problem* pr, const int* dims, const void* u_dev, void* uf_dev, void* divf_dev,
                           void* stream);
 
+/* ---- peer memory for the FR ghost layers (NVLink / NVSwitch, one process per GPU) ----
+ * A rank exports its face array (hf_ipc_handle), its neighbours open it
+ * (hf_ipc_open) and pass pointers into it as ghost_lo / ghost_hi of
+ * hf_fr_correct: the correction kernel then reads the neighbours' boundary
+ * faces straight from their memory over NVLink -- the exchange and the
+ * interface kernel are one kernel, no copy.  Thin wrappers over CUDA IPC; the
+ * handle names dev_ptr's whole allocation and *offset_out is dev_ptr's byte
+ * offset in it (add it to the pointer hf_ipc_open returns). */
+#define HF_IPC_HANDLE_BYTES 64
+HF_API int hf_ipc_handle(const void* dev_ptr, void* handle_out, int64_t* offset_out);
+HF_API int hf_ipc_open(const void* handle, void** dev_ptr_out);
+HF_API int hf_ipc_close(void* dev_ptr);
+
 /* ---- host-buffer entry point (the (b1) replacement) ----
  * u_host / divf_host: host arrays of hf_field_words(pr) words of the problem's
  * precision (float for HF_FP32, double for HF_FP64).  Pinned memory is used

@@ -2,6 +2,7 @@
 // construction, method selection, launches, the pipelined host-buffer path and
 // the multi-GPU partition.  Everything here is host code; the kernels live in
 // the hf_inst_*.cu units.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -476,6 +477,48 @@ int hf_fr_residual(const hf_problem* pr, const int* dims, const void* u_dev, voi
     if (int rc = hf_fused_divergence(pr, u_dev, divf_dev, stream)) return rc;  // stages 2+3+6
     if (int rc = hf_fr_project(pr, u_dev, uf_dev, stream)) return rc;        // stage 1
     return hf_fr_correct(pr, &ms, uf_dev, nullptr, nullptr, divf_dev, stream);  // stages 4+5
+}
+
+int hf_ipc_handle(const void* dev_ptr, void* handle_out, int64_t* offset_out) {
+    if (!dev_ptr || !handle_out || !offset_out) return fail(HF_EINVAL, "hf_ipc_handle: null argument");
+    // the handle names the whole allocation (caching allocators hand out pieces of one)
+    // (driver entry point through the runtime: no link-time dependency on libcuda)
+    using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static GetRange get_range = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<GetRange>(fn);
+    }();
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (!get_range || get_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+        return fail(HF_ERUNTIME, "hf_ipc_handle: cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) == HF_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle_out, &h, sizeof(h));
+    *offset_out = int64_t(reinterpret_cast<uintptr_t>(dev_ptr) - uintptr_t(base));
+    return HF_OK;
+}
+
+int hf_ipc_open(const void* handle, void** dev_ptr_out) {
+    if (!handle || !dev_ptr_out) return fail(HF_EINVAL, "hf_ipc_open: null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+    return HF_OK;
+}
+
+int hf_ipc_close(void* dev_ptr) {
+    if (!dev_ptr) return HF_OK;
+    cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+    return HF_OK;
 }
 
 int hf_unfused_divergence(const hf_problem* pr, const void* u_dev, void* divf_dev, void* ws_dev, void* stream) {

@@ -400,6 +400,26 @@ def fr_residual_device(pr: hf_problem, dims, u, uf, out, stream=None) -> None:
           "hf_fr_residual")
 
 
+def ipc_handle(dev) -> tuple[bytes, int]:
+    """CUDA IPC handle (64 bytes) of the allocation holding `dev`, and dev's byte offset in it."""
+    buf = (C.c_char * 64)()
+    off = C.c_int64()
+    check(_lib.load().hf_ipc_handle(_ptr(dev), buf, C.byref(off)), "hf_ipc_handle")
+    return bytes(buf), int(off.value)
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map a peer process's allocation; returns its device address in this process."""
+    out = C.c_void_p()
+    buf = (C.c_char * 64).from_buffer_copy(handle)
+    check(_lib.load().hf_ipc_open(buf, C.byref(out)), "hf_ipc_open")
+    return int(out.value)
+
+
+def ipc_close(ptr: int) -> None:
+    check(_lib.load().hf_ipc_close(C.c_void_p(ptr)), "hf_ipc_close")
+
+
 def fused_divergence_variant(pr: hf_problem, method: Method, variant: int, u, out, stream=None) -> None:
     """Tuning hook: launch a specific method/variant, bypassing the selection table."""
     check(_lib.load().hf_fused_divergence_variant(C.byref(pr), int(method), int(variant), _ptr(u), _ptr(out),

@@ -194,3 +194,56 @@ def fr_residual_slab(sl: FrSlab, u, out, uf, ghost_lo, ghost_hi, dist=None, ops=
         r.wait()
     mesh = H.make_mesh(sl.dims, sl.d, sl.e_begin, sl.n_elem, sl.layer if sl.world > 1 else 0)
     ops.correct(sl.problem, mesh, uf, out, ghost_lo if sl.world > 1 else None, ghost_hi if sl.world > 1 else None)
+
+
+class FrPeers:
+    """The neighbouring ranks' face arrays mapped into this process (CUDA IPC:
+    peer memory over NVLink / NVSwitch).  With them, hf_fr_correct reads the
+    ghost layers straight from the neighbours' memory -- the exchange and the
+    interface kernel are one kernel, with no copy and no NCCL call on the data
+    path; ``torch.distributed`` only orders the steps (barriers)."""
+
+    def __init__(self, sl: FrSlab, uf, dist=None):
+        if dist is None:
+            import torch.distributed as dist
+        self.sl = sl
+        self._opened = []
+        handle, off = H.ipc_handle(uf)
+        table = [None] * sl.world
+        dist.all_gather_object(table, (handle, off, sl.n_layers))
+        wb = uf.element_size()
+        lo, hi = (sl.rank - 1) % sl.world, (sl.rank + 1) % sl.world
+        base = {}
+        for r in {lo, hi}:
+            h, o, _ = table[r]
+            if r == sl.rank:  # world == 1: our own array
+                base[r] = int(uf.data_ptr())
+            else:
+                ptr = H.ipc_open(h)
+                self._opened.append(ptr)
+                base[r] = ptr + o
+        w = sl.face_layer_words
+        self.ghost_lo = base[lo] + (table[lo][2] - 1) * w * wb  # last layer below us
+        self.ghost_hi = base[hi]                                 # first layer above us
+
+    def close(self):
+        for ptr in self._opened:
+            H.ipc_close(ptr)
+        self._opened = []
+
+
+def fr_residual_slab_peer(sl: FrSlab, u, out, uf, peers: FrPeers, dist=None):
+    """Stages 1-6 on one rank's slab with the ghost layers read from peer memory.
+    Barriers: every rank's faces are projected before anyone corrects, and every
+    correction has finished before anyone projects the next step's faces."""
+    if dist is None:
+        import torch.distributed as dist
+    import torch
+    H.fr_project_device(sl.problem, u, uf)
+    H.fused_divergence_device(sl.problem, u, out)
+    torch.cuda.current_stream().synchronize()
+    dist.barrier()
+    mesh = H.make_mesh(sl.dims, sl.d, sl.e_begin, sl.n_elem, sl.layer)
+    H.fr_correct_device(sl.problem, mesh, uf, out, peers.ghost_lo, peers.ghost_hi)
+    torch.cuda.current_stream().synchronize()
+    dist.barrier()

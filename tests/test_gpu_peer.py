@@ -1,0 +1,88 @@
+"""GPU: the FR right-hand side on layer slabs with the ghost layers read from the
+neighbours' memory through CUDA IPC (multi_gpu.FrPeers) -- two (three) processes
+sharing the one GPU of the test box stand in for ranks on NVLink-connected GPUs;
+the result must equal the single-partition residual bit-for-bit... up to the
+summation order, which is the same kernel's: exactly equal."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _peer_worker(rank, world, port, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    import paper_2107_14027_b200 as hf
+    from gpu_util import PAR
+    from paper_2107_14027_b200 import Precision
+    from paper_2107_14027_b200.multi_gpu import FrPeers, fr_residual_slab_peer, make_fr_slab
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = []
+    for d, p, dims, g in [(3, 3, (4, 2, 6), 4), (2, 4, (8, 6), 4)]:
+        n = int(np.prod(dims))
+        U = O.random_field(d, p, n, g, False, 41)
+        pr = hf.make_problem(d, p, n, g, Precision.fp64, PAR, with_source=True)
+        sl = make_fr_slab(pr, dims, world, rank)
+        gw = hf.field_words(pr) // (n // g)
+        e0, e1 = sl.e_begin, sl.e_begin + sl.n_elem
+        u = torch.from_numpy(U[e0 // g * gw:e1 // g * gw].copy()).cuda()
+        out = torch.zeros_like(u)
+        uf = torch.zeros(hf.face_words(sl.problem), dtype=torch.float64, device="cuda")
+        peers = FrPeers(sl, uf, dist)
+        fr_residual_slab_peer(sl, u, out, uf, peers, dist)
+        parts = [None] * world
+        dist.all_gather_object(parts, (e0, e1, out.cpu().numpy()))
+        peers.close()
+        if rank == 0:
+            full = np.zeros(hf.field_words(pr))
+            for a, b, arr in parts:
+                full[a // g * gw:b // g * gw] = arr
+            # the single-device residual of the same library
+            ud = torch.from_numpy(U).cuda()
+            od = torch.zeros_like(ud)
+            ufd = torch.zeros(hf.face_words(pr), dtype=torch.float64, device="cuda")
+            hf.fr_residual_device(pr, dims, ud, ufd, od)
+            torch.cuda.synchronize()
+            ref = O.fr_residual(d, p, dims, g, U, PAR.nu, PAR.zeta, PAR.T, (1.0, 1.0, 1.0), True)
+            res.append((float(np.max(np.abs(full - od.cpu().numpy()))), O.field_rel_error(d, p, n, g, full, ref)))
+        dist.barrier()
+    dist.destroy_process_group()
+    q.put((rank, res))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fr_ghost_layers_from_peer_memory(cuda, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr_ in procs:
+        pr_.start()
+    out = dict(q.get(timeout=600) for _ in procs)
+    for pr_ in procs:
+        pr_.join(timeout=60)
+    assert len(out[0]) == 2, out
+    for diff_device, err_oracle in out[0]:
+        assert diff_device == 0.0 and err_oracle <= 1e-12, out[0]
