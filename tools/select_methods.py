@@ -137,6 +137,7 @@ def main():
                 cands = [(Method.lines, v) for v in vs]
                 if d == 3 and not args.no_planar:
                     cands.append((Method.planar, 0))
+                    cands.append((Method.planar_managed, 0))
                 if not args.no_unfused:
                     cands.append((Method.unfused, 0))
                 for r in measure_config(d, p, prec, cands, args.points):
@@ -179,7 +180,7 @@ def write_table(rows, points, raw="profiles/select_r01_*.jsonl"):
     with open(path, "w") as f:
         f.write("// hf_select_table.inc -- measured method selection (replaces the reference's\n"
                 "// preset_table, presets.hpp:25-37, and default_lines_n, presets.hpp:86-103).\n"
-                "//\n// Row: { d, p, precision(0=fp32,1=fp64), method(1=planar,2=lines), variant }.\n"
+                "//\n// Row: { d, p, precision(0=fp32,1=fp64), method(1=planar,2=lines,4=planar-managed), variant }.\n"
                 "// lines variants (hf_launch.cuh): 0/1/2/7 = one chunk per CTA with NE0, NE0/2, 2*NE0, NE0/4\n"
                 "// elements; 3..6, 8..15 = persistent TMA-ring kernel, (elements, stages, consumer groups):\n"
                 "// 3 (NE0,2,1) 4 (NE0/2,3,1) 5 (NE0/2,2,1) 6 (NE0,3,1) 8 (NE0/4,3,1) 9 (NE0/4,4,1)\n"
@@ -189,7 +190,7 @@ def write_table(rows, points, raw="profiles/select_r01_*.jsonl"):
                 f"// HBM GB/s, median of 20 launches at ~{points:.0e} points per configuration;\n"
                 f"// raw rows in {raw}).\n")
         for (d, p, prec), (_, r) in sorted(best.items()):
-            m = 1 if r["method"] == "planar" else 2
+            m = {"planar": 1, "lines": 2, "planar_managed": 4}[r["method"]]
             f.write(f"    {{{d}, {p}, {0 if prec == 'fp32' else 1}, {m}, {r['variant']}}},"
                     f"  // {r['kernel']}: {r['alg_GBps']:.0f} GB/s, {r['gdofs']:.2f} GDoF/s\n")
     print("wrote", path)
