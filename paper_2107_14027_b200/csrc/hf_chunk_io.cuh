@@ -11,10 +11,10 @@
 //     NE >= 1 works and chunk sizes can be chosen for occupancy alone.
 //   * rows: group % NE == 0 with 16-byte rows; one copy per (point, variable)
 //     row of NE words at stride `group`.
-// The work is split over the 32 lanes of one warp: lane l owns a fixed region
-// of the stage buffer for both directions, so a producer lane can store its
-// region of a finished chunk, wait for just that region to leave shared memory,
-// and refill it with the next chunk.
+// The work is split over the lanes of one warp: lane l owns a fixed region (a
+// piece of >= 64 KB, so one lane for most chunks) of the stage buffer for both
+// directions, so a producer lane can store its region of a finished chunk, wait
+// for just that region to leave shared memory, and refill it with the next chunk.
 #pragma once
 
 #include "hf_common.cuh"

@@ -7,11 +7,10 @@
 //
 //   warp 0 (producer)  : keeps up to STAGES chunks in flight.  For each chunk
 //                        it waits for the owning group to finish the stage;
-//                        then every lane bulk-stores its 1/32 slice of the
-//                        finished divergence, waits for that slice to have
-//                        left shared memory, and reloads the slice with the
-//                        chunk STAGES ahead (mbarrier complete_tx) -- stores and
-//                        loads of a stage overlap slice by slice.
+//                        then each lane that owns a piece of the stage (pieces
+//                        of >= 64 KB, hf_chunk_io.cuh) bulk-stores it, waits
+//                        for it to have left shared memory, and reloads it
+//                        with the chunk STAGES ahead (mbarrier complete_tx).
 //   consumer group g   : chunks it = g, g+GROUPS, ... on its own SPG =
 //   (warps 1+g*W ..)     STAGES/GROUPS stages (s = g*SPG + (it/GROUPS) % SPG):
 //                        wait full[s], run the d sweeps (named barrier 1+g
