@@ -136,6 +136,66 @@ struct LineMetric {
     }
 };
 
+// Scalar / pair arithmetic for line_derivative (Pair<R>: FFMA2 for FP32).
+template <class R>
+__device__ __forceinline__ R t_mul(R s, R a) { return s * a; }
+template <class R>
+__device__ __forceinline__ R t_fma(R s, R a, R c) { return fma(s, a, c); }
+template <class R>
+__device__ __forceinline__ R t_add(R a, R b) { return a + b; }
+template <class R>
+__device__ __forceinline__ R t_sub(R a, R b) { return a - b; }
+template <class R>
+__device__ __forceinline__ Pair<R> t_mul(R s, Pair<R> a) { return pmul(s, a); }
+template <class R>
+__device__ __forceinline__ Pair<R> t_fma(R s, Pair<R> a, Pair<R> c) { return pfma(s, a, c); }
+template <class R>
+__device__ __forceinline__ Pair<R> t_add(Pair<R> a, Pair<R> b) { return padd(a, b); }
+template <class R>
+__device__ __forceinline__ Pair<R> t_sub(Pair<R> a, Pair<R> b) { return psub(a, b); }
+
+// d = D y along one line (y is overwritten).  From m = HF_EVEN_ODD_MIN_M the
+// even-odd split of D (Params::DE/DO/DC, as the lines kernel): about half the FMAs.
+template <class R, int M, class T>
+__device__ __forceinline__ void line_derivative(const Params<R>& p, T (&y)[M], T (&d)[M]) {
+    if constexpr (M < HF_EVEN_ODD_MIN_M) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            T a = t_mul(p.D[i * M], y[0]);
+#pragma unroll
+            for (int t = 1; t < M; ++t) a = t_fma(p.D[i * M + t], y[t], a);
+            d[i] = a;
+        }
+    } else {
+        constexpr int H = M / 2, K = kMaxH;
+#pragma unroll
+        for (int t = 0; t < H; ++t) {
+            const T y0 = y[t], y1 = y[M - 1 - t];
+            y[t] = t_add(y0, y1);
+            y[M - 1 - t] = t_sub(y0, y1);
+        }
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            T x = t_mul(p.DE[i * K], y[0]);
+            T z = t_mul(p.DO[i * K], y[M - 1]);
+#pragma unroll
+            for (int t = 1; t < H; ++t) {
+                x = t_fma(p.DE[i * K + t], y[t], x);
+                z = t_fma(p.DO[i * K + t], y[M - 1 - t], z);
+            }
+            if constexpr (M % 2 == 1) x = t_fma(p.DC[i], y[H], x);
+            d[i] = t_add(x, z);
+            d[M - 1 - i] = t_sub(z, x);
+        }
+        if constexpr (M % 2 == 1) {
+            T z = t_mul(p.DO[H * K], y[M - 1]);
+#pragma unroll
+            for (int t = 1; t < H; ++t) z = t_fma(p.DO[H * K + t], y[M - 1 - t], z);
+            d[H] = z;
+        }
+    }
+}
+
 // Accumulate d = D * Y (line rows of one batch) into the shared partial sums.
 // Rows go through the contraction in pairs (same D row): FFMA2 for FP32.
 template <class R, int M, int NE, int STRIDE, int NROW>
@@ -144,23 +204,28 @@ __device__ __forceinline__ void mapped_contract(const Params<R>& p, const R (&Y)
     constexpr int NP_STRIDE = NE * STRIDE;
     using PR = Pair<R>;
 #pragma unroll
-    for (int i = 0; i < M; ++i) {
+    for (int r = 0; r < NROW; r += 2) {
+        if (r + 1 < NROW) {
+            PR y[M], d[M];
 #pragma unroll
-        for (int r = 0; r < NROW; r += 2) {
-            if (r + 1 < NROW) {
-                PR d = pmul(p.D[i * M], PR::make(Y[r][0], Y[r + 1][0]));
+            for (int t = 0; t < M; ++t) y[t] = PR::make(Y[r][t], Y[r + 1][t]);
+            line_derivative<R, M>(p, y, d);
 #pragma unroll
-                for (int t = 1; t < M; ++t) d = pfma(p.D[i * M + t], PR::make(Y[r][t], Y[r + 1][t]), d);
+            for (int i = 0; i < M; ++i) {
                 R* q0 = acc_line + rows[r] + NP_STRIDE * i;
                 R* q1 = acc_line + rows[r + 1] + NP_STRIDE * i;
-                *q0 = first ? scale * d.x() : fma(scale, d.x(), *q0);
-                *q1 = first ? scale * d.y() : fma(scale, d.y(), *q1);
-            } else {
-                R s = p.D[i * M] * Y[r][0];
+                *q0 = first ? scale * d[i].x() : fma(scale, d[i].x(), *q0);
+                *q1 = first ? scale * d[i].y() : fma(scale, d[i].y(), *q1);
+            }
+        } else {
+            R y[M], d[M];
 #pragma unroll
-                for (int t = 1; t < M; ++t) s = fma(p.D[i * M + t], Y[r][t], s);
+            for (int t = 0; t < M; ++t) y[t] = Y[r][t];
+            line_derivative<R, M>(p, y, d);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
                 R* q = acc_line + rows[r] + NP_STRIDE * i;
-                *q = first ? scale * s : fma(scale, s, *q);
+                *q = first ? scale * d[i] : fma(scale, d[i], *q);
             }
         }
     }
