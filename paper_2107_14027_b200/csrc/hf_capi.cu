@@ -160,6 +160,16 @@ hfb::Params<R> make_params(const hf_problem* pr, const void* u, void* out, void*
     const double* D = ops().D[m];
     for (int i = 0; i < m * m; ++i) p.D[i] = R(D[i]);
     for (int i = 0; i < m; ++i) p.xg[i] = R(ops().x[m][i]);
+    for (int t = 0; t < m; ++t) {  // Lagrange basis at -1, +1 (FR stage 1 fused into the lines kernel)
+        double a = 1.0, b = 1.0;
+        for (int q = 0; q < m; ++q) {
+            if (q == t) continue;
+            a *= (-1.0 - ops().x[m][q]) / (ops().x[m][t] - ops().x[m][q]);
+            b *= (1.0 - ops().x[m][q]) / (ops().x[m][t] - ops().x[m][q]);
+        }
+        p.lm[t] = R(a);
+        p.lp[t] = R(b);
+    }
     const int h = m / 2;
     for (int i = 0; i <= h && i < hfb::kMaxH; ++i) {
         for (int t = 0; t < h; ++t) {
@@ -237,28 +247,32 @@ hfb::FrParams<R> make_fr_params(const hf_problem* pr, const hf_mesh* mesh, const
 
 // Resolve + launch (dry: describe only).  ws only for the unfused method.
 int dispatch(const hf_problem* pr, const void* u, void* out, void* ws, cudaStream_t st, hfb::KInfo* info, bool dry,
-             int force_method = -1, int force_variant = -1) {
+             int force_method = -1, int force_variant = -1, bool faces = false, void* uf = nullptr) {
     int method, variant;
     select_method(pr, &method, &variant);
     if (force_method >= 0) method = force_method;
     if (force_variant >= 0) variant = force_variant;
     const bool src = pr->with_source != 0;
     int rc;
+    if (faces && method != HF_METHOD_LINES) return hfb::kUnsupported;
     if (pr->precision == HF_FP32) {
-        const auto prm = make_params<float>(pr, u, out, ws);
+        auto prm = make_params<float>(pr, u, out, ws);
+        prm.uf = static_cast<float*>(uf);
         if (method == HF_METHOD_PLANAR) rc = hfb::planar_f32(pr->p, src, prm, st, info, dry);
         else if (method == HF_METHOD_PLANAR_MANAGED) rc = hfb::planar_managed_f32(pr->p, src, prm, st, info, dry);
         else if (method == HF_METHOD_UNFUSED) rc = hfb::unfused_f32(pr->d, pr->p, src, prm, st, info, dry);
-        else rc = pr->d == 3 ? hfb::lines_f32_d3(pr->p, variant, src, prm, st, info, dry)
-                             : hfb::lines_f32_d2(pr->p, variant, src, prm, st, info, dry);
+        else rc = pr->d == 3 ? hfb::lines_f32_d3(pr->p, variant, src, prm, st, info, dry, faces)
+                             : hfb::lines_f32_d2(pr->p, variant, src, prm, st, info, dry, faces);
     } else {
-        const auto prm = make_params<double>(pr, u, out, ws);
+        auto prm = make_params<double>(pr, u, out, ws);
+        prm.uf = static_cast<double*>(uf);
         if (method == HF_METHOD_PLANAR) rc = hfb::planar_f64(pr->p, src, prm, st, info, dry);
         else if (method == HF_METHOD_PLANAR_MANAGED) rc = hfb::planar_managed_f64(pr->p, src, prm, st, info, dry);
         else if (method == HF_METHOD_UNFUSED) rc = hfb::unfused_f64(pr->d, pr->p, src, prm, st, info, dry);
-        else rc = pr->d == 3 ? hfb::lines_f64_d3(pr->p, variant, src, prm, st, info, dry)
-                             : hfb::lines_f64_d2(pr->p, variant, src, prm, st, info, dry);
+        else rc = pr->d == 3 ? hfb::lines_f64_d3(pr->p, variant, src, prm, st, info, dry, faces)
+                             : hfb::lines_f64_d2(pr->p, variant, src, prm, st, info, dry, faces);
     }
+    if (faces && rc == hfb::kUnsupported) return rc;  // caller falls back to the separate stage-1 kernel
     if (rc == hfb::kUnsupported) return fail(HF_EINVAL, "no kernel for this (method, d, p, variant)");
     if (rc != 0) return cuda_fail(cudaError_t(rc), "kernel launch");
     return HF_OK;
@@ -474,8 +488,19 @@ int hf_fr_residual(const hf_problem* pr, const int* dims, const void* u_dev, voi
     ms.layer = 0;
     if (pr && int64_t(ms.dims[0]) * ms.dims[1] * ms.dims[2] != pr->n_elem)
         return fail(HF_EINVAL, "hf_fr_residual: n_elem must equal the mesh's element count");
-    if (int rc = hf_fused_divergence(pr, u_dev, divf_dev, stream)) return rc;  // stages 2+3+6
-    if (int rc = hf_fr_project(pr, u_dev, uf_dev, stream)) return rc;        // stage 1
+    if (int rc = validate(pr)) return rc;
+    if (pr->n_elem > 0 && (!u_dev || !uf_dev || !divf_dev)) return fail(HF_EINVAL, "hf_fr_residual: null buffer");
+    if (u_dev == divf_dev && pr->n_elem > 0) return fail(HF_EINVAL, "hf_fr_residual: in-place not supported");
+    // stages 1+2+3+6 in one pass of the lines kernel (faces written beside the divergence);
+    // the separate stage-1 kernel where no fused form is built (e.g. a planar selection)
+    const int rc = dispatch(pr, u_dev, divf_dev, nullptr, static_cast<cudaStream_t>(stream), nullptr, false, -1, -1,
+                            true, uf_dev);
+    if (rc == hfb::kUnsupported) {
+        if (int r2 = hf_fused_divergence(pr, u_dev, divf_dev, stream)) return r2;  // stages 2+3+6
+        if (int r2 = hf_fr_project(pr, u_dev, uf_dev, stream)) return r2;         // stage 1
+    } else if (rc != HF_OK) {
+        return rc;
+    }
     return hf_fr_correct(pr, &ms, uf_dev, nullptr, nullptr, divf_dev, stream);  // stages 4+5
 }
 

@@ -34,10 +34,12 @@ struct Params {
     R jac[3];            // constant per-axis metric (oracle.hpp:47)
     R jac_invT[3];       // jac[a] / T : gradient-row scale
     R xg[kMaxM];         // Gauss-Legendre nodes (mapped elements: the reference point of each node)
+    R lm[kMaxM], lp[kMaxM];  // Lagrange basis at xi = -1, +1 (FR stage 1 fused into the lines kernel)
     const R* __restrict__ u;  // input field, AoSoA (layout.hpp:128-134)
     R* __restrict__ out;      // divergence, same layout
     R* __restrict__ ws;       // unfused only: flux workspace
     const R* __restrict__ geo;  // mapped elements only: 2^d corners per element (hf_mapped.cuh)
+    R* __restrict__ uf;         // lines kernel with FACES: the FR face array (stage 1) written beside the divergence
     long long n_elem;
     long long group_words;    // group * m^d * n_v
     long long total_words;    // n_groups * group_words (allocation size of u and out)
@@ -46,6 +48,24 @@ struct Params {
     int group;
     int fast_ok;              // host-verified: bulk-copy alignment holds for full chunks
 };
+
+// FR face array (stage 1 output, hf_fr.cuh): word of (element e, axis a, side s,
+// line l = the line's transverse indices, variable v), AoSoA with the field's group.
+__device__ __forceinline__ long long face_word(int dim, int m, long long group, long long e, int a, int s, int l,
+                                               int v) {
+    const int nv = 1 + dim + dim * dim;
+    const int L = dim == 3 ? m * m : m;
+    return (e / group) * group * 2 * dim * L * nv + e % group + group * (l + (long long)L * (s + 2 * (a + dim * v)));
+}
+
+// line l of axis a, point t -> point index i + m j + m^2 k
+template <int DIM, int M>
+__device__ __forceinline__ int fr_line_point(int a, int l, int t) {
+    const int t0 = l % M, t1 = l / M;
+    if (a == 0) return t + M * t0 + M * M * (DIM == 3 ? t1 : 0);
+    if (a == 1) return t0 + M * t + M * M * (DIM == 3 ? t1 : 0);
+    return t0 + M * t1 + M * M * t;
+}
 
 // ---------------------------------------------------------------------------------------------
 // PTX: mbarrier + cp.async.bulk (SASS UBLKCP / SYNCS.*)

@@ -7,64 +7,79 @@
 
 namespace hfb {
 
+template <class R, int DIM, int M, int VARIANT, bool FACES>
+int lines_variant_f(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
+    constexpr int NE = variant_ne<R, DIM, M, VARIANT>();
+    if constexpr (is_pipe_variant<VARIANT>()) {
+        constexpr int ST = pipe_stages<VARIANT>();
+        constexpr int GR = pipe_groups<VARIANT>();
+        return src ? int(launch_lines_pipe<R, DIM, M, NE, ST, GR, true, FACES>(prm, st, info, dry))
+                   : int(launch_lines_pipe<R, DIM, M, NE, ST, GR, false, FACES>(prm, st, info, dry));
+    } else {
+        constexpr int LPT = lines_per_thread<VARIANT>();
+        return src ? int(launch_lines<R, DIM, M, NE, true, LPT, FACES>(prm, st, info, dry))
+                   : int(launch_lines<R, DIM, M, NE, false, LPT, FACES>(prm, st, info, dry));
+    }
+}
+
+// faces: FR stage 1 fused in (lines_sweeps<FACES>); instantiated for the selected
+// variant only (and every variant in the tuning build).
 template <class R, int DIM, int M, int VARIANT>
-int lines_variant(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
+int lines_variant(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry, bool faces = false) {
     constexpr int NE = variant_ne<R, DIM, M, VARIANT>();
     if constexpr (NE == 0 || !variant_built<R, DIM, M, VARIANT>()) {
         return kUnsupported;
-    } else if constexpr (is_pipe_variant<VARIANT>()) {
-        constexpr int ST = pipe_stages<VARIANT>();
-        constexpr int GR = pipe_groups<VARIANT>();
-        if constexpr (PipeShape<R, DIM, M, NE, ST, GR>::SMEM > size_t(kMaxSmemPerCta) ||
-                      PipeShape<R, DIM, M, NE, ST, GR>::BS > 1024) {
-            return kUnsupported;
-        } else {
-            return src ? int(launch_lines_pipe<R, DIM, M, NE, ST, GR, true>(prm, st, info, dry))
-                       : int(launch_lines_pipe<R, DIM, M, NE, ST, GR, false>(prm, st, info, dry));
-        }
-    } else if constexpr (LinesShape<R, DIM, M, NE>::SMEM > size_t(kMaxSmemPerCta) ||
-                         LinesShape<R, DIM, M, NE, lines_per_thread<VARIANT>()>::BS > 1024) {
+    } else if constexpr (is_pipe_variant<VARIANT>() &&
+                         (PipeShape<R, DIM, M, NE, pipe_stages<VARIANT>(), pipe_groups<VARIANT>()>::SMEM >
+                              size_t(kMaxSmemPerCta) ||
+                          PipeShape<R, DIM, M, NE, pipe_stages<VARIANT>(), pipe_groups<VARIANT>()>::BS > 1024)) {
+        return kUnsupported;
+    } else if constexpr (!is_pipe_variant<VARIANT>() &&
+                         (LinesShape<R, DIM, M, NE>::SMEM > size_t(kMaxSmemPerCta) ||
+                          LinesShape<R, DIM, M, NE, lines_per_thread<VARIANT>()>::BS > 1024)) {
         return kUnsupported;
     } else {
-        constexpr int LPT = lines_per_thread<VARIANT>();
-        return src ? int(launch_lines<R, DIM, M, NE, true, LPT>(prm, st, info, dry))
-                   : int(launch_lines<R, DIM, M, NE, false, LPT>(prm, st, info, dry));
+        if (!faces) return lines_variant_f<R, DIM, M, VARIANT, false>(src, prm, st, info, dry);
+        if constexpr (variant_faces_built<R, DIM, M, VARIANT>())
+            return lines_variant_f<R, DIM, M, VARIANT, true>(src, prm, st, info, dry);
+        return kUnsupported;
     }
 }
 
 // Variants [VLO, VHI] of one order (the instantiation units split the variant
 // range so that the template instances compile in parallel).
 template <class R, int DIM, int M, int VLO, int VHI, int V = VLO>
-int lines_m(int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
-    if (variant == V) return lines_variant<R, DIM, M, V>(src, prm, st, info, dry);
-    if constexpr (V < VHI) return lines_m<R, DIM, M, VLO, VHI, V + 1>(variant, src, prm, st, info, dry);
+int lines_m(int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry, bool faces) {
+    if (variant == V) return lines_variant<R, DIM, M, V>(src, prm, st, info, dry, faces);
+    if constexpr (V < VHI) return lines_m<R, DIM, M, VLO, VHI, V + 1>(variant, src, prm, st, info, dry, faces);
     return kUnsupported;
 }
 
 template <class R, int DIM, int VLO, int VHI>
-int run_lines_range(int p, int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
+int run_lines_range(int p, int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry,
+                    bool faces) {
     if (variant < VLO || variant > VHI) return kUnsupported;
     if constexpr (DIM == 3) {
         switch (p) {
-            case 1: return lines_m<R, 3, 2, VLO, VHI>(variant, src, prm, st, info, dry);
-            case 2: return lines_m<R, 3, 3, VLO, VHI>(variant, src, prm, st, info, dry);
-            case 3: return lines_m<R, 3, 4, VLO, VHI>(variant, src, prm, st, info, dry);
-            case 4: return lines_m<R, 3, 5, VLO, VHI>(variant, src, prm, st, info, dry);
-            case 5: return lines_m<R, 3, 6, VLO, VHI>(variant, src, prm, st, info, dry);
-            case 6: return lines_m<R, 3, 7, VLO, VHI>(variant, src, prm, st, info, dry);
-            case 7: return lines_m<R, 3, 8, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 1: return lines_m<R, 3, 2, VLO, VHI>(variant, src, prm, st, info, dry, faces);
+            case 2: return lines_m<R, 3, 3, VLO, VHI>(variant, src, prm, st, info, dry, faces);
+            case 3: return lines_m<R, 3, 4, VLO, VHI>(variant, src, prm, st, info, dry, faces);
+            case 4: return lines_m<R, 3, 5, VLO, VHI>(variant, src, prm, st, info, dry, faces);
+            case 5: return lines_m<R, 3, 6, VLO, VHI>(variant, src, prm, st, info, dry, faces);
+            case 6: return lines_m<R, 3, 7, VLO, VHI>(variant, src, prm, st, info, dry, faces);
+            case 7: return lines_m<R, 3, 8, VLO, VHI>(variant, src, prm, st, info, dry, faces);
             default: return kUnsupported;
         }
     } else {
         switch (p) {
-            case 1: return lines_m<R, 2, 2, VLO, VHI>(variant, src, prm, st, info, dry);
-            case 2: return lines_m<R, 2, 3, VLO, VHI>(variant, src, prm, st, info, dry);
-            case 3: return lines_m<R, 2, 4, VLO, VHI>(variant, src, prm, st, info, dry);
-            case 4: return lines_m<R, 2, 5, VLO, VHI>(variant, src, prm, st, info, dry);
-            case 5: return lines_m<R, 2, 6, VLO, VHI>(variant, src, prm, st, info, dry);
-            case 6: return lines_m<R, 2, 7, VLO, VHI>(variant, src, prm, st, info, dry);
-            case 7: return lines_m<R, 2, 8, VLO, VHI>(variant, src, prm, st, info, dry);
-            case 8: return lines_m<R, 2, 9, VLO, VHI>(variant, src, prm, st, info, dry);
+            case 1: return lines_m<R, 2, 2, VLO, VHI>(variant, src, prm, st, info, dry, faces);
+            case 2: return lines_m<R, 2, 3, VLO, VHI>(variant, src, prm, st, info, dry, faces);
+            case 3: return lines_m<R, 2, 4, VLO, VHI>(variant, src, prm, st, info, dry, faces);
+            case 4: return lines_m<R, 2, 5, VLO, VHI>(variant, src, prm, st, info, dry, faces);
+            case 5: return lines_m<R, 2, 6, VLO, VHI>(variant, src, prm, st, info, dry, faces);
+            case 6: return lines_m<R, 2, 7, VLO, VHI>(variant, src, prm, st, info, dry, faces);
+            case 7: return lines_m<R, 2, 8, VLO, VHI>(variant, src, prm, st, info, dry, faces);
+            case 8: return lines_m<R, 2, 9, VLO, VHI>(variant, src, prm, st, info, dry, faces);
             default: return kUnsupported;
         }
     }
@@ -176,13 +191,13 @@ int run_unfused_impl(int d, int p, bool src, const Params<R>& prm, cudaStream_t 
 }
 
 // Entry points defined in the instantiation units (lines: variants 0-9 in *_lo, 10-15 in *_hi).
-#define HF_LINES_DECL(NAME, R)                                                                      \
-    int NAME##_lo(int p, int variant, bool src, const Params<R>&, cudaStream_t, KInfo*, bool);       \
-    int NAME##_hi(int p, int variant, bool src, const Params<R>&, cudaStream_t, KInfo*, bool);       \
-    inline int NAME(int p, int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, \
-                    bool dry) {                                                                     \
-        return variant < 10 ? NAME##_lo(p, variant, src, prm, st, info, dry)                        \
-                            : NAME##_hi(p, variant, src, prm, st, info, dry);                       \
+#define HF_LINES_DECL(NAME, R)                                                                        \
+    int NAME##_lo(int p, int variant, bool src, const Params<R>&, cudaStream_t, KInfo*, bool, bool);   \
+    int NAME##_hi(int p, int variant, bool src, const Params<R>&, cudaStream_t, KInfo*, bool, bool);   \
+    inline int NAME(int p, int variant, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info,   \
+                    bool dry, bool faces = false) {                                                   \
+        return variant < 10 ? NAME##_lo(p, variant, src, prm, st, info, dry, faces)                   \
+                            : NAME##_hi(p, variant, src, prm, st, info, dry, faces);                  \
     }
 HF_LINES_DECL(lines_f32_d3, float)
 HF_LINES_DECL(lines_f64_d3, double)

@@ -47,22 +47,6 @@ __host__ __device__ constexpr int fr_lines() {
     return ipow_c(M, DIM - 1);
 }
 
-__device__ __forceinline__ long long face_word(int dim, int m, long long group, long long e, int a, int s, int l,
-                                               int v) {
-    const int nv = 1 + dim + dim * dim;
-    const int L = dim == 3 ? m * m : m;
-    return (e / group) * group * 2 * dim * L * nv + e % group + group * (l + (long long)L * (s + 2 * (a + dim * v)));
-}
-
-// line l of axis a, point t -> point index i + m j + m^2 k
-template <int DIM, int M>
-__device__ __forceinline__ int fr_line_point(int a, int l, int t) {
-    const int t0 = l % M, t1 = l / M;
-    if (a == 0) return t + M * t0 + M * M * (DIM == 3 ? t1 : 0);
-    if (a == 1) return t0 + M * t + M * M * (DIM == 3 ? t1 : 0);
-    return t0 + M * t1 + M * M * t;
-}
-
 // ---------------------------------------------------------------------------------------------
 // stage 1
 // ---------------------------------------------------------------------------------------------

@@ -2,7 +2,7 @@
 #include "hf_dispatch.cuh"
 namespace hfb {
 int lines_f64_d2_lo(int p, int variant, bool src, const Params<double>& prm, cudaStream_t st, KInfo* info,
-                     bool dry) {
-    return run_lines_range<double, 2, 0, 9>(p, variant, src, prm, st, info, dry);
+                     bool dry, bool faces) {
+    return run_lines_range<double, 2, 0, 9>(p, variant, src, prm, st, info, dry, faces);
 }
 }  // namespace hfb

@@ -78,6 +78,19 @@ constexpr SelRow kSelect[] = {
 // CTA), 3 (TMA ring) and 10 (grouped TMA ring), so that every kernel form stays
 // parity-tested; the tuning build (make tuning, -DHF_TUNING) carries all of them
 // for tools/select_methods.py.
+// The FACES (fused FR stage 1) form: the selected variant of each configuration.
+template <class R, int DIM, int M, int VARIANT>
+constexpr bool variant_faces_built() {
+#ifdef HF_TUNING
+    return VARIANT == 0 || VARIANT == 3;
+#else
+    for (const SelRow& r : kSelect)
+        if (r.d == DIM && r.p == M - 1 && r.prec == (sizeof(R) == 8 ? 1 : 0) && r.method == 2 && r.variant == VARIANT)
+            return true;
+    return false;
+#endif
+}
+
 template <class R, int DIM, int M, int VARIANT>
 constexpr bool variant_built() {
 #ifdef HF_TUNING
@@ -177,10 +190,10 @@ inline void fill_regs(K kernel, KInfo* info) {
 inline const char* prec_name(size_t w) { return w == 4 ? "fp32" : "fp64"; }
 
 // Launch (or, with dry = true, only describe) the lines kernel.
-template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1>
+template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false>
 cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
     using S = LinesShape<R, DIM, M, NE, LPT>;
-    auto kernel = hf_lines_kernel<R, DIM, M, NE, SRC, LPT>;
+    auto kernel = hf_lines_kernel<R, DIM, M, NE, SRC, LPT, FACES>;
     const long long grid = (p.n_elem + NE - 1) / NE;
     const bool fast_layout = bulk_layout<R, NE>(p.group);
     if (info) {
@@ -218,11 +231,11 @@ inline int num_sms() {
 }
 
 // Persistent pipelined lines kernel over the whole chunks, guarded tail through hf_lines_kernel.
-template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC>
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES = false>
 cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
     using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS>;
     using L = LinesShape<R, DIM, M, NE>;
-    auto kernel = hf_lines_pipe_kernel<R, DIM, M, NE, STAGES, GROUPS, SRC>;
+    auto kernel = hf_lines_pipe_kernel<R, DIM, M, NE, STAGES, GROUPS, SRC, FACES>;
     const bool fast_layout = bulk_layout<R, NE>(p.group);
     long long n_full = p.n_elem / NE;
     // contiguous chunks load a 16-byte superset: keep the allocation's last chunk
@@ -271,7 +284,7 @@ cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dr
     }
     if (dry || p.n_elem == 0) return cudaSuccess;
     p.fast_ok = fast_layout && aligned16(p.u) && aligned16(p.out);
-    if (!p.fast_ok || n_full == 0) return launch_lines<R, DIM, M, NE, SRC>(p, st, nullptr, false);
+    if (!p.fast_ok || n_full == 0) return launch_lines<R, DIM, M, NE, SRC, 1, FACES>(p, st, nullptr, false);
     p.chunk0 = 0;
     p.n_chunks = n_full;
     kernel<<<dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st>>>(p);
@@ -279,7 +292,7 @@ cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dr
     if (e != cudaSuccess) return e;
     const long long n_chunks = (p.n_elem + NE - 1) / NE;
     if (n_full < n_chunks) {  // the partial (or allocation-final) chunk(s)
-        auto tail = hf_lines_kernel<R, DIM, M, NE, SRC>;
+        auto tail = hf_lines_kernel<R, DIM, M, NE, SRC, 1, FACES>;
         if (int e2 = set_smem_attr(tail, L::SMEM)) return cudaError_t(e2);
         p.chunk0 = n_full;
         tail<<<unsigned(n_chunks - n_full), L::BS, L::SMEM, st>>>(p);

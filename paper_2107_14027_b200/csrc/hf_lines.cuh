@@ -284,8 +284,43 @@ __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ a
 // costs ~30 registers and ~10 % of HBM throughput, measured).  BAR: 0 = the
 // whole CTA (__syncthreads), k > 0 = the NTHR threads of one consumer group
 // (named barrier k), -1 = named barrier `bar_id` (runtime).
-template <class R, int DIM, int M, int NE, bool SRC, int HEADB, int BAR, int NTHR>
-__device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const Params<R>& p, int t, int bar_id = 0) {
+// FACES: FR stage 1 fused in (hf_fr.cuh): before the sweeps overwrite the staged
+// chunk, every a-line of every variable is extrapolated to xi_a = -1, +1 and
+// written to p.uf -- the face projection without a second read of the field.
+template <class R, int DIM, int M, int NE>
+__device__ __forceinline__ void lines_project_faces(const R* __restrict__ s, const Params<R>& p, long long E0, int t,
+                                                    int nthr) {
+    constexpr int NP = ipow_c(M, DIM), NV = n_vars_c(DIM), LN = ipow_c(M, DIM - 1);
+    for (int task = t; task < NE * LN * DIM; task += nthr) {
+        const int el = task % NE;
+        const int l = (task / NE) % LN;
+        const int a = task / (NE * LN);
+        const long long e = E0 + el;
+        if (e >= p.n_elem) continue;
+        int pt[M];
+#pragma unroll
+        for (int q = 0; q < M; ++q) pt[q] = el + NE * fr_line_point<DIM, M>(a, l, q);
+        const long long ge = e / p.group;
+        R* ub = p.uf + ge * p.group * 2 * DIM * LN * NV + (e - ge * p.group) + (long long)p.group * (l + LN * 2 * a);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            R sm = R(0), sp = R(0);
+#pragma unroll
+            for (int q = 0; q < M; ++q) {
+                const R u = s[pt[q] + NE * NP * v];
+                sm = fma(p.lm[q], u, sm);
+                sp = fma(p.lp[q], u, sp);
+            }
+            R* w = ub + (long long)p.group * LN * 2 * DIM * v;  // face_word(e, a, s, l, v)
+            w[0] = sm;
+            w[(long long)p.group * LN] = sp;
+        }
+    }
+}
+
+template <class R, int DIM, int M, int NE, bool SRC, int HEADB, int BAR, int NTHR, bool FACES = false>
+__device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const Params<R>& p, int t, int bar_id = 0,
+                                             long long E0 = 0) {
     using S = LinesShape<R, DIM, M, NE>;
     R* s = reinterpret_cast<R*>(buf + HEADB);
 #ifdef HF_IO_ONLY  // measurement build: chunk traffic only, no sweeps (tools/gpu_ab_io.sh)
@@ -311,6 +346,10 @@ __device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const P
     using I0 = std::integral_constant<int, 0>;
     using I1 = std::integral_constant<int, 1>;
     using I2 = std::integral_constant<int, 2>;
+    if constexpr (FACES) {
+        lines_project_faces<R, DIM, M, NE>(s, p, E0, t, NTHR);
+        sync();  // every line is read before sweep 0 writes in place
+    }
     if constexpr (DIM == 3) {
         sweep(I0{}, I0{});
         sync();
@@ -326,25 +365,25 @@ __device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const P
 
 // Runtime head (bytes, a multiple of sizeof(R), < 16) -> compile-time HEADB.
 // Chunks whose byte size is a multiple of 16 always start aligned: one instance.
-template <class R, int DIM, int M, int NE, bool SRC, int BAR, int NTHR>
+template <class R, int DIM, int M, int NE, bool SRC, int BAR, int NTHR, bool FACES = false>
 __device__ __forceinline__ void lines_sweeps_at(unsigned char* buf, int head, R* acc, const Params<R>& p, int t,
-                                                int bar_id = 0) {
+                                                int bar_id = 0, long long E0 = 0) {
     if constexpr (LinesShape<R, DIM, M, NE>::IN_BYTES % 16 == 0) {
-        lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR>(buf, acc, p, t, bar_id);
+        lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES>(buf, acc, p, t, bar_id, E0);
     } else if constexpr (sizeof(R) == 8) {
-        if (head == 0) lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR>(buf, acc, p, t, bar_id);
-        else lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR>(buf, acc, p, t, bar_id);
+        if (head == 0) lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES>(buf, acc, p, t, bar_id, E0);
+        else lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR, FACES>(buf, acc, p, t, bar_id, E0);
     } else {
         switch (head) {
-            case 0: lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR>(buf, acc, p, t, bar_id); break;
-            case 4: lines_sweeps<R, DIM, M, NE, SRC, 4, BAR, NTHR>(buf, acc, p, t, bar_id); break;
-            case 8: lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR>(buf, acc, p, t, bar_id); break;
-            default: lines_sweeps<R, DIM, M, NE, SRC, 12, BAR, NTHR>(buf, acc, p, t, bar_id); break;
+            case 0: lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES>(buf, acc, p, t, bar_id, E0); break;
+            case 4: lines_sweeps<R, DIM, M, NE, SRC, 4, BAR, NTHR, FACES>(buf, acc, p, t, bar_id, E0); break;
+            case 8: lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR, FACES>(buf, acc, p, t, bar_id, E0); break;
+            default: lines_sweeps<R, DIM, M, NE, SRC, 12, BAR, NTHR, FACES>(buf, acc, p, t, bar_id, E0); break;
         }
     }
 }
 
-template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1>
+template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false>
 __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT>::BS)
     hf_lines_kernel(const __grid_constant__ Params<R> p) {
     using S = LinesShape<R, DIM, M, NE, LPT>;
@@ -394,7 +433,7 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT>::BS)
     }
 
     // ---------------- d sweeps ----------------
-    lines_sweeps_at<R, DIM, M, NE, SRC, 0, BS>(buf, head, acc, p, tid);
+    lines_sweeps_at<R, DIM, M, NE, SRC, 0, BS, FACES>(buf, head, acc, p, tid, 0, E0);
 
     // ---------------- write the finished chunk ----------------
     if (fast) {

@@ -55,7 +55,7 @@ struct PipeShape {
 // accumulator region) is a runtime offset from the __shared__ window, so every
 // group runs the same code -- one copy of the sweeps per stage, not per
 // (group, stage), which keeps the kernel inside the instruction cache.
-template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC>
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES>
 __device__ __forceinline__ void pipe_consume(unsigned char* smem_raw, uint64_t* full, uint64_t* computed,
                                              const Params<R>& p, long long count, long long first, long long step,
                                              int g, int ct) {
@@ -79,11 +79,11 @@ __device__ __forceinline__ void pipe_consume(unsigned char* smem_raw, uint64_t* 
             unsigned char* buf = gbuf + size_t(j) * S::STAGE_BYTES;
             mbar_wait_parity(&full[s], ph);
             if constexpr (GROUPS == 1)
-                lines_sweeps_at<R, DIM, M, NE, SRC, 1, S::NCONS>(buf, IO::head_bytes(p.u + cb, contiguous), acc, p,
-                                                                 ct);
+                lines_sweeps_at<R, DIM, M, NE, SRC, 1, S::NCONS, FACES>(buf, IO::head_bytes(p.u + cb, contiguous),
+                                                                        acc, p, ct, 0, E0);
             else
-                lines_sweeps_at<R, DIM, M, NE, SRC, -1, S::NCONS>(buf, IO::head_bytes(p.u + cb, contiguous), acc,
-                                                                  p, ct, 1 + g);
+                lines_sweeps_at<R, DIM, M, NE, SRC, -1, S::NCONS, FACES>(buf, IO::head_bytes(p.u + cb, contiguous),
+                                                                         acc, p, ct, 1 + g, E0);
             fence_proxy_async_smem();
             named_bar_sync(1 + g, S::NCONS);
             if (ct == 0) mbar_arrive(&computed[s]);
@@ -91,7 +91,7 @@ __device__ __forceinline__ void pipe_consume(unsigned char* smem_raw, uint64_t* 
     }
 }
 
-template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC>
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES = false>
 __global__ void __launch_bounds__(PipeShape<R, DIM, M, NE, STAGES, GROUPS>::BS)
     hf_lines_pipe_kernel(const __grid_constant__ Params<R> p) {
     using L = LinesShape<R, DIM, M, NE>;
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(PipeShape<R, DIM, M, NE, STAGES, GROUPS>::BS)
     // ---------------- consumer groups ----------------
     const int g = (tid - 32) / S::NCONS;
     const int ct = (tid - 32) - g * S::NCONS;
-    pipe_consume<R, DIM, M, NE, STAGES, GROUPS, SRC>(smem_raw, full, computed, p, count, first, step, g, ct);
+    pipe_consume<R, DIM, M, NE, STAGES, GROUPS, SRC, FACES>(smem_raw, full, computed, p, count, first, step, g, ct);
 }
 
 }  // namespace hfb

@@ -137,3 +137,33 @@ def test_fr_slab_driver_single_rank(cuda):
     torch.cuda.synchronize()
     ref = O.fr_residual(d, p, dims, g, U, PAR.nu, PAR.zeta, PAR.T, (1.0, 1.0, 1.0), True)
     assert O.field_rel_error(d, p, n, g, out.cpu().numpy(), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+@pytest.mark.parametrize("d,p,dims,g", [(3, 1, (4, 4, 2), None), (3, 3, (3, 4, 4), None), (3, 6, (2, 3, 3), None),
+                                        (2, 4, (8, 6), None), (3, 4, (3, 2, 5), 1)])
+def test_fused_stage1_equals_separate_stages(cuda, d, p, dims, g, fp32):
+    """hf_fr_residual writes the faces from inside the fused kernel (FR stage 1
+    fused into the lines kernel's staged chunk): faces and residual bit-identical
+    to the separate hf_fused_divergence + hf_fr_project + hf_fr_correct path."""
+    import paper_2107_14027_b200 as hf
+    from paper_2107_14027_b200 import Precision
+    prec = Precision.fp32 if fp32 else Precision.fp64
+    if g is None:
+        g = hf.preferred_group(hf.make_problem(d, p, 1, 1, prec, PAR))
+    n = int(np.prod(dims))
+    U = O.random_field(d, p, n, g, fp32, 77)
+    pr = _pr(d, p, n, g, fp32, jac=(1.0, 0.5, 2.0), src=True)
+    dt = torch.float32 if fp32 else torch.float64
+    u = _t(U, fp32)
+    out_a = torch.zeros(hf.field_words(pr), dtype=dt, device="cuda")
+    uf_a = torch.zeros(hf.face_words(pr), dtype=dt, device="cuda")
+    hf.fr_residual_device(pr, dims, u, uf_a, out_a)
+    out_b = torch.zeros_like(out_a)
+    uf_b = torch.zeros_like(uf_a)
+    hf.fused_divergence_device(pr, u, out_b)
+    hf.fr_project_device(pr, u, uf_b)
+    hf.fr_correct_device(pr, hf.make_mesh(dims, d), uf_b, out_b)
+    torch.cuda.synchronize()
+    assert torch.equal(uf_a, uf_b)
+    assert torch.equal(out_a, out_b)
