@@ -157,12 +157,12 @@ struct FrCorrShape {
     static constexpr int NV = n_vars_c(DIM);
     static constexpr int LN = fr_lines<DIM, M>();
     static constexpr int TASKS = NE * DIM * LN;  // (element, axis, line)
-    // one thread per stage-4 task of an axis (NE * LN * 2); FP32 also at least one
-    // per two stage-5 points; whole warps, 64..256 (measured per precision,
-    // profiles/ext_r01c_fr.jsonl: FP64 p3-p6 0.55-0.74 -> 0.8-0.9 of the roofline)
+    // one thread per stage-4 task of an axis (NE * LN * 2: one round per axis, no
+    // tail before the barrier); FP32 also at least one per two stage-5 points;
+    // whole warps, 64..512
     static constexpr int T4 = NE * LN * 2, T5 = (NE * ipow_c(M, DIM) + 1) / 2;
     static constexpr int T = ((sizeof(R) == 8 || T4 > T5 ? T4 : T5) + 31) / 32 * 32;
-    static constexpr int BS = T < 64 ? 64 : (T > 256 ? 256 : T);
+    static constexpr int BS = T < 64 ? 64 : (T > 512 ? 512 : T);
     static constexpr size_t SMEM = size_t(TASKS) * 2 * NV * sizeof(R);  // jumps [v][s][a][l][el]
 };
 
@@ -204,17 +204,50 @@ __device__ __forceinline__ void fr_jump_rows(const R (&Uo)[n_vars_c(DIM)], const
     }
 }
 
+// Element-local word offset of the AoSoA layouts: (e/group)*group*words + e%group.
+__device__ __forceinline__ long long fr_elem_base(long long e, long long group, long long words_per_elem) {
+    const long long g = e / group;
+    return g * group * words_per_elem + (e - g * group);
+}
+
 template <class R, int DIM, int M, int NE>
 __global__ void __launch_bounds__(FrCorrShape<R, DIM, M, NE>::BS)
     hf_fr_correct_kernel(const __grid_constant__ Params<R> p, const __grid_constant__ FrParams<R> f) {
     using S = FrCorrShape<R, DIM, M, NE>;
-    constexpr int NV = S::NV, LN = S::LN, BS = S::BS, NP = ipow_c(M, DIM);
+    constexpr int NV = S::NV, LN = S::LN, BS = S::BS, NP = ipow_c(M, DIM), FW = 2 * DIM * LN * NV;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     R* jump = reinterpret_cast<R*>(smem_raw);  // [v][s][a][l][el]
+    // per element: own faces, the 2*DIM neighbour faces it meets (face (A, 1-s) of the
+    // neighbour across side s of axis A) and its output words -- the 64-bit mesh and
+    // group arithmetic once per element, 32-bit offsets in the task loops
+    __shared__ const R* own_f[NE];
+    __shared__ const R* nbr_f[NE][DIM][2];
+    __shared__ R* out_e[NE];
     auto jidx = [](int el, int a, int s, int l, int v) { return el + NE * (l + LN * (a + DIM * (s + 2 * v))); };
     const int tid = threadIdx.x;
     const long long E0 = static_cast<long long>(blockIdx.x) * NE;
-    const long long n_mesh = (long long)f.mesh.dims[0] * f.mesh.dims[1] * (DIM == 3 ? f.mesh.dims[2] : 1);
+    const int ne = int(p.n_elem - E0 < NE ? p.n_elem - E0 : NE);
+    const int G = int(p.group);
+    const int VS = G * 2 * DIM * LN;  // face word stride between variables
+
+    for (int q = tid; q < ne * 2 * DIM; q += BS) {
+        const int el = q % ne, side = q / ne, A = side >> 1, s = side & 1;
+        const long long e = E0 + el;
+        const long long eg = f.mesh.e_begin + e;
+        const long long nx = f.mesh.dims[0], ny = f.mesh.dims[1];
+        const long long n_mesh = nx * ny * (DIM == 3 ? f.mesh.dims[2] : 1);
+        long long c[3] = {eg % nx, (eg / nx) % ny, DIM == 3 ? eg / (nx * ny) : 0};
+        c[A] = (c[A] + (s ? 1 : -1) + f.mesh.dims[A]) % f.mesh.dims[A];
+        const long long en = c[0] + nx * (c[1] + ny * c[2]);
+        long long enl;
+        const R* nb = fr_faces_of(f, en, n_mesh, &enl);
+        nbr_f[el][A][s] = nb + fr_elem_base(enl, G, FW) + (long long)G * LN * (1 - s + 2 * A);
+        if (side == 0) {
+            own_f[el] = f.uf + fr_elem_base(e, G, FW);
+            out_e[el] = p.out + fr_elem_base(e, G, NP * NV);
+        }
+    }
+    __syncthreads();
 
     // ---- stage 4: common fluxes and jumps at both ends of every line (axis unrolled)
     auto stage4 = [&](auto a_tag) {
@@ -223,21 +256,14 @@ __global__ void __launch_bounds__(FrCorrShape<R, DIM, M, NE>::BS)
             const int el = task % NE;
             const int l = (task / NE) % LN;
             const int s = task / (NE * LN);
-            const long long e = E0 + el;  // local element
-            if (e >= p.n_elem) continue;
-            const long long eg = f.mesh.e_begin + e;
-            int c[3] = {int(eg % f.mesh.dims[0]), int((eg / f.mesh.dims[0]) % f.mesh.dims[1]),
-                        DIM == 3 ? int(eg / ((long long)f.mesh.dims[0] * f.mesh.dims[1])) : 0};
-            // side s = 1: this element's +A face vs the +A neighbour's -1 side; s = 0: the -A face
-            c[A] = (c[A] + (s ? 1 : -1) + f.mesh.dims[A]) % f.mesh.dims[A];
-            const long long en = c[0] + (long long)f.mesh.dims[0] * (c[1] + (long long)f.mesh.dims[1] * c[2]);
-            long long enl;
-            const R* nb = fr_faces_of(f, en, n_mesh, &enl);
+            if (el >= ne) continue;
+            const R* ow = own_f[el] + G * (l + LN * (s + 2 * A));
+            const R* nw = nbr_f[el][A][s] + G * l;
             R Uo[NV], Un[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
-                Uo[v] = f.uf[face_word(DIM, M, p.group, e, A, s, l, v)];
-                Un[v] = nb[face_word(DIM, M, p.group, enl, A, 1 - s, l, v)];
+                Uo[v] = ow[VS * v];
+                Un[v] = nw[VS * v];
             }
             const R lam = fmax(fr_wavespeed<R, DIM, A>(Uo, p), fr_wavespeed<R, DIM, A>(Un, p));
             fr_jump_rows<R, DIM, M, NE, A>(Uo, Un, lam, s, p, jump + jidx(el, A, s, l, 0));
@@ -248,19 +274,20 @@ __global__ void __launch_bounds__(FrCorrShape<R, DIM, M, NE>::BS)
     if constexpr (DIM == 3) stage4(std::integral_constant<int, 2>{});
     __syncthreads();
 
-    // ---- stage 5: corrections at every solution point, over the fused kernel's result
-    for (int task = tid; task < NE * NP; task += BS) {
+    // ---- stage 5: corrections at every solution point, over the fused kernel's result;
+    // two points per thread and iteration, all 2 n_v loads in flight before the updates
+    // (FP64 p4: 822 -> 753 us, FP32 p4: 434 -> 335 us)
+    auto point = [&](int task, R (&cur)[NV], bool load) {
         const int el = task % NE;
         const int pt = task / NE;
-        const long long e = E0 + el;
-        if (e >= p.n_elem) continue;
-        const int i = pt % M, j = (pt / M) % M, k = pt / (M * M);
-        const long long ge = e / p.group;
-        R* ob = p.out + ge * p.group_words + (e - ge * p.group);
-        // all n_v loads first (independent, in flight together), then the updates
-        R cur[NV];
+        if (task >= NE * NP || el >= ne) return;
+        R* ob = out_e[el] + G * pt;
+        if (load) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) cur[v] = ob[static_cast<long long>(p.group) * (pt + NP * v)];
+            for (int v = 0; v < NV; ++v) cur[v] = ob[G * NP * v];
+            return;
+        }
+        const int i = pt % M, j = (pt / M) % M, k = pt / (M * M);
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
             R corr = R(0);
@@ -270,8 +297,18 @@ __global__ void __launch_bounds__(FrCorrShape<R, DIM, M, NE>::BS)
                 const int l = a == 0 ? (j + M * k) : (a == 1 ? (i + M * k) : (i + M * j));
                 corr = fma(p.jac[a], fma(f.gl[t], jump[jidx(el, a, 0, l, v)], f.gr[t] * jump[jidx(el, a, 1, l, v)]), corr);
             }
-            ob[static_cast<long long>(p.group) * (pt + NP * v)] = cur[v] - corr;
+            ob[G * NP * v] = cur[v] - corr;
         }
+    };
+    // (one point per iteration for FP32 blocks above 256 threads: the second point's
+    // registers would cost a resident CTA -- p6 FP32: 92 registers, 336 -> 488 us)
+    constexpr int ILP = (sizeof(R) == 8 || BS <= 256) ? 2 : 1;
+    for (int task = tid; task < NE * NP; task += ILP * BS) {
+        R c0[NV], c1[NV];
+        point(task, c0, true);
+        if constexpr (ILP == 2) point(task + BS, c1, true);
+        point(task, c0, false);
+        if constexpr (ILP == 2) point(task + BS, c1, false);
     }
 }
 
@@ -291,10 +328,11 @@ constexpr int fr_proj_ne() {
     return ne;
 }
 
-template <class R, int DIM, int M>
+// power of two elements per CTA, <= KB kilobytes of jumps
+template <class R, int DIM, int M, int KB>
 constexpr int fr_corr_ne() {
     int ne = 32;
-    while (ne > 1 && size_t(ne) * DIM * ipow_c(M, DIM - 1) * 2 * n_vars_c(DIM) * sizeof(R) > size_t(48 * 1024)) ne /= 2;
+    while (ne > 1 && size_t(ne) * DIM * ipow_c(M, DIM - 1) * 2 * n_vars_c(DIM) * sizeof(R) > size_t(KB * 1024)) ne /= 2;
     return ne;
 }
 
@@ -324,16 +362,33 @@ int fr_project_dispatch(const Params<R>& prm, const FrParams<R>& fp, R* uf, cuda
     return fr_project_launch<R, DIM, M, NE>(prm, fp, uf, st);
 }
 
+template <class R, int DIM, int M, int NE>
+int fr_correct_launch(const Params<R>& prm, const FrParams<R>& fp, cudaStream_t st) {
+    using S = FrCorrShape<R, DIM, M, NE>;
+    auto kernel = hf_fr_correct_kernel<R, DIM, M, NE>;
+    if (S::SMEM > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM));
+        if (e != cudaSuccess) return int(e);
+    }
+    kernel<<<unsigned((prm.n_elem + NE - 1) / NE), S::BS, S::SMEM, st>>>(prm, fp);
+    return int(cudaGetLastError());
+}
+
 template <class R, int DIM, int M>
 int fr_stage(int which, const Params<R>& prm, const FrParams<R>& fp, R* uf, cudaStream_t st) {
     if (prm.n_elem == 0) return 0;
     if (which == 1) return fr_project_dispatch<R, DIM, M>(prm, fp, uf, st);
-    constexpr int NE = fr_corr_ne<R, DIM, M>();
-    using S = FrCorrShape<R, DIM, M, NE>;
-    auto kernel = hf_fr_correct_kernel<R, DIM, M, NE>;
-    kernel<<<unsigned((prm.n_elem + NE - 1) / NE), S::BS, S::SMEM, st>>>(prm, fp);
-    return int(cudaGetLastError());
+    // <= 48 KB of jumps per CTA (occupancy), or <= 64 KB when the AoSoA group is at
+    // least that many elements, so that stage 5's point loads cover whole 32-byte
+    // sectors (p6: FP32 486 -> 336 us, FP64 832 -> 744 us; a larger chunk with a
+    // smaller group only costs occupancy: p4 FP64 822 -> 978 us)
+    constexpr int NE1 = fr_corr_ne<R, DIM, M, 48>(), NE2 = fr_corr_ne<R, DIM, M, 64>();
+    if constexpr (NE2 > NE1) {
+        if (prm.group >= NE2) return fr_correct_launch<R, DIM, M, NE2>(prm, fp, st);
+    }
+    return fr_correct_launch<R, DIM, M, NE1>(prm, fp, st);
 }
+
 
 template <class R>
 int run_fr_impl(int which, int d, int p, const Params<R>& prm, const FrParams<R>& fp, R* uf, cudaStream_t st) {
