@@ -4,7 +4,11 @@ correction (stages 4+5), each with its algorithmic HBM bytes:
 
   fused    2 n_v m^d w per element
   project  n_v m^d w  read + F w written,      F = 2 d m^(d-1) n_v (face words per element)
-  correct  2 F w read (own + neighbour faces) + 2 n_v m^d w (read-modify-write of the residual)
+  correct  F w read + 2 n_v m^d w (read-modify-write of the residual); every face array
+           word is read twice (own side, neighbour side) but is unique data once, the
+           second read an L2 hit when the neighbour's chunk is close in launch order
+  residual (hf_fr_residual: the fused kernel writes the faces, then the correction)
+           2 n_v m^d w + F w  +  F w + 2 n_v m^d w
 
     python tools/bench_fr.py [--points 1e7] [--out gpurun_out/fr.jsonl]
 """
@@ -76,10 +80,10 @@ def main():
             row = {"d": d, "p": p, "precision": prec.name, "dims": dims, "points": n * m ** d,
                    "fused_us": round(t_div * 1e6, 1), "fused_GBps": round(2 * field / t_div / 1e9, 1),
                    "project_us": round(t_prj * 1e6, 1), "project_GBps": round((field + faces) / t_prj / 1e9, 1),
-                   "correct_us": round(t_cor * 1e6, 1), "correct_GBps": round((2 * faces + 2 * field) / t_cor / 1e9, 1),
+                   "correct_us": round(t_cor * 1e6, 1), "correct_GBps": round((faces + 2 * field) / t_cor / 1e9, 1),
                    "residual_us": round(t_all * 1e6, 1),
                    "residual_gdofs": round(n * m ** d / t_all / 1e9, 3),
-                   "residual_GBps_alg": round((2 * field + field + faces + 2 * faces + 2 * field) / t_all / 1e9, 1)}
+                   "residual_GBps_alg": round((4 * field + 2 * faces) / t_all / 1e9, 1)}
             print(json.dumps(row), flush=True)
             if fh:
                 fh.write(json.dumps(row) + "\n")
