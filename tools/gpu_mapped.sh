@@ -1,8 +1,11 @@
 #!/bin/bash
 # Mapped-element kernel: GPU parity, timing sweep beside the constant-Jacobian kernel, one ncu capture.
-O=gpurun_out/mapped; mkdir -p $O
+O=gpurun_out/${OUT:-mapped}; mkdir -p $O
+SPECS=${SPECS:-"3 3 fp64;3 6 fp64"}
+if [ -z "$PROF_ONLY" ]; then
 timeout 600 python -m pytest tests/test_gpu_mapped.py -q -x > $O/pytest.log 2>&1; tail -1 $O/pytest.log
 timeout 900 python tools/bench_mapped.py --out $O/bench_mapped.jsonl > /dev/null 2> $O/bench_mapped.err; echo "bench rc=$?"
+fi
 cat > $O/prof.py <<'PY'
 import sys, torch
 sys.path.insert(0, '.')
@@ -25,13 +28,13 @@ for _ in range(2):
     hf.fused_divergence_mapped_device(pr, u, geo, o)
 torch.cuda.synchronize()
 PY
-for spec in "3 3 fp64" "3 6 fp64"; do
+IFS=";" read -ra SPL <<< "$SPECS"
+for spec in "${SPL[@]}"; do
   set -- $spec
   out=$O/ncu_d$1p$2$3
   timeout 300 ncu --set full --import-source on --clock-control none -k regex:hf_mapped -s 1 -c 1 -o $out python $O/prof.py $1 $2 $3 > $out.log 2>&1
   ncu -i $out.ncu-rep --page raw --csv > ${out}_raw.csv 2>/dev/null
   ncu -i $out.ncu-rep --page source --csv > ${out}_src.csv 2>/dev/null
   ncu -i $out.ncu-rep --page details --csv > ${out}_details.csv 2>/dev/null
-  rm -f $out.ncu-rep
 done
 echo done
