@@ -139,7 +139,11 @@ HF_API int hf_mapped_kernel_info(const hf_problem* pr, hf_kernel_info* out);
  *                   |V_a| + sqrt(V_a^2 + zeta + nu/T)) and the DG correction
  *                   -sum_a jac_a (g_L' jump_(-a) + g_R' jump_(+a)) added in place
  *                   to divf_dev, which holds hf_fused_divergence's result;
- *   hf_fr_residual  the whole right-hand side on one device (2+3+6, 1, 4+5).
+ *   hf_fr_divergence_faces  stages 1+2+3+6 in one pass: the fused kernel also
+ *                   writes the faces from the chunk it has staged (the two
+ *                   kernels hf_fused_divergence + hf_fr_project where no fused
+ *                   form is built); bit-identical to them;
+ *   hf_fr_residual  the whole right-hand side on one device (1+2+3+6, then 4+5).
  * Face layout (AoSoA, the field's group, L = m^(d-1), l = transverse indices,
  * s = 0 at xi = -1, 1 at +1):
  *   word (e, a, s, l, v) = (e/group)*group*2*d*L*n_v + e%group + group*(l + L*(s + 2*(a + d*v))).
@@ -156,6 +160,7 @@ HF_API int64_t hf_face_words(const hf_problem* pr);
 HF_API int hf_fr_project(const hf_problem* pr, const void* u_dev, void* uf_dev, void* stream);
 HF_API int hf_fr_correct(const hf_problem* pr, const hf_mesh* mesh, const void* uf_dev, const void* ghost_lo,
                          const void* ghost_hi, void* divf_dev, void* stream);
+HF_API int hf_fr_divergence_faces(const hf_problem* pr, const void* u_dev, void* uf_dev, void* divf_dev, void* stream);
 HF_API int hf_fr_residual(const hf_problem* pr, const int* dims, const void* u_dev, void* uf_dev, void* divf_dev,
                           void* stream);
 

@@ -25,6 +25,7 @@ from .hexfuse import (  # noqa: F401
     fused_divergence_mapped_device,
     face_words,
     fr_correct_device,
+    fr_divergence_faces_device,
     fr_project_device,
     fr_residual_device,
     make_mesh,

@@ -54,7 +54,7 @@ EXPORTED = [
     "hf_fused_divergence", "hf_unfused_workspace_bytes", "hf_unfused_divergence", "hf_context_create",
     "hf_context_destroy", "hf_fused_divergence_host", "hf_partition", "hf_last_error", "hf_version",
     "hf_geometry_words", "hf_fused_divergence_mapped", "hf_mapped_kernel_info",
-    "hf_face_words", "hf_fr_project", "hf_fr_correct", "hf_fr_residual",
+    "hf_face_words", "hf_fr_project", "hf_fr_correct", "hf_fr_divergence_faces", "hf_fr_residual",
     "hf_ipc_handle", "hf_ipc_open", "hf_ipc_close",
 ]
 
@@ -118,6 +118,7 @@ def load() -> C.CDLL:
     L.hf_face_words.restype = C.c_int64
     L.hf_fr_project.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p]
     L.hf_fr_correct.argtypes = [P, C.POINTER(hf_mesh), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.hf_fr_divergence_faces.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     L.hf_fr_residual.argtypes = [P, C.POINTER(C.c_int), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     L.hf_ipc_handle.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]
     L.hf_ipc_open.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]

@@ -476,6 +476,22 @@ int hf_fr_correct(const hf_problem* pr, const hf_mesh* mesh, const void* uf_dev,
     return HF_OK;
 }
 
+int hf_fr_divergence_faces(const hf_problem* pr, const void* u_dev, void* uf_dev, void* divf_dev, void* stream) {
+    if (int rc = validate(pr)) return rc;
+    if (pr->n_elem > 0 && (!u_dev || !uf_dev || !divf_dev))
+        return fail(HF_EINVAL, "hf_fr_divergence_faces: null buffer");
+    if (u_dev == divf_dev && pr->n_elem > 0) return fail(HF_EINVAL, "hf_fr_divergence_faces: in-place not supported");
+    // stages 1+2+3+6 in one pass of the lines kernel (faces written beside the divergence);
+    // the separate stage-1 kernel where no fused form is built (e.g. a planar selection)
+    const int rc = dispatch(pr, u_dev, divf_dev, nullptr, static_cast<cudaStream_t>(stream), nullptr, false, -1, -1,
+                            true, uf_dev);
+    if (rc == hfb::kUnsupported) {
+        if (int r2 = hf_fused_divergence(pr, u_dev, divf_dev, stream)) return r2;  // stages 2+3+6
+        return hf_fr_project(pr, u_dev, uf_dev, stream);                         // stage 1
+    }
+    return rc;
+}
+
 int hf_fr_residual(const hf_problem* pr, const int* dims, const void* u_dev, void* uf_dev, void* divf_dev,
                    void* stream) {
     if (!dims) return fail(HF_EINVAL, "hf_fr_residual: null dims");
@@ -491,16 +507,7 @@ int hf_fr_residual(const hf_problem* pr, const int* dims, const void* u_dev, voi
     if (int rc = validate(pr)) return rc;
     if (pr->n_elem > 0 && (!u_dev || !uf_dev || !divf_dev)) return fail(HF_EINVAL, "hf_fr_residual: null buffer");
     if (u_dev == divf_dev && pr->n_elem > 0) return fail(HF_EINVAL, "hf_fr_residual: in-place not supported");
-    // stages 1+2+3+6 in one pass of the lines kernel (faces written beside the divergence);
-    // the separate stage-1 kernel where no fused form is built (e.g. a planar selection)
-    const int rc = dispatch(pr, u_dev, divf_dev, nullptr, static_cast<cudaStream_t>(stream), nullptr, false, -1, -1,
-                            true, uf_dev);
-    if (rc == hfb::kUnsupported) {
-        if (int r2 = hf_fused_divergence(pr, u_dev, divf_dev, stream)) return r2;  // stages 2+3+6
-        if (int r2 = hf_fr_project(pr, u_dev, uf_dev, stream)) return r2;         // stage 1
-    } else if (rc != HF_OK) {
-        return rc;
-    }
+    if (int rc = hf_fr_divergence_faces(pr, u_dev, uf_dev, divf_dev, stream)) return rc;  // stages 1+2+3+6
     return hf_fr_correct(pr, &ms, uf_dev, nullptr, nullptr, divf_dev, stream);  // stages 4+5
 }
 

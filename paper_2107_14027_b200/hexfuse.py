@@ -393,6 +393,13 @@ def fr_correct_device(pr: hf_problem, mesh, uf, out, ghost_lo=None, ghost_hi=Non
           "hf_fr_correct")
 
 
+def fr_divergence_faces_device(pr: hf_problem, u, uf, out, stream=None) -> None:
+    """Stages 1+2+3+6 in one pass: the fused divergence into `out` and the faces
+    into `uf` (bit-identical to fused_divergence_device + fr_project_device)."""
+    check(_lib.load().hf_fr_divergence_faces(C.byref(pr), _ptr(u), _ptr(uf), _ptr(out), _stream(stream)),
+          "hf_fr_divergence_faces")
+
+
 def fr_residual_device(pr: hf_problem, dims, u, uf, out, stream=None) -> None:
     """The FR right-hand side (stages 1-6) on the periodic dims mesh, one device."""
     d3 = (C.c_int * 3)(*(list(dims) + [1] * (3 - len(dims))))

@@ -174,22 +174,34 @@ class FrOps:
         H.fr_project_device(sp, u, uf)
 
     @staticmethod
+    def divergence_faces(sp, u, out, uf):
+        H.fr_divergence_faces_device(sp, u, uf, out)
+
+    @staticmethod
     def correct(sp, mesh, uf, out, ghost_lo, ghost_hi):
         H.fr_correct_device(sp, mesh, uf, out, ghost_lo, ghost_hi)
 
 
 def fr_residual_slab(sl: FrSlab, u, out, uf, ghost_lo, ghost_hi, dist=None, ops=FrOps):
-    """Stages 1-6 on one rank's slab: project the faces, start the ghost-layer
-    exchange, run the fused divergence while it is in flight, then the interface
-    corrections.  With world == 1 the mesh wraps onto itself and no message is sent."""
-    ops.project(sl.problem, u, uf)
+    """Stages 1-6 on one rank's slab, then the ghost-layer exchange and the
+    interface corrections.  With ``ops.divergence_faces`` (the device default:
+    faces written by the fused kernel, one pass over U) the exchange follows
+    that kernel; otherwise the faces are projected first and the exchange runs
+    while the fused divergence computes.  With world == 1 the mesh wraps onto
+    itself and no message is sent."""
+    fused = getattr(ops, "divergence_faces", None)
+    if fused is not None:
+        fused(sl.problem, u, out, uf)
+    else:
+        ops.project(sl.problem, u, uf)
     reqs = []
     if sl.world > 1:
         if hasattr(u, "is_cuda") and u.is_cuda:
             import torch
             torch.cuda.current_stream().synchronize()  # faces complete before NCCL reads them
         reqs = exchange_ghost_layers(sl, uf, ghost_lo, ghost_hi, dist)
-    ops.divergence(sl.problem, u, out)
+    if fused is None:
+        ops.divergence(sl.problem, u, out)
     for r in reqs:
         r.wait()
     mesh = H.make_mesh(sl.dims, sl.d, sl.e_begin, sl.n_elem, sl.layer if sl.world > 1 else 0)
@@ -239,8 +251,7 @@ def fr_residual_slab_peer(sl: FrSlab, u, out, uf, peers: FrPeers, dist=None):
     if dist is None:
         import torch.distributed as dist
     import torch
-    H.fr_project_device(sl.problem, u, uf)
-    H.fused_divergence_device(sl.problem, u, out)
+    H.fr_divergence_faces_device(sl.problem, u, uf, out)  # stages 1+2+3+6, one pass over U
     torch.cuda.current_stream().synchronize()
     dist.barrier()
     mesh = H.make_mesh(sl.dims, sl.d, sl.e_begin, sl.n_elem, sl.layer)

@@ -167,3 +167,11 @@ def test_fused_stage1_equals_separate_stages(cuda, d, p, dims, g, fp32):
     torch.cuda.synchronize()
     assert torch.equal(uf_a, uf_b)
     assert torch.equal(out_a, out_b)
+    # the stand-alone stages 1+2+3+6 entry point (the multi-GPU drivers' first step)
+    out_c = torch.zeros_like(out_a)
+    uf_c = torch.zeros_like(uf_a)
+    hf.fr_divergence_faces_device(pr, u, uf_c, out_c)
+    hf.fr_correct_device(pr, hf.make_mesh(dims, d), uf_c, out_c)
+    torch.cuda.synchronize()
+    assert torch.equal(uf_c, uf_b)
+    assert torch.equal(out_c, out_b)
