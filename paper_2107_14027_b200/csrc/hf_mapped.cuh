@@ -68,20 +68,51 @@ __device__ __forceinline__ R mapped_adjugate(const R (&J)[DIM * DIM], R (&S)[DIM
     }
 }
 
-// Column j of J = dx/dxi at reference point xi, from the element's corners in
-// shared memory ([c][x][el] layout): sum_c X_c dN_c/dxi_j.
+// The (bi/tri)linear map in monomial form: X(xi) = sum_k a_k prod_{i in k} xi_i
+// over the 2^d axis subsets k, with a_k = 2^-d sum_c (-1)^popc(k & ~c) X_c (corner
+// c at xi_i = bit i of c ? +1 : -1).  Converted once per element in shared memory
+// ([k][x][el], in place of the corners), so that a Jacobian column costs 2^(d-1)
+// FMAs per coordinate instead of 2^d corner shape-function derivatives.
+template <class R, int DIM, int NE, int BS>
+__device__ __forceinline__ void mapped_corners_to_monomials(R* __restrict__ geo, int tid) {
+    constexpr int NC = 1 << DIM;
+    for (int q = tid; q < DIM * NE; q += BS) {
+        const int el = q % NE, x = q / NE;
+        R X[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) X[c] = geo[el + NE * (x + DIM * c)];
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+            R a = R(0);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) a = (__popc(k & ~c) & 1) ? a - X[c] : a + X[c];
+            geo[el + NE * (x + DIM * k)] = a * (R(1) / R(NC));
+        }
+    }
+}
+
+// Column j of J = dx/dxi at reference point xi from the monomial coefficients:
+// sum over subsets k containing j of a_k prod_{i in k, i != j} xi_i.
 template <class R, int DIM, int NE>
 __device__ __forceinline__ void mapped_jcol(const R* __restrict__ geo, int el, int j, const R (&xi)[3], R (&col)[DIM]) {
 #pragma unroll
     for (int i = 0; i < DIM; ++i) col[i] = R(0);
 #pragma unroll
-    for (int c = 0; c < (1 << DIM); ++c) {
-        R dn = R(0.5) * ((c >> j) & 1 ? R(1) : R(-1));
+    for (int k = 0; k < (1 << DIM); ++k) {
+        if (!((k >> j) & 1)) continue;
+        R mono = R(1);
+        bool one = true;
 #pragma unroll
-        for (int k = 0; k < DIM; ++k)
-            if (k != j) dn *= R(0.5) * (R(1) + ((c >> k) & 1 ? xi[k] : -xi[k]));
+        for (int i = 0; i < DIM; ++i)
+            if (i != j && ((k >> i) & 1)) {
+                mono = one ? xi[i] : mono * xi[i];
+                one = false;
+            }
 #pragma unroll
-        for (int i = 0; i < DIM; ++i) col[i] = fma(geo[el + NE * (i + DIM * c)], dn, col[i]);
+        for (int i = 0; i < DIM; ++i) {
+            const R a = geo[el + NE * (i + DIM * k)];
+            col[i] = one ? col[i] + a : fma(a, mono, col[i]);
+        }
     }
 }
 
@@ -376,6 +407,8 @@ __global__ void __launch_bounds__(MappedShape<R, DIM, M, NE>::BS)
     }
 
     if (fast) mbar_wait_parity(bar, 0);
+    __syncthreads();
+    mapped_corners_to_monomials<R, DIM, NE, BS>(geo, tid);
     __syncthreads();
 
     // ---------------- d sweeps ----------------
