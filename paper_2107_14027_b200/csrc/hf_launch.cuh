@@ -357,15 +357,26 @@ cudaError_t launch_planar_managed(Params<R> p, cudaStream_t st, KInfo* info, boo
     return cudaGetLastError();
 }
 
-// Mapped elements: the largest power-of-two chunk (<= 64 / 128 elements) with
-// <= 64 KB of shared memory (three CTAs per SM) and <= 512 lines.
+// Mapped elements: the largest power-of-two chunk (<= 64 / 128 elements) within
+// the measured shared-memory budget and <= 512 lines.
 template <class R, int DIM, int M>
 constexpr int mapped_ne() {
+    // shared-memory budget of the chunk (U + partial sums + corners), measured per
+    // (d, p, precision) over 32 / 64 KB (profiles/ext_r01e_mapped_kb*.jsonl):
+    // small chunks win where the element count then avoids bank-class collisions
+    // of the x-lines and more CTAs hide the chunk loads (d3 p1 FP64 643 -> 522 us,
+    // d2 p3 FP64 293 -> 225 us); HF_MAPPED_KB overrides it for such sweeps
+#ifdef HF_MAPPED_KB
+    constexpr int KB = HF_MAPPED_KB;
+#else
+    constexpr int KB = DIM == 3 ? (M <= 3 ? 32 : 64)
+                                : (sizeof(R) == 4 ? ((M == 2 || (M >= 4 && M <= 6)) ? 32 : 64) : (M <= 4 ? 32 : 64));
+#endif
     int ne = (DIM == 2) ? 128 : 64;
     while (ne > 1 && (MappedShape<R, DIM, M, 1>::HDR + 48 + size_t(ne) * ipow_c(M, DIM) *
                                                                (2 * n_vars_c(DIM)) * sizeof(R) +
                           size_t(ne) * (1 << DIM) * DIM * sizeof(R) >
-                      size_t(64 * 1024) ||
+                      size_t(KB * 1024) ||
                       ne * ipow_c(M, DIM - 1) > 512))
         ne /= 2;
     // NE*m a multiple of the bank period puts every x-line of a warp in a few bank
