@@ -187,6 +187,12 @@ typedef struct hf_context hf_context;
 HF_API hf_context* hf_context_create(int device);
 HF_API void hf_context_destroy(hf_context* ctx);
 HF_API int hf_fused_divergence_host(hf_context* ctx, const hf_problem* pr, const void* u_host, void* divf_host);
+/* Several fields (e.g. one per polynomial order of a p-adaptive mesh) through ONE
+ * slice pipeline: the copy engines fill once before the first field and drain once
+ * after the last, instead of per field.  Same per-field semantics and errors as
+ * hf_fused_divergence_host; synchronous. */
+HF_API int hf_fused_divergence_host_batch(hf_context* ctx, int n_fields, const hf_problem* prs,
+                                          const void* const* u_hosts, void* const* divf_hosts);
 
 /* ---- multi-GPU partition (element-parallel, no collective) ----
  * Part `part` of `n_parts` contiguous, group-aligned slices: elements

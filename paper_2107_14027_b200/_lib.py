@@ -52,7 +52,7 @@ EXPORTED = [
     "hf_n_vars", "hf_field_words", "hf_offset", "hf_validate", "hf_derivative_matrix",
     "hf_algorithmic_bytes_per_point", "hf_selected_method", "hf_preferred_group", "hf_kernel_info_get",
     "hf_fused_divergence", "hf_unfused_workspace_bytes", "hf_unfused_divergence", "hf_context_create",
-    "hf_context_destroy", "hf_fused_divergence_host", "hf_partition", "hf_last_error", "hf_version",
+    "hf_context_destroy", "hf_fused_divergence_host", "hf_fused_divergence_host_batch", "hf_partition", "hf_last_error", "hf_version",
     "hf_geometry_words", "hf_fused_divergence_mapped", "hf_mapped_kernel_info",
     "hf_face_words", "hf_fr_project", "hf_fr_correct", "hf_fr_divergence_faces", "hf_fr_residual",
     "hf_ipc_handle", "hf_ipc_open", "hf_ipc_close",
@@ -104,6 +104,8 @@ def load() -> C.CDLL:
     L.hf_context_destroy.argtypes = [C.c_void_p]
     L.hf_context_destroy.restype = None
     L.hf_fused_divergence_host.argtypes = [C.c_void_p, P, C.c_void_p, C.c_void_p]
+    L.hf_fused_divergence_host_batch.argtypes = [C.c_void_p, C.c_int, P, C.POINTER(C.c_void_p),
+                                                 C.POINTER(C.c_void_p)]
     L.hf_partition.argtypes = [P, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                C.POINTER(C.c_int64)]
     L.hf_last_error.restype = C.c_char_p

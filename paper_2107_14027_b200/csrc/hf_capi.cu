@@ -682,84 +682,120 @@ void hf_context_destroy(hf_context* c) {
 }
 
 int hf_fused_divergence_host(hf_context* c, const hf_problem* pr, const void* u_host, void* divf_host) {
+    return hf_fused_divergence_host_batch(c, 1, pr, &u_host, &divf_host);
+}
+
+int hf_fused_divergence_host_batch(hf_context* c, int n_fields, const hf_problem* prs, const void* const* u_hosts,
+                                   void* const* divf_hosts) {
     if (!c) return fail(HF_EINVAL, "hf_fused_divergence_host: null context");
-    if (int rc = validate(pr)) return rc;
-    if (pr->n_elem == 0) return HF_OK;
-    if (!u_host || !divf_host) return fail(HF_EINVAL, "hf_fused_divergence_host: null buffer");
+    if (n_fields < 0 || (n_fields > 0 && (!prs || !u_hosts || !divf_hosts)))
+        return fail(HF_EINVAL, "hf_fused_divergence_host_batch: null arrays");
+    for (int i = 0; i < n_fields; ++i) {
+        if (int rc = validate(&prs[i])) return rc;
+        if (prs[i].n_elem > 0 && (!u_hosts[i] || !divf_hosts[i]))
+            return fail(HF_EINVAL, "hf_fused_divergence_host: null buffer");
+    }
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
 
-    const size_t w = word_bytes(pr);
-    const int64_t gw = int64_t(pr->group) * ipow64(pr->p + 1, pr->d) * (1 + pr->d + pr->d * pr->d);
-    const int64_t n_groups = (pr->n_elem + pr->group - 1) / pr->group;
-    // Slices: whole groups, multiples of the kernel's chunk, at most ~48 MB (the slot size).
-    // The copy pipeline moves one direction alone while it fills (the first H2D) and drains
-    // (the last D2H), so the plan ramps up and down: b/8, b/4, b/2, b, ..., b, b/2, b/4, b/8.
-    int pref = hf_preferred_group(pr);
-    if (pref < 1) pref = 1;
-    const int64_t chunk_groups = std::max<int64_t>(1, (pref + pr->group - 1) / pr->group);
-    auto rnd = [&](int64_t x) { return std::max<int64_t>(chunk_groups, x / chunk_groups * chunk_groups); };
-    const int64_t base = std::min<int64_t>(rnd((int64_t(48) << 20) / int64_t(gw * w)), n_groups);
-    std::vector<int64_t> plan;
-    {
+    // One slice plan over all fields: slices of whole groups of one field, multiples of
+    // the kernel's chunk, at most ~48 MB (the slot size).  The copy pipeline moves one
+    // direction alone while it fills (the first H2D) and drains (the last D2H), so the
+    // plan ramps up at the start of the first field and down at the end of the last one
+    // (b/8, b/4, b/2, b, ..., b, b/2, b/4, b/8); the fields in between stream at full
+    // slices with no fill or drain of their own.
+    struct Slice {
+        int field;
+        int64_t g0, ng;
+    };
+    std::vector<Slice> plan;
+    size_t slot_need = 0;
+    for (int i = 0; i < n_fields; ++i) {
+        const hf_problem* pr = &prs[i];
+        if (pr->n_elem == 0) continue;
+        const size_t w = word_bytes(pr);
+        const int64_t gw = int64_t(pr->group) * ipow64(pr->p + 1, pr->d) * (1 + pr->d + pr->d * pr->d);
+        const int64_t n_groups = (pr->n_elem + pr->group - 1) / pr->group;
+        int pref = hf_preferred_group(pr);
+        if (pref < 1) pref = 1;
+        const int64_t chunk_groups = std::max<int64_t>(1, (pref + pr->group - 1) / pr->group);
+        auto rnd = [&](int64_t x) { return std::max<int64_t>(chunk_groups, x / chunk_groups * chunk_groups); };
+        const int64_t base = std::min<int64_t>(rnd((int64_t(48) << 20) / int64_t(gw * w)), n_groups);
+        const bool up = plan.empty();
+        bool down = true;  // the last field with elements ramps down
+        for (int k = i + 1; k < n_fields; ++k) down = down && prs[k].n_elem == 0;
+        std::vector<int64_t> q;
         const int64_t ramp[3] = {rnd(base / 8), rnd(base / 4), rnd(base / 2)};
         const int64_t tail = ramp[0] + ramp[1] + ramp[2];
         int64_t rem = n_groups;
-        if (rem <= 2 * tail + base) {  // small: ~6 equal slices
-            const int64_t q = rnd(std::max<int64_t>(1, rem / 6));
+        const int64_t need = (up ? tail : 0) + (down ? tail : 0) + base;
+        if (rem <= need) {  // small: ~6 equal slices (or whole base slices between ramps)
+            const int64_t s = (up || down) ? rnd(std::max<int64_t>(1, rem / 6)) : base;
             while (rem > 0) {
-                plan.push_back(std::min(q, rem));
-                rem -= plan.back();
+                q.push_back(std::min(s, rem));
+                rem -= q.back();
             }
         } else {
-            for (int k = 0; k < 3; ++k) {
-                plan.push_back(ramp[k]);
-                rem -= ramp[k];
-            }
-            while (rem > tail + base) {
-                plan.push_back(base);
+            if (up)
+                for (int k = 0; k < 3; ++k) {
+                    q.push_back(ramp[k]);
+                    rem -= ramp[k];
+                }
+            const int64_t end = down ? tail : 0;
+            while (rem > end + base) {
+                q.push_back(base);
                 rem -= base;
             }
-            const int64_t mid = (rem - tail) / chunk_groups * chunk_groups;  // whole chunks
-            if (mid > 0) plan.push_back(mid);
-            for (int k = 2; k >= 0; --k) plan.push_back(ramp[k]);
-            plan.back() += rem - tail - mid;  // the remainder rides in the final slice
+            const int64_t mid = (rem - end) / chunk_groups * chunk_groups;  // whole chunks
+            if (mid > 0) q.push_back(mid);
+            if (down)
+                for (int k = 2; k >= 0; --k) q.push_back(ramp[k]);
+            q.back() += rem - end - mid;  // the remainder rides in the final slice
+        }
+        int64_t g0 = 0;
+        for (int64_t ng : q) {
+            plan.push_back({i, g0, ng});
+            g0 += ng;
+            slot_need = std::max(slot_need, size_t(ng * gw) * w);
         }
     }
-    int64_t slice_groups = 0;
-    for (int64_t q : plan) slice_groups = std::max(slice_groups, q);
-    if (int rc = ctx_reserve(c, size_t(slice_groups * gw) * w)) return rc;
+    if (plan.empty()) return HF_OK;
+    if (int rc = ctx_reserve(c, slot_need)) return rc;
 
     // Pageable host memory is pinned for the duration of the call.
-    const size_t total = size_t(n_groups * gw) * w;
-    bool reg_in = false, reg_out = false;
-    if (!is_pinned(u_host)) {
-        if (cudaHostRegister(const_cast<void*>(u_host), total, cudaHostRegisterReadOnly) == cudaSuccess) reg_in = true;
+    std::vector<const void*> reg;
+    auto pin = [&](const void* p, size_t bytes, unsigned flags) {
+        if (is_pinned(p)) return;
+        if (cudaHostRegister(const_cast<void*>(p), bytes, flags) == cudaSuccess) reg.push_back(p);
         else cudaGetLastError();
-    }
-    if (!is_pinned(divf_host)) {
-        if (cudaHostRegister(divf_host, total, cudaHostRegisterDefault) == cudaSuccess) reg_out = true;
-        else cudaGetLastError();
+    };
+    for (int i = 0; i < n_fields; ++i) {
+        if (prs[i].n_elem == 0) continue;
+        const size_t total = size_t(hf_field_words(&prs[i])) * word_bytes(&prs[i]);
+        pin(u_hosts[i], total, cudaHostRegisterReadOnly);
+        pin(divf_hosts[i], total, cudaHostRegisterDefault);
     }
 
     int rc = HF_OK;
-    int64_t g0 = 0;
-    for (size_t s_idx = 0; s_idx < plan.size() && rc == HF_OK; g0 += plan[s_idx], ++s_idx) {
+    for (size_t s_idx = 0; s_idx < plan.size() && rc == HF_OK; ++s_idx) {
+        const Slice& sl = plan[s_idx];
+        const hf_problem* pr = &prs[sl.field];
+        const size_t w = word_bytes(pr);
+        const int64_t gw = int64_t(pr->group) * ipow64(pr->p + 1, pr->d) * (1 + pr->d + pr->d * pr->d);
         const int slot = int(s_idx % hf_context::kSlots);
-        const int64_t ng = plan[s_idx];
-        const size_t bytes = size_t(ng * gw) * w;
+        const size_t bytes = size_t(sl.ng * gw) * w;
         cudaStream_t st = c->stream[slot];
-        const auto* src = static_cast<const unsigned char*>(u_host) + size_t(g0 * gw) * w;
-        auto* dst = static_cast<unsigned char*>(divf_host) + size_t(g0 * gw) * w;
+        const auto* src = static_cast<const unsigned char*>(u_hosts[sl.field]) + size_t(sl.g0 * gw) * w;
+        auto* dst = static_cast<unsigned char*>(divf_hosts[sl.field]) + size_t(sl.g0 * gw) * w;
         // the stream is in-order, so the slot's previous D2H has completed before this H2D lands
         if ((e = cudaMemcpyAsync(c->d_in[slot], src, bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
             rc = cuda_fail(e, "H2D");
             break;
         }
         hf_problem sp = *pr;
-        sp.n_elem = std::min<int64_t>(pr->n_elem - g0 * pr->group, ng * pr->group);
+        sp.n_elem = std::min<int64_t>(pr->n_elem - sl.g0 * pr->group, sl.ng * pr->group);
         if (sp.method == HF_METHOD_UNFUSED) sp.method = HF_METHOD_AUTO;
-        if (sp.n_elem < ng * pr->group) {
+        if (sp.n_elem < sl.ng * pr->group) {
             // partial last group: padding comes back as zeros, like the reference's zeroed result (oracle.hpp:26-27)
             if ((e = cudaMemsetAsync(c->d_out[slot], 0, bytes, st)) != cudaSuccess) {
                 rc = cuda_fail(e, "memset");
@@ -777,8 +813,7 @@ int hf_fused_divergence_host(hf_context* c, const hf_problem* pr, const void* u_
         e = cudaStreamSynchronize(c->stream[s]);
         if (e != cudaSuccess && rc == HF_OK) rc = cuda_fail(e, "hf_fused_divergence_host");
     }
-    if (reg_in) cudaHostUnregister(const_cast<void*>(u_host));
-    if (reg_out) cudaHostUnregister(divf_host);
+    for (const void* p : reg) cudaHostUnregister(const_cast<void*>(p));
     return rc;
 }
 

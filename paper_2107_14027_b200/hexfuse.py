@@ -475,6 +475,15 @@ class Context:
         check(_lib.load().hf_fused_divergence_host(self._h, C.byref(pr), _host_ptr(u_host), _host_ptr(out_host)),
               "hf_fused_divergence_host")
 
+    def run_batch(self, items) -> None:
+        """[(problem, u_host, out_host), ...] through one copy pipeline (hf_fused_divergence_host_batch)."""
+        items = list(items)
+        n = len(items)
+        prs = (hf_problem * n)(*[it[0] for it in items])
+        us = (C.c_void_p * n)(*[_host_ptr(it[1]) for it in items])
+        outs = (C.c_void_p * n)(*[_host_ptr(it[2]) for it in items])
+        check(_lib.load().hf_fused_divergence_host_batch(self._h, n, prs, us, outs), "hf_fused_divergence_host_batch")
+
 
 def _host_ptr(a) -> int:
     if hasattr(a, "data_ptr"):

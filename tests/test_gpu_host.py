@@ -56,3 +56,41 @@ def test_host_path_matches_device_path(cuda, d, p, fp32, target_mb):
         want = out[sl]
         err = np.max(np.abs(got - want)) / max(1.0, np.max(np.abs(want)))
         assert err <= (1e-5 if fp32 else 1e-12), err
+
+
+def test_host_batch_matches_device_path(cuda):
+    """hf_fused_divergence_host_batch: several fields (mixed d, p, precision, a partial
+    last group, an empty field) through one copy pipeline, each bit-identical to the
+    device-buffer kernel on the same field."""
+    import paper_2107_14027_b200 as hf
+    from paper_2107_14027_b200 import Precision
+    specs = [(3, 1, True, 120), (3, 6, False, 90), (2, 4, True, 40), (3, 3, False, 0), (3, 3, False, 150)]
+    gen = torch.Generator().manual_seed(11)
+    items, refs = [], []
+    for d, p, fp32, target_mb in specs:
+        prec = Precision.fp32 if fp32 else Precision.fp64
+        g = hf.preferred_group(hf.make_problem(d, p, 1, 1, prec, PAR))
+        nv, npt, w = O.n_vars(d), (p + 1) ** d, (4 if fp32 else 8)
+        n = 0 if target_mb == 0 else max(g, int(target_mb * 2 ** 20 / (nv * npt * w)) // g * g) + 1
+        pr = hf.make_problem(d, p, n, g, prec, PAR, with_source=True)
+        dt = torch.float32 if fp32 else torch.float64
+        u = (torch.rand(hf.field_words(pr), generator=gen, dtype=torch.float64) * 2 - 1).to(dt)
+        if n:
+            nwg = hf.field_words(pr) // ((n + g - 1) // g)
+            u[-nwg:].view(nv * npt, g)[:, n % g:] = 0  # padding elements stay zero
+            ud = u.cuda()
+            od = torch.zeros_like(ud)
+            hf.fused_divergence_device(pr, ud, od)
+            torch.cuda.synchronize()
+            refs.append(od.cpu())
+        else:
+            refs.append(u.clone())
+        src = u.pin_memory()
+        dst = torch.zeros_like(src).pin_memory() if n else src.clone()
+        items.append((pr, src, dst))
+    ctx = hf.Context(0)
+    ctx.run_batch(items)
+    ctx.close()
+    for (pr, src, dst), ref in zip(items, refs):
+        if pr.n_elem:
+            assert torch.equal(dst, ref), (pr.d, pr.p, pr.precision)
