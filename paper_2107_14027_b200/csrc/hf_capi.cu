@@ -763,11 +763,22 @@ int hf_fused_divergence_host_batch(hf_context* c, int n_fields, const hf_problem
     if (int rc = ctx_reserve(c, slot_need)) return rc;
 
     // Pageable host memory is pinned for the duration of the call.
+    // (Read-only registration needs device support, cudaDevAttrHostRegisterReadOnlySupported:
+    // where it is refused the input is registered read-write.  If registration fails
+    // altogether, the copies stage through the driver's pageable path -- slower, same result.)
     std::vector<const void*> reg;
     auto pin = [&](const void* p, size_t bytes, unsigned flags) {
         if (is_pinned(p)) return;
-        if (cudaHostRegister(const_cast<void*>(p), bytes, flags) == cudaSuccess) reg.push_back(p);
-        else cudaGetLastError();
+        if (cudaHostRegister(const_cast<void*>(p), bytes, flags) == cudaSuccess) {
+            reg.push_back(p);
+            return;
+        }
+        cudaGetLastError();
+        if (flags != cudaHostRegisterDefault &&
+            cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterDefault) == cudaSuccess)
+            reg.push_back(p);
+        else
+            cudaGetLastError();
     };
     for (int i = 0; i < n_fields; ++i) {
         if (prs[i].n_elem == 0) continue;
