@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -250,6 +251,8 @@ int dispatch(const hf_problem* pr, const void* u, void* out, void* ws, cudaStrea
              int force_method = -1, int force_variant = -1, bool faces = false, void* uf = nullptr) {
     int method, variant;
     select_method(pr, &method, &variant);
+    if (faces && method == HF_METHOD_LINES && hfb::faces_variant_override(pr->d, pr->p) >= 0)
+        variant = hfb::faces_variant_override(pr->d, pr->p);
     if (force_method >= 0) method = force_method;
     if (force_variant >= 0) variant = force_variant;
     const bool src = pr->with_source != 0;
@@ -483,8 +486,14 @@ int hf_fr_divergence_faces(const hf_problem* pr, const void* u_dev, void* uf_dev
     if (u_dev == divf_dev && pr->n_elem > 0) return fail(HF_EINVAL, "hf_fr_divergence_faces: in-place not supported");
     // stages 1+2+3+6 in one pass of the lines kernel (faces written beside the divergence);
     // the separate stage-1 kernel where no fused form is built (e.g. a planar selection)
-    const int rc = dispatch(pr, u_dev, divf_dev, nullptr, static_cast<cudaStream_t>(stream), nullptr, false, -1, -1,
-                            true, uf_dev);
+#ifdef HF_FACES_AB
+    const char* fv = std::getenv("HF_FACES_VARIANT");
+    const int force_v = fv ? std::atoi(fv) : -1;
+#else
+    const int force_v = -1;
+#endif
+    const int rc = dispatch(pr, u_dev, divf_dev, nullptr, static_cast<cudaStream_t>(stream), nullptr, false, -1,
+                            force_v, true, uf_dev);
     if (rc == hfb::kUnsupported) {
         if (int r2 = hf_fused_divergence(pr, u_dev, divf_dev, stream)) return r2;  // stages 2+3+6
         return hf_fr_project(pr, u_dev, uf_dev, stream);                         // stage 1

@@ -78,12 +78,23 @@ constexpr SelRow kSelect[] = {
 // CTA), 3 (TMA ring) and 10 (grouped TMA ring), so that every kernel form stays
 // parity-tested; the tuning build (make tuning, -DHF_TUNING) carries all of them
 // for tools/select_methods.py.
+// Lines variant for the FACES form where it differs from the selection: at d3 p6 the
+// one-chunk-per-CTA kernel (variant 0, the same chunk as the selected ring) writes
+// the faces faster than the TMA ring, whose consumers are the ring's bottleneck
+// (fused stages 1+2+3+6, 1e7 points: FP64 657 -> 518 us, FP32 300 -> 288 us;
+// profiles/ext_r01e_faces_variant_*.jsonl).  -1: the selected variant.
+constexpr int faces_variant_override(int d, int p) { return (d == 3 && p == 6) ? 0 : -1; }
+
 // The FACES (fused FR stage 1) form: the selected variant of each configuration.
 template <class R, int DIM, int M, int VARIANT>
 constexpr bool variant_faces_built() {
 #ifdef HF_TUNING
     return VARIANT == 0 || VARIANT == 3;
 #else
+#ifdef HF_FACES_AB
+    if (VARIANT == 0 || VARIANT == 3) return true;
+#endif
+    if (VARIANT == faces_variant_override(DIM, M - 1)) return true;
     for (const SelRow& r : kSelect)
         if (r.d == DIM && r.p == M - 1 && r.prec == (sizeof(R) == 8 ? 1 : 0) && r.method == 2 && r.variant == VARIANT)
             return true;
