@@ -14,6 +14,7 @@ import paper_2107_14027_b200 as hf
 from paper_2107_14027_b200 import HexfuseInvalid, Method, PhysParams, Precision, _lib
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HF_EINVAL = 2  # include/hexfuse_b200.h
 HEADER = os.path.join(ROOT, "include", "hexfuse_b200.h")
 
 
@@ -130,3 +131,19 @@ def test_partition_covers_every_element_once(n, g, parts):
 def test_unfused_workspace_bytes():
     pr = hf.make_problem(3, 4, 100, 8, Precision.fp32, PhysParams())
     assert hf.unfused_workspace_bytes(pr) == hf.field_words(pr) * 3 * 4
+
+
+def test_new_entry_points_validate_before_touching_the_device():
+    """hf_fr_divergence_faces / hf_fused_divergence_host_batch reject bad arguments
+    with HF_EINVAL before any CUDA call (so this runs without a GPU)."""
+    L = _lib.load()
+    pr = hf.make_problem(3, 3, 10, 2, Precision.fp64, PhysParams())
+    assert L.hf_fr_divergence_faces(C.byref(pr), None, None, None, None) == HF_EINVAL
+    assert "null buffer" in L.hf_last_error().decode()
+    buf = (C.c_double * 4)()
+    assert L.hf_fr_divergence_faces(C.byref(pr), buf, buf, buf, None) == HF_EINVAL  # u == divf
+    assert "in-place" in L.hf_last_error().decode()
+    bad = hf.make_problem(3, 0, 10, 2, Precision.fp64, PhysParams())
+    assert L.hf_fr_divergence_faces(C.byref(bad), buf, buf, None, None) == HF_EINVAL
+    assert L.hf_fused_divergence_host_batch(None, 1, C.byref(pr), None, None) == HF_EINVAL
+    assert "null context" in L.hf_last_error().decode()
