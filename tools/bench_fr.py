@@ -10,7 +10,7 @@ correction (stages 4+5), each with its algorithmic HBM bytes:
   residual (hf_fr_residual: the fused kernel writes the faces, then the correction)
            2 n_v m^d w + F w  +  F w + 2 n_v m^d w
 
-    python tools/bench_fr.py [--points 1e7] [--out gpurun_out/fr.jsonl]
+    python tools/bench_fr.py [--points 1e7] [--dims 3,2] [--out gpurun_out/fr.jsonl]
 """
 import argparse
 import json
@@ -20,6 +20,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2107_14027_b200 as hf  # noqa: E402
@@ -49,45 +50,51 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--points", type=float, default=1e7)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--dims", default="3", help="comma list of dimensions (3, 2)")
     a = ap.parse_args()
     fh = open(a.out, "w") if a.out else None
-    d = 3
-    for prec in (Precision.fp32, Precision.fp64):
-        for p in range(1, 7):
-            w = 4 if prec == Precision.fp32 else 8
-            m = p + 1
-            g = hf.preferred_group(hf.make_problem(d, p, 1, 1, prec, PAR))
+    for d, prec, p in [(d, prec, p) for d in map(int, a.dims.split(",")) for prec in (Precision.fp32, Precision.fp64)
+                       for p in range(1, 7 if d == 3 else 9)]:
+        w = 4 if prec == Precision.fp32 else 8
+        m = p + 1
+        g = hf.preferred_group(hf.make_problem(d, p, 1, 1, prec, PAR))
+        if d == 3:
             # periodic box nx x ny x nz with nx*ny a multiple of the group (layer partitions)
             nx = ny = max(2, round((a.points / m ** 3) ** (1 / 3)))
             while (nx * ny) % g:
                 nx += 1
             nz = max(2, round(a.points / m ** 3 / (nx * ny)))
             dims = (nx, ny, nz)
-            n = nx * ny * nz
-            pr = hf.make_problem(d, p, n, g, prec, PAR)
-            dt = torch.float32 if w == 4 else torch.float64
-            u = torch.rand(hf.field_words(pr), dtype=dt, device="cuda") * 2 - 1
-            out = torch.empty_like(u)
-            uf = torch.empty(hf.face_words(pr), dtype=dt, device="cuda")
-            ms = hf.make_mesh(dims, d)
-            t_div = timed(lambda: hf.fused_divergence_device(pr, u, out))
-            t_prj = timed(lambda: hf.fr_project_device(pr, u, uf))
-            t_cor = timed(lambda: hf.fr_correct_device(pr, ms, uf, out))
-            t_all = timed(lambda: hf.fr_residual_device(pr, dims, u, uf, out))
-            nv, F = hf.n_vars(d), 2 * d * m ** (d - 1) * hf.n_vars(d)
-            field = n * nv * m ** d * w
-            faces = n * F * w
-            row = {"d": d, "p": p, "precision": prec.name, "dims": dims, "points": n * m ** d,
-                   "fused_us": round(t_div * 1e6, 1), "fused_GBps": round(2 * field / t_div / 1e9, 1),
-                   "project_us": round(t_prj * 1e6, 1), "project_GBps": round((field + faces) / t_prj / 1e9, 1),
-                   "correct_us": round(t_cor * 1e6, 1), "correct_GBps": round((faces + 2 * field) / t_cor / 1e9, 1),
-                   "residual_us": round(t_all * 1e6, 1),
-                   "residual_gdofs": round(n * m ** d / t_all / 1e9, 3),
-                   "residual_GBps_alg": round((4 * field + 2 * faces) / t_all / 1e9, 1)}
-            print(json.dumps(row), flush=True)
-            if fh:
-                fh.write(json.dumps(row) + "\n")
-            del u, out, uf
+        else:
+            nx = max(2, round((a.points / m ** 2) ** 0.5))
+            while nx % g:
+                nx += 1
+            dims = (nx, max(2, round(a.points / m ** 2 / nx)))
+        n = int(np.prod(dims))
+        pr = hf.make_problem(d, p, n, g, prec, PAR)
+        dt = torch.float32 if w == 4 else torch.float64
+        u = torch.rand(hf.field_words(pr), dtype=dt, device="cuda") * 2 - 1
+        out = torch.empty_like(u)
+        uf = torch.empty(hf.face_words(pr), dtype=dt, device="cuda")
+        ms = hf.make_mesh(dims, d)
+        t_div = timed(lambda: hf.fused_divergence_device(pr, u, out))
+        t_prj = timed(lambda: hf.fr_project_device(pr, u, uf))
+        t_cor = timed(lambda: hf.fr_correct_device(pr, ms, uf, out))
+        t_all = timed(lambda: hf.fr_residual_device(pr, dims, u, uf, out))
+        nv, F = hf.n_vars(d), 2 * d * m ** (d - 1) * hf.n_vars(d)
+        field = n * nv * m ** d * w
+        faces = n * F * w
+        row = {"d": d, "p": p, "precision": prec.name, "dims": dims, "points": n * m ** d,
+               "fused_us": round(t_div * 1e6, 1), "fused_GBps": round(2 * field / t_div / 1e9, 1),
+               "project_us": round(t_prj * 1e6, 1), "project_GBps": round((field + faces) / t_prj / 1e9, 1),
+               "correct_us": round(t_cor * 1e6, 1), "correct_GBps": round((faces + 2 * field) / t_cor / 1e9, 1),
+               "residual_us": round(t_all * 1e6, 1),
+               "residual_gdofs": round(n * m ** d / t_all / 1e9, 3),
+               "residual_GBps_alg": round((4 * field + 2 * faces) / t_all / 1e9, 1)}
+        print(json.dumps(row), flush=True)
+        if fh:
+            fh.write(json.dumps(row) + "\n")
+        del u, out, uf
 
 
 if __name__ == "__main__":
