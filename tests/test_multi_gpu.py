@@ -91,7 +91,7 @@ def test_slices_tile_the_field():
 
 
 # ---------------------------------------------------------------- FR right-hand side: layer slabs + ghost exchange
-def _fr_worker(rank, world, port, cases, q):
+def _fr_worker(rank, world, port, cases, q, fused=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -142,6 +142,10 @@ def _fr_worker(rank, world, port, cases, q):
                 O.fr_correct(d, p, g, dims, Ufg, outg, par.nu, par.zeta, par.T, jac, e0, e1)
                 out[:] = torch.from_numpy(outg[e0 // g * gw:e1 // g * gw])
 
+        if fused:  # the device drivers' order: faces with the divergence, then the exchange
+            CpuOps.divergence_faces = staticmethod(
+                lambda sp, u_, out_, uf_: (CpuOps.divergence(sp, u_, out_), CpuOps.project(sp, u_, uf_)))
+
         u = torch.from_numpy(U[e0 // g * gw:e1 // g * gw].copy())
         out = torch.zeros_like(u)
         uf = torch.zeros(hf.face_words(sl.problem), dtype=torch.float64)
@@ -161,13 +165,13 @@ def _fr_worker(rank, world, port, cases, q):
     q.put((rank, ok))
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_fr_slabs_with_ghost_exchange_gloo(world):
+@pytest.mark.parametrize("world,fused", [(2, False), (3, False), (2, True)])
+def test_fr_slabs_with_ghost_exchange_gloo(world, fused):
     cases = [(3, 2, (2, 2, 6), 4, True), (3, 3, (3, 2, 3), 2, False), (2, 4, (4, 6), 4, True)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_fr_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    procs = [ctx.Process(target=_fr_worker, args=(r, world, port, cases, q, fused)) for r in range(world)]
     for pr_ in procs:
         pr_.start()
     res = dict(q.get(timeout=300) for _ in procs)
