@@ -378,11 +378,12 @@ template <class R, int DIM, int M>
 int fr_stage(int which, const Params<R>& prm, const FrParams<R>& fp, R* uf, cudaStream_t st) {
     if (prm.n_elem == 0) return 0;
     if (which == 1) return fr_project_dispatch<R, DIM, M>(prm, fp, uf, st);
-    // <= 48 KB of jumps per CTA (occupancy), or <= 64 KB when the AoSoA group is at
+    // <= 48 KB of jumps per CTA (occupancy), or <= 96 KB when the AoSoA group is at
     // least that many elements, so that stage 5's point loads cover whole 32-byte
-    // sectors (p6: FP32 486 -> 336 us, FP64 832 -> 744 us; a larger chunk with a
-    // smaller group only costs occupancy: p4 FP64 822 -> 978 us)
-    constexpr int NE1 = fr_corr_ne<R, DIM, M, 48>(), NE2 = fr_corr_ne<R, DIM, M, 64>();
+    // sectors and rows (p6: FP32 486 -> 336 us, FP64 832 -> 744 us; p1 FP64, group 64:
+    // 1297 -> 1091 us; a larger chunk with a smaller group only costs occupancy:
+    // p4 FP64 822 -> 978 us)
+    constexpr int NE1 = fr_corr_ne<R, DIM, M, 48>(), NE2 = fr_corr_ne<R, DIM, M, 96>();
     if constexpr (NE2 > NE1) {
         if (prm.group >= NE2) return fr_correct_launch<R, DIM, M, NE2>(prm, fp, st);
     }
