@@ -21,6 +21,8 @@
 // (same layout, one layer each) through NCCL (multi_gpu.FrSlab).
 #pragma once
 
+#include <cstdlib>
+
 #include "hf_lines.cuh"
 
 namespace hfb {
@@ -312,6 +314,164 @@ __global__ void __launch_bounds__(FrCorrShape<R, DIM, M, NE>::BS)
     }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// stages 4 + 5, staged form: the residual chunk is bulk-copied into shared memory while
+// stage 4 loads the faces; per axis one thread per (element, A-line) computes both line-end
+// jumps in registers and applies out(t) -= jac_A (g_L'(x_t) jump_- + g_R'(x_t) jump_+) to the
+// staged chunk (lines of one axis are disjoint; one barrier between axes); bulk copy out.
+// Selected per (d, p, precision) where it beats hf_fr_correct_kernel (fr_correct_staged()).
+// ---------------------------------------------------------------------------------------------
+template <class R, int DIM, int M, int NE>
+struct FrCorrStagedShape {
+    using L = LinesShape<R, DIM, M, NE>;
+    static constexpr int NV = n_vars_c(DIM);
+    static constexpr int LN = fr_lines<DIM, M>();
+    static constexpr int T = (NE * LN + 31) / 32 * 32;
+    static constexpr int BS = T < 64 ? 64 : T;
+    static constexpr int HDR = 128;
+    static constexpr size_t SMEM = HDR + size_t(L::BUF_BYTES);
+};
+
+template <class R, int DIM, int A, int V = 0>
+__device__ __forceinline__ void fr_jump_regs(const R (&Uo)[n_vars_c(DIM)], const R (&Un)[n_vars_c(DIM)], R lam, int s,
+                                             const Params<R>& p, R (&j)[n_vars_c(DIM)]) {
+    if constexpr (V < n_vars_c(DIM)) {
+        const R fo = fr_flux_row<R, DIM, A, V>(Uo, p), fn = fr_flux_row<R, DIM, A, V>(Un, p);
+        const R du = s ? (Un[V] - Uo[V]) : (Uo[V] - Un[V]);
+        const R FI = R(0.5) * (fo + fn) - R(0.5) * lam * du;
+        j[V] = FI - fo;
+        fr_jump_regs<R, DIM, A, V + 1>(Uo, Un, lam, s, p, j);
+    }
+}
+
+template <class R, int DIM, int M, int NE>
+__global__ void __launch_bounds__(FrCorrStagedShape<R, DIM, M, NE>::BS)
+    hf_fr_correct_staged_kernel(const __grid_constant__ Params<R> p, const __grid_constant__ FrParams<R> f) {
+    using S = FrCorrStagedShape<R, DIM, M, NE>;
+    using L = typename S::L;
+    using IO = typename L::IO;
+    constexpr int NV = S::NV, LN = S::LN, BS = S::BS, NP = ipow_c(M, DIM), FW = 2 * DIM * LN * NV;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    unsigned char* buf = smem_raw + S::HDR;
+    __shared__ const R* own_f[NE];
+    __shared__ const R* nbr_f[NE][DIM][2];
+    const int tid = threadIdx.x;
+    const long long E0 = static_cast<long long>(blockIdx.x) * NE;
+    const int ne = int(p.n_elem - E0 < NE ? p.n_elem - E0 : NE);
+    const int G = int(p.group);
+    const int VS = G * 2 * DIM * LN;
+    const long long grp = E0 / p.group;
+    const long long gbase = grp * p.group_words + (E0 - grp * p.group);
+    const bool contiguous = (p.group == NE);
+    const bool fast = chunk_bulk_ok<R, L::IN_WORDS>(p, gbase, E0 + NE <= p.n_elem, contiguous);
+    const int head = fast ? IO::head_bytes(p.out + gbase, contiguous) : 0;
+
+    if (fast) {
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (tid < 32) {
+            if (tid == 0) mbar_arrive_expect_tx(bar, IO::tx_bytes(p.out + gbase, contiguous));
+            __syncwarp();
+            IO::load(buf, p.out + gbase, p.group, contiguous, bar, tid);
+        }
+    } else {
+        R* s0 = reinterpret_cast<R*>(buf);
+        for (int idx = tid; idx < L::IN_WORDS; idx += BS) {
+            const long long e = E0 + idx % NE;
+            R v = R(0);
+            if (e < p.n_elem) {
+                const long long ge = e / p.group;
+                v = p.out[ge * p.group_words + (e - ge * p.group) + static_cast<long long>(p.group) * (idx / NE)];
+            }
+            s0[idx] = v;
+        }
+    }
+    for (int q = tid; q < ne * 2 * DIM; q += BS) {
+        const int el = q % ne, side = q / ne, A = side >> 1, s = side & 1;
+        const long long e = E0 + el;
+        const long long eg = f.mesh.e_begin + e;
+        const long long nx = f.mesh.dims[0], ny = f.mesh.dims[1];
+        const long long n_mesh = nx * ny * (DIM == 3 ? f.mesh.dims[2] : 1);
+        long long cx = eg % nx, cy = (eg / nx) % ny, cz = DIM == 3 ? eg / (nx * ny) : 0;
+        const int step = s ? 1 : -1;
+        if (A == 0) cx = (cx + step + nx) % nx;
+        else if (A == 1) cy = (cy + step + ny) % ny;
+        else cz = (cz + step + f.mesh.dims[2]) % f.mesh.dims[2];
+        const long long en = cx + nx * (cy + ny * cz);
+        long long enl;
+        const R* nb = fr_faces_of(f, en, n_mesh, &enl);
+        nbr_f[el][A][s] = nb + fr_elem_base(enl, G, FW) + (long long)G * LN * (1 - s + 2 * A);
+        if (side == 0) own_f[el] = f.uf + fr_elem_base(e, G, FW);
+    }
+    __syncthreads();
+    R* sm = reinterpret_cast<R*>(buf + head);
+
+    auto axis = [&](auto a_tag) {
+        constexpr int A = decltype(a_tag)::value;
+        for (int task = tid; task < NE * LN; task += BS) {
+            const int el = task % NE;
+            const int l = task / NE;
+            if (el >= ne) continue;
+            R jm[NV], jp[NV];
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const R* ow = own_f[el] + G * (l + LN * (s + 2 * A));
+                const R* nw = nbr_f[el][A][s] + G * l;
+                R Uo[NV], Un[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    Uo[v] = ow[VS * v];
+                    Un[v] = nw[VS * v];
+                }
+                const R lam = fmax(fr_wavespeed<R, DIM, A>(Uo, p), fr_wavespeed<R, DIM, A>(Un, p));
+                if (s == 0) fr_jump_regs<R, DIM, A>(Uo, Un, lam, 0, p, jm);
+                else fr_jump_regs<R, DIM, A>(Uo, Un, lam, 1, p, jp);
+            }
+            if constexpr (A == 0) {
+                if (fast) mbar_wait_parity(bar, 0);  // the chunk has landed (idempotent per thread)
+            }
+            R* ln = sm + el + NE * fr_line_point<DIM, M>(A, l, 0);
+            constexpr int TS = NE * (A == 0 ? 1 : (A == 1 ? M : M * M));
+            const R ja = p.jac[A];
+#pragma unroll
+            for (int t = 0; t < M; ++t) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    R* q = ln + TS * t + NE * NP * v;
+                    *q = *q - ja * fma(f.gl[t], jm[v], f.gr[t] * jp[v]);
+                }
+            }
+        }
+        __syncthreads();
+    };
+    axis(std::integral_constant<int, 0>{});
+    axis(std::integral_constant<int, 1>{});
+    if constexpr (DIM == 3) axis(std::integral_constant<int, 2>{});
+
+    if (fast) {
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid < 32) {
+            IO::store(p.out + gbase, buf, p.group, contiguous, tid);
+            bulk_wait_read_all();
+        }
+    } else {
+        const R* s0 = reinterpret_cast<const R*>(buf);
+        for (int idx = tid; idx < L::IN_WORDS; idx += BS) {
+            const long long e = E0 + idx % NE;
+            if (e < p.n_elem) {
+                const long long ge = e / p.group;
+                p.out[ge * p.group_words + (e - ge * p.group) + static_cast<long long>(p.group) * (idx / NE)] = s0[idx];
+            }
+        }
+    }
+}
+
 }  // namespace hfb
 
 // ---------------------------------------------------------------------------------------------
@@ -374,10 +534,58 @@ int fr_correct_launch(const Params<R>& prm, const FrParams<R>& fp, cudaStream_t 
     return int(cudaGetLastError());
 }
 
+template <class R, int DIM, int M, int NE>
+int fr_correct_staged_launch(const Params<R>& prm, const FrParams<R>& fp, cudaStream_t st) {
+    using S = FrCorrStagedShape<R, DIM, M, NE>;
+    auto kernel = hf_fr_correct_staged_kernel<R, DIM, M, NE>;
+    Params<R> p = prm;
+    p.fast_ok = (p.group == NE || (p.group % NE == 0 && (NE * sizeof(R)) % 16 == 0 &&
+                                   ((long long)p.group * sizeof(R)) % 16 == 0)) &&
+                (reinterpret_cast<uintptr_t>(p.out) & 15u) == 0;
+    if (S::SMEM > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM));
+        if (e != cudaSuccess) return int(e);
+    }
+    kernel<<<unsigned((p.n_elem + NE - 1) / NE), S::BS, S::SMEM, st>>>(p, fp);
+    return int(cudaGetLastError());
+}
+
+// the chunk follows the caller's AoSoA group (bulk path), <= 72 KB, as stage 1
+template <class R, int DIM, int M, int NE = fr_proj_ne<R, DIM, M>()>
+int fr_correct_staged_dispatch(const Params<R>& prm, const FrParams<R>& fp, cudaStream_t st) {
+    if constexpr (NE > 1) {
+        if (prm.group != NE && prm.group % NE != 0) return fr_correct_staged_dispatch<R, DIM, M, NE / 2>(prm, fp, st);
+    }
+    return fr_correct_staged_launch<R, DIM, M, NE>(prm, fp, st);
+}
+
+template <class R, int DIM, int M>
+int fr_correct_dispatch_jumps(const Params<R>& prm, const FrParams<R>& fp, cudaStream_t st);
+
+// (d, p, precision) where the staged correction wins by > 7 % (same box, 1e7 points,
+// profiles/ext_r01f_fr_staged_{jumps,staged}.jsonl): d2 FP32 p2-p8 (1.09-1.38x), d2 FP64
+// p4-p5 (1.24-1.27x), d3 FP32 p2 and p5 (1.39x, 1.19x); elsewhere the jump-array kernel
+template <class R, int DIM, int M>
+constexpr bool fr_correct_staged() {
+    if constexpr (DIM == 2) return sizeof(R) == 4 ? M >= 3 : (M == 5 || M == 6);
+    else return sizeof(R) == 4 && (M == 3 || M == 6);
+}
+
 template <class R, int DIM, int M>
 int fr_stage(int which, const Params<R>& prm, const FrParams<R>& fp, R* uf, cudaStream_t st) {
     if (prm.n_elem == 0) return 0;
     if (which == 1) return fr_project_dispatch<R, DIM, M>(prm, fp, uf, st);
+#ifdef HF_FR_AB
+    if (const char* ev = std::getenv("HF_FR_STAGED"))
+        return ev[0] == '1' ? fr_correct_staged_dispatch<R, DIM, M>(prm, fp, st)
+                            : fr_correct_dispatch_jumps<R, DIM, M>(prm, fp, st);
+#endif
+    if constexpr (fr_correct_staged<R, DIM, M>()) return fr_correct_staged_dispatch<R, DIM, M>(prm, fp, st);
+    return fr_correct_dispatch_jumps<R, DIM, M>(prm, fp, st);
+}
+
+template <class R, int DIM, int M>
+int fr_correct_dispatch_jumps(const Params<R>& prm, const FrParams<R>& fp, cudaStream_t st) {
     // <= 48 KB of jumps per CTA (occupancy), or <= 96 KB when the AoSoA group is at
     // least that many elements, so that stage 5's point loads cover whole 32-byte
     // sectors and rows (p6: FP32 486 -> 336 us, FP64 832 -> 744 us; p1 FP64, group 64:
