@@ -1,7 +1,7 @@
 """Benchmark driver for the B200 fused flux + divergence kernels.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload config2|config1|config3|config4|config5]
-                    [--impl ours|reference] [--scaling weak|strong] [--no-e2e]
+                    [--impl ours|reference] [--scaling weak|strong] [--no-e2e] [--no-cpu] [--no-parity]
 
 Metric (BASELINE.json): GDoF/s = solution-point updates per second (all n_v
 variables of a point = one update), with the fraction of the HBM roofline of
@@ -13,21 +13,37 @@ on: d=3 hexes, p = 1..6, FP32 and FP64, ~1e7 solution points per (p,
 precision).  One step = one fused launch per (p, precision) = 12 launches over
 resident synthetic inputs (uniform(-1,1), every case's input larger than L2).
 
-Under torchrun (N > 1) each rank owns its own element slice (no data-path
-collective; the NCCL group is only used for the barrier and the max-over-ranks
-of the device time).  `value` is the whole-job aggregate.
+Multi-GPU: one process per GPU.  Under torchrun (WORLD_SIZE set) each rank owns
+its element slice (no data-path collective; NCCL is used only for the barrier,
+the max-over-ranks of the device time and the sum of the points).  Without
+torchrun, ``--gpus N`` (N > 1) re-launches this script under
+``torch.distributed.run`` with N ranks on 127.0.0.1.  `value` is the whole-job
+aggregate.  ``--scaling weak`` (default): every rank runs the full per-case
+problem; ``--scaling strong``: the case's elements are split across the ranks
+(hf_partition, contiguous whole AoSoA groups).
+
+After timing, every rank checks a sample of element groups of every case
+against the CPU oracle (test infrastructure, outside the timed region): the
+first and last group of the field and 30 more spread over it, so the largest
+byte offsets of config 5 (> 4 GB) are covered.  The line carries the worst
+relative error per precision (`parity`).
 
 `--impl reference` times the reference's own CPU implementation
-(hexfuse::oracle_divergence compiled from /root/reference by oracle/Makefile
-into oracle/_ref/libhexfuse_ref.so) on the host cores for a bounded sample of
-the same workload; rank 0 alone runs it.
+(hexfuse::oracle_divergence from /root/reference/proj/include, compiled by
+oracle/Makefile into oracle/_ref; the -O3 -march=x86-64-v4/-v3 timing build the
+host supports) on all host threads for a bounded sample of the same workload.
+That arm never imports the B200 package or touches CUDA: the AoSoA groups come
+from the static GPU_GROUPS table below (checked against the library by
+tests/test_gpu_scale.py).  Rank 0 alone runs it.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -36,6 +52,21 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 L2_BYTES = 126 * 1024 * 1024
+PARITY_GROUPS = 32
+METRIC = "GDoF/s (solution-point updates/sec), fused flux+divergence; roofline = fraction of HBM"
+
+# hf_preferred_group() of the library for every (d, p, precision) a workload uses: the
+# AoSoA group that makes one group one kernel chunk.  Static so that the reference arm
+# can lay its sample out exactly like the GPU's field without loading the B200 library;
+# tests/test_gpu_scale.py checks it against the library.
+GPU_GROUPS = {
+    (3, 1, "fp32"): 64, (3, 2, "fp32"): 32, (3, 3, "fp32"): 4, (3, 4, "fp32"): 4, (3, 5, "fp32"): 1,
+    (3, 6, "fp32"): 4,
+    (3, 1, "fp64"): 64, (3, 2, "fp64"): 8, (3, 3, "fp64"): 2, (3, 4, "fp64"): 1, (3, 5, "fp64"): 1,
+    (3, 6, "fp64"): 2,
+    (2, 1, "fp32"): 128, (2, 2, "fp32"): 64, (2, 3, "fp32"): 32, (2, 4, "fp32"): 16, (2, 5, "fp32"): 16,
+    (2, 6, "fp32"): 16, (2, 7, "fp32"): 16, (2, 8, "fp32"): 8,
+}
 
 
 # ------------------------------------------------------------------------------------------------ workloads
@@ -59,8 +90,30 @@ WORKLOAD_DESC = {
     "config1": "d3 hex p=3 fp64, 32768 elements (BASELINE config 1)",
     "config3": "d2 quad p=1..8 fp32, 1e6 elements per case (BASELINE config 3)",
     "config4": "d3 hex p=4 fp32, ~1e7 points, fused (BASELINE config 4; unfused timed beside it)",
-    "config5": "d3 hex p=3 and p=5 fp64, 1.5e8 points (BASELINE config 5)",
+    "config5": "d3 hex p=3 and p=5 fp64, 1.5e8 points per case (BASELINE config 5)",
 }
+
+
+def case_elements(d, p, precn, target):
+    """(group, whole-problem element count) of one workload case: target points rounded
+    to whole groups."""
+    g = GPU_GROUPS[(d, p, precn)]
+    npt = (p + 1) ** d
+    return g, max(g, int(round(target / npt / g)) * g)
+
+
+def workload_config(workload: str, world: int, scaling: str) -> dict:
+    """The `config` object of the JSON line -- identical for both arms (no device state)."""
+    pts = 0
+    for (d, p, precn, target) in workload_cases(workload):
+        _, n = case_elements(d, p, precn, target)
+        pts += n * (p + 1) ** d
+    if world > 1 and scaling == "weak":
+        pts *= world
+    return {"workload": workload, "description": WORKLOAD_DESC[workload],
+            "cases": len(workload_cases(workload)), "points_per_step": pts,
+            "l2": "no flush; every case's input+output exceeds the 126 MB L2",
+            "parallelism": f"element-partition x{world} ({scaling if world > 1 else 'single GPU'})"}
 
 
 def load_peaks():
@@ -119,7 +172,7 @@ class ClockSampler:
                         self.reasons.add(nm)
             except Exception:
                 pass
-            time.sleep(0.01)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self._ok:
@@ -138,15 +191,125 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+# ------------------------------------------------------------------------------------------------ ranks
+class Ranks:
+    """rank / world / local rank and the three reductions the bench needs.  NCCL
+    reduces device tensors, gloo (the CPU self-test) host tensors."""
+
+    def __init__(self):
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.dev = None
+
+    def init(self, backend: str, device=None):
+        self.dev = device
+        if self.world > 1:
+            import torch.distributed as dist
+            kw = {"device_id": device} if backend == "nccl" else {}
+            dist.init_process_group(backend, **kw)
+
+    def close(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            if dist.is_initialized():
+                dist.destroy_process_group()
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def _reduce(self, x: float, op: str) -> float:
+        if self.world == 1:
+            return float(x)
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([float(x)], dtype=torch.float64, device=self.dev)
+        dist.all_reduce(t, op=getattr(dist.ReduceOp, op))
+        return float(t.item())
+
+    def max(self, x: float) -> float:
+        return self._reduce(x, "MAX")
+
+    def sum(self, x: float) -> float:
+        return self._reduce(x, "SUM")
+
+
+def free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(n: int) -> int:
+    """`bench.py --gpus N` without torchrun: re-launch under torch.distributed.run, one rank
+    per GPU on this node; rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
 # ------------------------------------------------------------------------------------------------ ours
-def run_ours(args, rank, world, local_rank):
+def launches_per_call(info: dict, n_elem: int, group: int, word_bytes: int, total_words: int) -> int:
+    """Kernel launches of one hf_fused_divergence call: the TMA-ring variant runs the full
+    chunks persistently and the partial / allocation-final chunk in a second launch
+    (hf_launch.cuh launch_lines_pipe)."""
+    if not info["name"].startswith("hf_lines_pipe"):
+        return 1
+    ne = info["elems_per_cta"]
+    n_full = n_elem // ne
+    if group == ne and n_full > 0 and n_full * ne == n_elem and (total_words * word_bytes) % 16:
+        n_full -= 1
+    return 1 + (1 if n_full < -(-n_elem // ne) else 0)
+
+
+def parity_sample(hf, cases, rank, n_groups_sample):
+    """Checker (outside the timed region): the fused result of sampled element groups of every
+    case against the CPU oracle (oracle_divergence restated, oracle.hpp:20-62).  Returns the
+    per-case worst relative error (verify.hpp:19-33 definition over the sampled elements)."""
+    import numpy as np
+
+    import oracle as O
+    out = []
+    for ci, c in enumerate(cases):
+        d, p, g = c["d"], c["p"], c["group"]
+        nv, npt = 1 + d + d * d, (p + 1) ** d
+        gw = g * npt * nv
+        n_groups = -(-c["n_elem"] // g)
+        rng = np.random.default_rng(7919 * (rank + 1) + ci)
+        pick = {0, n_groups - 1}
+        if n_groups > 2:
+            pick |= set(int(x) for x in rng.choice(np.arange(1, n_groups - 1),
+                                                   size=min(n_groups - 2, n_groups_sample - 2), replace=False))
+        maxdiff, maxref = 0.0, 0.0
+        for gi in sorted(pick):
+            n_e = min(g, c["n_elem"] - gi * g)
+            U = c["u"][gi * gw:(gi + 1) * gw].double().cpu().numpy()
+            got = c["o"][gi * gw:(gi + 1) * gw].double().cpu().numpy()
+            ref = O.oracle_divergence(d, p, n_e, g, U, 1.0 / 1600.0, 2.5, 1.0)
+            real = (np.arange(g) < n_e)[None, None, :]
+            a = got.reshape(nv, npt, g)
+            b = ref.reshape(nv, npt, g)
+            diff = np.where(real, np.abs(a - b), 0.0)
+            if not np.all(np.isfinite(diff)):
+                maxdiff = float("inf")
+            maxdiff = max(maxdiff, float(diff.max()))
+            maxref = max(maxref, float(np.where(real, np.abs(b), 0.0).max()))
+        out.append({"groups": len(pick), "last_byte_offset": (n_groups * gw) * c["u"].element_size(),
+                    "max_rel_err": maxdiff / max(1.0, maxref)})
+    return out
+
+
+def run_ours(args, R: Ranks):
     import torch
-    import torch.distributed as dist
 
     import paper_2107_14027_b200 as hf
-    from paper_2107_14027_b200 import Method, PhysParams, Precision
+    from paper_2107_14027_b200 import PhysParams, Precision
 
-    torch.cuda.set_device(local_rank)
+    rank, world, local_rank = R.rank, R.world, R.local
     dev = torch.device("cuda", local_rank)
     par = PhysParams(1.0 / 1600.0, 2.5, 1.0)
     peak, peak_src = load_peaks()
@@ -157,11 +320,14 @@ def run_ours(args, rank, world, local_rank):
     cases = []
     gen = torch.Generator(device=dev)
     gen.manual_seed(2024 + rank)
+    launches = 0
     for (d, p, precn, target) in workload_cases(args.workload):
         prec = Precision[precn]
-        g = hf.preferred_group(hf.make_problem(d, p, 1, 1, prec, par))
+        g, n_total = case_elements(d, p, precn, target)
+        lib_g = hf.preferred_group(hf.make_problem(d, p, 1, 1, prec, par))
+        if lib_g != g:
+            raise SystemExit(f"bench.py GPU_GROUPS[{(d, p, precn)}] = {g} but the library prefers {lib_g}")
         npt = (p + 1) ** d
-        n_total = max(g, int(round(target / npt / g)) * g)
         if world > 1 and args.scaling == "strong":
             full = hf.make_problem(d, p, n_total, g, prec, par)
             _, n_elem, _ = hf.partition(full, world, rank)
@@ -175,6 +341,7 @@ def run_ours(args, rank, world, local_rank):
         o = torch.empty_like(u)
         wb = 4 if prec == Precision.fp32 else 8
         info = hf.kernel_info(pr)
+        launches += launches_per_call(info, n_elem, g, wb, words)
         cases.append({"d": d, "p": p, "precision": precn, "pr": pr, "u": u, "o": o, "n_elem": n_elem,
                       "points": n_elem * npt, "alg_bytes": n_elem * npt * 2 * hf.n_vars(d) * wb,
                       "kernel": info["name"], "group": g, "info": info})
@@ -188,10 +355,6 @@ def run_ours(args, rank, world, local_rank):
             if record is not None:
                 record[i][1].record(st)
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -201,26 +364,18 @@ def run_ours(args, rank, world, local_rank):
           for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
-        barrier()
+        R.barrier()
         torch.cuda.synchronize()
         t0.record(st)
         for k in range(args.steps):
             step(ev[k])
         t1.record(st)
         torch.cuda.synchronize()
-        barrier()
-    elapsed = t0.elapsed_time(t1) * 1e-3
+        R.barrier()
+    elapsed = R.max(t0.elapsed_time(t1) * 1e-3)
     per_case = [[ev[k][i][0].elapsed_time(ev[k][i][1]) * 1e-3 for k in range(args.steps)] for i in range(len(cases))]
-    if world > 1:
-        tt = torch.tensor([elapsed], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed = float(tt.item())
     points_rank = sum(c["points"] for c in cases)
-    points_all = points_rank * world if not (world > 1 and args.scaling == "strong") else None
-    if points_all is None:
-        pt = torch.tensor([float(points_rank)], device=dev, dtype=torch.float64)
-        dist.all_reduce(pt, op=dist.ReduceOp.SUM)
-        points_all = float(pt.item())
+    points_all = R.sum(points_rank)
     value = points_all * args.steps / elapsed / 1e9
 
     # ---- per-case roofline, dominant kernel
@@ -276,31 +431,23 @@ def run_ours(args, rank, world, local_rank):
         # (hf_fused_divergence_host_batch: fill before the first case, drain after the last)
         batch = [(pr_e, hu, ho) for hu, ho, pr_e, _ in hosts]
         ctx.run_batch(batch)  # warm (allocates the context's slots)
-        barrier()
+        R.barrier()
         ta = time.perf_counter()
         for _ in range(e2e_steps):
             ctx.run_batch(batch)
         tb = time.perf_counter()
-        barrier()
-        te = tb - ta
-        if world > 1:
-            tt = torch.tensor([te], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt.item())
-        pts_e = sum(h[3] for h in hosts) * (world if not (world > 1 and args.scaling == "strong") else 1)
-        if world > 1 and args.scaling == "strong":
-            pt = torch.tensor([float(sum(h[3] for h in hosts))], device=dev, dtype=torch.float64)
-            dist.all_reduce(pt, op=dist.ReduceOp.SUM)
-            pts_e = float(pt.item())
+        R.barrier()
+        te = R.max(tb - ta)
+        pts_e = R.sum(sum(h[3] for h in hosts))
         h2d = sum(h[0].numel() * h[0].element_size() for h in hosts)
         e2e = {"value": round(pts_e * e2e_steps / te / 1e9, 4), "unit": "GDoF/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d, "steps": e2e_steps,
                "path": "hf_fused_divergence_host_batch (pinned host buffers, one 3-stream slice pipeline per step)"}
         if frac < 1.0:
             e2e["sample"] = f"each case cut to {frac:.3f} of its elements (host RAM {host_ram / 2**30:.0f} GiB)"
-        # the first e2e step's result must equal the device-resident run's result
+        # the e2e result must equal the device-resident run's result
         same = all(torch.equal(h[1].to(dev), c["o"][: h[1].numel()]) for h, c in zip(hosts, cases))
-        e2e["matches_device_result"] = bool(same)
+        e2e["matches_device_result"] = bool(R.sum(0.0 if same else 1.0) == 0.0)
         ctx.close()
         del hosts
 
@@ -319,29 +466,49 @@ def run_ours(args, rank, world, local_rank):
         b.record(st)
         torch.cuda.synchronize()
         tu = a.elapsed_time(b) * 1e-3 / args.steps
+        ubytes = c["points"] * 8 * hf.n_vars(c["d"]) * c["u"].element_size()  # io_model S2+S3, io_model.hpp:32-33
         unfused = {"us_per_step": round(tu * 1e6, 2), "gdofs": round(c["points"] / tu / 1e9, 3),
+                   "alg_bytes_per_point": 8 * hf.n_vars(c["d"]) * c["u"].element_size(),
+                   "achieved_GBps": round(ubytes / tu / 1e9, 1), "frac": round(ubytes / tu / 1e9 / peak, 4),
                    "fused_speedup": round(tu / (case_rows[0]["us_per_launch"] * 1e-6), 3),
                    "model_speedup": 4.0}
+        step()  # the parity check below reads the fused result
+        torch.cuda.synchronize()
+
+    # ---- parity (checker, after timing): sampled groups of every case against the CPU oracle
+    parity = None
+    if not args.no_parity:
+        rows = parity_sample(hf, cases, rank, PARITY_GROUPS)
+        worst = {}
+        for c, r, cr in zip(cases, rows, case_rows):
+            cr["parity_rel_err"] = float(f"{r['max_rel_err']:.3e}")
+            worst[c["precision"]] = max(worst.get(c["precision"], 0.0), r["max_rel_err"])
+        worst = {k: R.max(v) for k, v in sorted(worst.items())}
+        tol = {"fp32": 1e-5, "fp64": 1e-12}
+        parity = {"max_rel_err": {k: float(f"{v:.3e}") for k, v in worst.items()},
+                  "tol": {k: tol[k] for k in worst}, "ok": all(v <= tol[k] for k, v in worst.items()),
+                  "groups_per_case": min(PARITY_GROUPS, min(r["groups"] for r in rows)),
+                  "max_byte_offset": max(r["last_byte_offset"] for r in rows),
+                  "oracle": "oracle_divergence (oracle.hpp:20-62) restated in oracle/hexfuse_oracle.c, "
+                            "first + last + 30 random element groups per case and rank"}
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args, n_threads=args.cpu_threads)
 
     if rank == 0:
         line = {
-            "metric": "GDoF/s (solution-point updates/sec), fused flux+divergence; roofline = fraction of HBM",
+            "metric": METRIC,
             "value": round(value, 4), "unit": "GDoF/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(elapsed / args.steps * 1e3, 4),
             "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f32+f64" if args.workload in ("config2",) else
             ("f64" if all(c["precision"] == "fp64" for c in cases) else "f32"),
             "data": "synthetic uniform(-1,1) fields, resident in HBM",
-            "config": {"workload": args.workload, "description": WORKLOAD_DESC[args.workload],
-                       "cases": len(cases), "points_per_rank_per_step": points_rank,
-                       "l2": "no flush; every case's input+output (>=0.4 GB) exceeds the 126 MB L2",
-                       "method": "auto (measured selection table)", "parallelism": f"element-partition x{world}"},
-            "roofline": roofline, "cases": case_rows, "e2e": e2e, "cpu_baseline": cpu,
-            "gpu_launches": args.steps * len(cases), "clocks": clk.summary(),
+            "config": workload_config(args.workload, world, args.scaling),
+            "method": "auto (measured selection table)",
+            "roofline": roofline, "cases": case_rows, "e2e": e2e, "parity": parity, "cpu_baseline": cpu,
+            "gpu_launches": args.steps * launches, "clocks": clk.summary(),
         }
         if unfused:
             line["unfused"] = unfused
@@ -349,19 +516,18 @@ def run_ours(args, rank, world, local_rank):
 
 
 # ------------------------------------------------------------------------------------------------ reference CPU
-def cpu_sample_cases(args, budget_points):
-    """Bounded, group-aligned sample of every case of the workload (same d, p, precision, group)."""
-    import oracle as O  # noqa: F401  (test infrastructure: the CPU baseline leg only)
-    from paper_2107_14027_b200 import PhysParams, Precision
-    import paper_2107_14027_b200 as hf
-    par = PhysParams(1.0 / 1600.0, 2.5, 1.0)
+def cpu_sample_cases(workload: str, budget_points: float):
+    """Bounded, group-aligned sample of every case of the workload (same d, p, precision and
+    AoSoA group as the GPU's field), each case's share proportional to its points in the
+    GPU workload."""
+    cases = workload_cases(workload)
+    sizes = [case_elements(d, p, precn, t)[1] * (p + 1) ** d for (d, p, precn, t) in cases]
+    tot = float(sum(sizes))
     out = []
-    cases = workload_cases(args.workload)
-    for (d, p, precn, target) in cases:
-        prec = Precision[precn]
-        g = hf.preferred_group(hf.make_problem(d, p, 1, 1, prec, par))
+    for (d, p, precn, _), sz in zip(cases, sizes):
+        g = GPU_GROUPS[(d, p, precn)]
         npt = (p + 1) ** d
-        n = max(g, int(budget_points / len(cases) / npt) // g * g)
+        n = max(g, int(budget_points * sz / tot / npt) // g * g)
         out.append((d, p, precn, g, n))
     return out
 
@@ -371,13 +537,20 @@ def ref_supports(d, p):
     return p + 1 <= 8
 
 
-def time_cpu_case(kind, d, p, g, n, fp32, U, n_threads):
-    """Seconds for the CPU oracle over elements [0, n): the compiled reference on n_threads
-    threads, or (outside the reference's domain, or without it) the C restatement on one."""
+def cpu_threads(requested):
     import oracle as O
+    return requested if requested and requested > 0 else O.host_cpu()["logical_cpus"]
+
+
+def time_cpu_case(kind, d, p, g, n, fp32, U, n_threads):
+    """Seconds for the CPU oracle over elements [0, n): the reference's timing build on n_threads
+    threads, or (outside the reference's domain, or without it) the C restatement on one."""
     import numpy as np
+
+    import oracle as O
     if kind == "reference" and ref_supports(d, p):
-        t, _ = O.ref_time_oracle_mt(d, p, n, g, fp32, U, 1.0 / 1600.0, 2.5, 1.0, (1.0, 1.0, 1.0), False, n_threads)
+        t, _ = O.ref_time_oracle_mt(d, p, n, g, fp32, U, 1.0 / 1600.0, 2.5, 1.0, (1.0, 1.0, 1.0), False, n_threads,
+                                    timing_build=True)
         return t
     out = np.zeros_like(U)
     ta = time.perf_counter()
@@ -385,42 +558,64 @@ def time_cpu_case(kind, d, p, g, n, fp32, U, n_threads):
     return time.perf_counter() - ta
 
 
+def sample_field(kind, d, p, n, g, fp32):
+    import oracle as O
+    if kind == "reference" and ref_supports(d, p):
+        return O.ref_random_field_timing(d, p, n, g, fp32, 2024)  # hexfuse::random_field, oracle.hpp:154-166
+    return O.random_field(d, p, n, g, fp32, 2024)
+
+
+def cpu_kind():
+    import oracle as O
+    try:
+        O.ref_timing()
+        return "reference"
+    except Exception:
+        return "port"
+
+
+def cpu_desc(kind, n_threads):
+    import oracle as O
+    hc = O.host_cpu()
+    build = O.ref_timing()[1] if kind == "reference" else "C restatement -O2 (1 thread)"
+    return hc, build
+
+
 def cpu_baseline(args, n_threads=None, budget_points=None):
     """The reference oracle (oracle/_ref) on the host cores, bounded sample; returns the cpu_baseline dict."""
-    import oracle as O
-    if n_threads is None or n_threads <= 0:
-        n_threads = os.cpu_count() or 1
-    kind = "reference" if O.ref_available() else "port"
+    kind = cpu_kind()
+    n_threads = cpu_threads(n_threads) if kind == "reference" else 1
     if budget_points is None:  # ~10 s of reference CPU work at ~4e5 points/s/thread, capped for host memory
-        budget_points = min(3e7, 10.0 * 4e5 * (n_threads if kind == "reference" else 1))
-    if kind != "reference":
-        n_threads = 1
+        budget_points = min(3e7, 10.0 * 4e5 * n_threads)
     tot_pts, tot_s, ported = 0, 0.0, []
-    for (d, p, precn, g, n) in cpu_sample_cases(args, budget_points):
+    for (d, p, precn, g, n) in cpu_sample_cases(args.workload, budget_points):
         fp32 = precn == "fp32"
-        U = O.random_field(d, p, n, g, fp32, 2024)
+        U = sample_field(kind, d, p, n, g, fp32)
         tot_s += time_cpu_case(kind, d, p, g, n, fp32, U, n_threads)
         tot_pts += n * (p + 1) ** d
         if kind == "reference" and not ref_supports(d, p):
             ported.append(f"d{d} p{p}")
+    hc, build = cpu_desc(kind, n_threads)
     note = (f"; {', '.join(ported)} lie outside the reference's domain (m <= 8, operators.hpp:18) and were "
             "timed with the C restatement on one thread") if ported else ""
     return {"value": round(tot_pts / tot_s / 1e9, 6), "unit": "GDoF/s", "cores": n_threads, "kind": kind,
-            "sample": f"{tot_pts} points across every case of {args.workload} (group-aligned element prefixes, "
-                      f"seed 2024), hexfuse::oracle_divergence -O3 on {n_threads} threads, "
-                      f"{tot_s:.1f} s of CPU work{note}", "seconds": round(tot_s, 3)}
+            "cpu_model": hc["model"], "host_logical_cpus": hc["logical_cpus"], "build": build,
+            "sample": f"{tot_pts} points across every case of {args.workload} (group-aligned element prefixes "
+                      f"in the GPU's AoSoA groups, each case's share proportional to its points, seed 2024), "
+                      f"hexfuse::oracle_divergence {build} on {n_threads} threads, {tot_s:.1f} s of CPU work{note}",
+            "seconds": round(tot_s, 3)}
 
 
-def run_reference(args, rank):
-    if rank != 0:
+def run_reference(args, R: Ranks):
+    """The reference arm: rank 0 alone; no B200 package, no CUDA."""
+    if R.rank != 0:
         return
-    import oracle as O
-    n_threads = args.cpu_threads if args.cpu_threads and args.cpu_threads > 0 else (os.cpu_count() or 1)
-    # size each step so the whole --steps K --warmup W run does ~3e7 points of reference CPU work
-    per_step = max(2e5, 3e7 / max(1, args.steps + args.warmup))
-    samples = cpu_sample_cases(args, per_step)
-    kind = "reference" if O.ref_available() else "port"
-    fields = [(d, p, precn, g, n, O.random_field(d, p, n, g, precn == "fp32", 2024)) for (d, p, precn, g, n) in samples]
+    kind = cpu_kind()
+    n_threads = cpu_threads(args.cpu_threads) if kind == "reference" else 1
+    # size each step so the whole --steps K --warmup W run does --ref-budget points of reference CPU work (~8 s)
+    per_step = max(2e4, args.ref_budget / max(1, args.steps + args.warmup))
+    samples = cpu_sample_cases(args.workload, per_step)
+    fields = [(d, p, precn, g, n, sample_field(kind, d, p, n, g, precn == "fp32")) for (d, p, precn, g, n) in samples]
 
     def one_step():
         pts, secs = 0, 0.0
@@ -437,19 +632,43 @@ def run_reference(args, rank):
         P += a
         S += b
     value = P / S / 1e9
-    line = {"impl": "reference", "metric": "GDoF/s (solution-point updates/sec), fused flux+divergence; "
-                                           "roofline = fraction of HBM",
+    hc, build = cpu_desc(kind, n_threads)
+    line = {"impl": "reference", "metric": METRIC,
             "value": round(value, 6), "unit": "GDoF/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(S / args.steps * 1e3, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic mt19937_64 uniform(-1,1) fields (random_field, oracle.hpp:154-166)",
-            "config": {"workload": args.workload, "description": WORKLOAD_DESC[args.workload],
-                       "sample_points_per_step": int(P / args.steps)},
+            "scaling": args.scaling if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic mt19937_64 uniform(-1,1) fields (hexfuse::random_field, oracle.hpp:154-166)",
+            "config": workload_config(args.workload, args.gpus, args.scaling),
             "cpu_baseline": {"value": round(value, 6), "unit": "GDoF/s", "cores": n_threads, "kind": kind,
+                             "cpu_model": hc["model"], "host_logical_cpus": hc["logical_cpus"], "build": build,
                              "sample": f"{int(P / args.steps)} points per step across every case of "
-                                       f"{args.workload}, hexfuse::oracle_divergence (reference headers, -O3)"},
+                                       f"{args.workload} (the GPU's AoSoA groups, each case's share proportional "
+                                       f"to its points), hexfuse::oracle_divergence ({build}) on {n_threads} "
+                                       "threads, one contiguous group-aligned sub-field per thread"},
             "e2e": {"value": round(value, 6), "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------ self-test
+def run_selftest(args, R: Ranks):
+    """CPU self-test of the multi-rank plumbing (HF_BENCH_SELFTEST=1, gloo): the launch, the
+    barriers and the max / sum reductions of the real run, with every rank's device work
+    replaced by a sleep of (rank + 1) * 10 ms per step.  Prints a line marked "selftest"."""
+    per_rank_points = 1000 * (R.rank + 1)
+    R.barrier()
+    ta = time.perf_counter()
+    for _ in range(args.steps):
+        time.sleep(0.01 * (R.rank + 1))
+    own = time.perf_counter() - ta
+    R.barrier()
+    elapsed = R.max(own)
+    pts = R.sum(per_rank_points)
+    if R.rank == 0:
+        print(json.dumps({"selftest": True, "metric": METRIC, "value": pts * args.steps / elapsed / 1e9,
+                          "unit": "GDoF/s", "n_gpus": R.world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": elapsed / args.steps * 1e3, "rank0_ms_per_step": own / args.steps * 1e3,
+                          "points_all": pts, "config": workload_config(args.workload, R.world, args.scaling)}),
+              flush=True)
 
 
 def main():
@@ -462,31 +681,37 @@ def main():
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--ref-budget", type=float, default=1e8, help="reference arm: points of CPU work per run")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-
+    R = Ranks()
+    selftest = os.environ.get("HF_BENCH_SELFTEST") == "1"
     if args.impl == "reference":
-        run_reference(args, rank)
+        run_reference(args, R)
         return
-
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args.gpus))
+    if selftest:
+        R.init("gloo")
+        try:
+            run_selftest(args, R)
+        finally:
+            R.close()
+        return
+    import torch
+    if R.world > 1 and torch.cuda.device_count() < R.world:
+        raise SystemExit(f"bench.py: {R.world} ranks but {torch.cuda.device_count()} visible GPUs")
+    torch.cuda.set_device(R.local)
+    R.init("nccl", torch.device("cuda", R.local))
     try:
-        run_ours(args, rank, world, local_rank)
+        run_ours(args, R)
     finally:
-        if world > 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
+        R.close()
 
 
 if __name__ == "__main__":

@@ -135,8 +135,9 @@ HF_API int hf_mapped_kernel_info(const hf_problem* pr, hf_kernel_info* out);
  * elements, element e = ex + dims[0]*(ey + dims[1]*ez), the constant per-axis
  * Jacobian pr->jac (the reference models these stages' I/O only):
  *   hf_fr_project   stage 1: U_f = every a-line extrapolated to xi_a = -1, +1;
- *   hf_fr_correct   stages 4+5: Rusanov common flux (wave speed
- *                   |V_a| + sqrt(V_a^2 + zeta + nu/T)) and the DG correction
+ *   hf_fr_correct   stages 4+5: common flux (Rusanov on the
+ *                   pressure / velocity rows, wave speed |V_a| + sqrt(V_a^2 + zeta);
+ *                   the mean of both sides on the gradient rows) and the DG correction
  *                   -sum_a jac_a (g_L' jump_(-a) + g_R' jump_(+a)) added in place
  *                   to divf_dev, which holds hf_fused_divergence's result;
  *   hf_fr_divergence_faces  stages 1+2+3+6 in one pass: the fused kernel also

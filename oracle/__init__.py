@@ -114,6 +114,55 @@ def ref_available() -> bool:
     return os.path.exists(_REF_SO)
 
 
+def host_cpu() -> dict:
+    """Model name, logical CPUs usable by this process and the ISA flags of the host."""
+    model, flags = "unknown", set()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name") and model == "unknown":
+                    model = line.split(":", 1)[1].strip()
+                elif line.startswith("flags") and not flags:
+                    flags = set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    return {"model": model, "logical_cpus": usable, "flags": flags}
+
+
+_V3 = {"avx", "avx2", "bmi1", "bmi2", "f16c", "fma", "movbe", "xsave"}
+_V4 = _V3 | {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"}
+_timing = None
+
+
+def ref_timing():
+    """(library, build description) for TIMING the reference's oracle_divergence on this
+    host: the -O3 -march=x86-64-v4 / -v3 build of the same shim (what -march=native gives
+    on an AVX-512 / AVX2 host), else the portable parity build.  Never used for parity."""
+    global _timing
+    if _timing is None:
+        flags = host_cpu()["flags"]
+        path, desc = _REF_SO, "-O3 -ffp-contract=off (portable parity build)"
+        for isa, need in (("x86-64-v4", _V4), ("x86-64-v3", _V3)):
+            cand = os.path.join(_REF_DIR, f"libhexfuse_ref_{isa}.so")
+            if need <= flags and os.path.exists(cand):
+                path, desc = cand, f"-O3 -march={isa}"
+                break
+        if not os.path.exists(path):
+            raise RuntimeError("oracle/_ref/libhexfuse_ref*.so missing (reference tree absent at build time)")
+        R = C.CDLL(path)
+        R.ref_last_error.restype = C.c_char_p
+        R.ref_random_field.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_ulonglong, _dp]
+        R.ref_time_oracle_mt.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_double,
+                                         C.c_double, C.c_double, _dp, C.c_int, C.c_int]
+        R.ref_time_oracle_mt.restype = C.c_double
+        _timing = (R, desc)
+    return _timing
+
+
 def ref() -> C.CDLL:
     """The reference's own oracle (compiled in place).  Raises if never built."""
     global _ref
@@ -392,15 +441,28 @@ def ref_oracle_divergence(d, p, n_elem, group, fp32, U, nu, zeta, T, jac=(1.0, 1
 
 
 def ref_time_oracle_mt(d, p, n_elem, group, fp32, U, nu, zeta, T, jac=(1.0, 1.0, 1.0), with_source=False,
-                       n_threads=1):
-    """Returns (seconds, out) for the reference oracle run on n_threads group-aligned sub-fields."""
+                       n_threads=1, timing_build=False):
+    """Returns (seconds, out) for the reference oracle run on n_threads group-aligned sub-fields
+    (timing_build: the -march build of ref_timing() instead of the parity build)."""
+    R = ref_timing()[0] if timing_build else ref()
     U = np.ascontiguousarray(U, dtype=np.float64)
     out = np.zeros_like(U)
-    t = ref().ref_time_oracle_mt(d, p, n_elem, group, int(fp32), U, out, nu, zeta, T,
-                                 np.array(jac, dtype=np.float64), int(with_source), n_threads)
+    t = R.ref_time_oracle_mt(d, p, n_elem, group, int(fp32), U, out, nu, zeta, T,
+                             np.array(jac, dtype=np.float64), int(with_source), n_threads)
     if t < 0:
-        raise RuntimeError(ref().ref_last_error().decode())
+        raise RuntimeError(R.ref_last_error().decode())
     return t, out
+
+
+def ref_random_field_timing(d, p, n_elem, group, fp32, seed) -> np.ndarray:
+    """hexfuse::random_field through the timing build (no other library loaded)."""
+    R = ref_timing()[0]
+    nv = 1 + d + d * d
+    words = -(-n_elem // group) * group * (p + 1) ** d * nv
+    out = np.zeros(words)
+    if R.ref_random_field(d, p, n_elem, group, int(fp32), seed, out) != 0:
+        raise ValueError(R.ref_last_error().decode())
+    return out
 
 
 def ref_gl_derivative(m: int):

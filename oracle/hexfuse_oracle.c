@@ -547,11 +547,15 @@ HFO_EXPORT int hfo_oracle_divergence_mapped(int d, int p, int n_elem, int group,
  *
  *   stage 1 (M)  U_f = the a-lines of every element extrapolated to xi_a = -1, +1
  *                (Lagrange basis on the Gauss-Legendre nodes at +-1);
- *   stage 4 (I)  Rusanov common flux at every face point, normal +x_a:
+ *   stage 4 (I)  common flux at every face point, normal +x_a, as PAPER.md:856
+ *                sets it up for ACM-HD: a Rusanov solver for the hyperbolic
+ *                (pressure, velocity) rows,
  *                F^I = (F_a(UL) + F_a(UR))/2 - lambda (UR - UL)/2,
- *                lambda = max over UL, UR of |V_a| + sqrt(V_a^2 + zeta + nu/T)
- *                (the spectral radius of flux_jacobian, equations.hpp:112-140;
- *                pinned against the reference's own eigenvalues, eig.hpp);
+ *                lambda = max over UL, UR of |V_a| + sqrt(V_a^2 + zeta)
+ *                (the inviscid ACM spectral radius: the reference's flux_jacobian
+ *                eigenvalues at nu = 0, equations.hpp:112-140 + eig.hpp, pinned),
+ *                and the mean (F_a(UL) + F_a(UR))/2 for the d^2 additional
+ *                (gradient) equations;
  *   stage 5 (M)  DG correction: div^c = div^D + sum_a jac_a (g_L'(xi) (F^I - F^D)_(-a face)
  *                                              + g_R'(xi) (F^I - F^D)_(+a face)),
  *                g_L = (-1)^m/2 (P_m - P_{m-1}) (right Radau), g_R(x) = g_L(-x);
@@ -625,14 +629,18 @@ HFO_EXPORT int hfo_correction_derivs(int m, double *gl, double *gr) {
     return 0;
 }
 
-/* |V_a| + sqrt(V_a^2 + zeta + nu/T): spectral radius of the normal flux Jacobian. */
+/* |V_a| + sqrt(V_a^2 + zeta): spectral radius of the inviscid (nu = 0) normal flux Jacobian,
+ * the wave speed of the Rusanov solver for the hyperbolic rows. */
 HFO_EXPORT double hfo_max_wavespeed(int d, const double *s, int a, double nu, double zeta, double T) {
     (void)d;
+    (void)nu;
+    (void)T;
     const double u = s[1 + a];
-    return fabs(u) + sqrt(u * u + zeta + nu / T);
+    return fabs(u) + sqrt(u * u + zeta);
 }
 
-/* Rusanov common flux, normal +x_a (all n_v rows). */
+/* Common flux, normal +x_a: Rusanov on the 1+d pressure / velocity rows, the mean of the
+ * two sides on the d^2 gradient rows. */
 HFO_EXPORT void hfo_common_flux(int d, const double *UL, const double *UR, int a, double nu, double zeta, double T,
                                 double *FI) {
     const int nv = 1 + d + d * d;
@@ -641,7 +649,10 @@ HFO_EXPORT void hfo_common_flux(int d, const double *UL, const double *UR, int a
     hfo_flux(d, UR, nu, zeta, T, fr);
     const double ll = hfo_max_wavespeed(d, UL, a, nu, zeta, T), lr = hfo_max_wavespeed(d, UR, a, nu, zeta, T);
     const double lam = ll > lr ? ll : lr;
-    for (int v = 0; v < nv; ++v) FI[v] = 0.5 * (fl[a * nv + v] + fr[a * nv + v]) - 0.5 * lam * (UR[v] - UL[v]);
+    for (int v = 0; v < nv; ++v) {
+        FI[v] = 0.5 * (fl[a * nv + v] + fr[a * nv + v]);
+        if (v < 1 + d) FI[v] -= 0.5 * lam * (UR[v] - UL[v]);
+    }
 }
 
 /* Stage 1 over elements [e_begin, e_end). */

@@ -139,18 +139,53 @@ int validate(const hf_problem* pr) {
 // Selection
 // ---------------------------------------------------------------------------------------------
 
+// AUTO takes the measured row of the selection table; an explicit LINES request takes the
+// row's measured lines variant too (variant 0 when the row selected another method).
 void select_method(const hf_problem* pr, int* method, int* variant) {
     *variant = 0;
-    if (pr->method != HF_METHOD_AUTO) {
-        *method = pr->method;
-        return;
-    }
-    *method = HF_METHOD_LINES;
+    *method = pr->method != HF_METHOD_AUTO ? pr->method : HF_METHOD_LINES;
     for (const hfb::SelRow& r : hfb::kSelect)
         if (r.d == pr->d && r.p == pr->p && r.prec == pr->precision) {
-            *method = r.method;
-            *variant = r.variant;
+            if (pr->method == HF_METHOD_AUTO) {
+                *method = r.method;
+                *variant = r.variant;
+            } else if (pr->method == HF_METHOD_LINES && r.method == HF_METHOD_LINES) {
+                *variant = r.variant;
+            }
         }
+}
+
+// Restores the caller's current device on every return path of an entry point that
+// has to switch devices.
+struct DeviceGuard {
+    int prev = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// Mesh / partition checks of the FR stages (before anything is launched).
+int check_mesh(const hf_problem* pr, const hf_mesh* mesh, const void* ghost_lo, const void* ghost_hi,
+               const char* who) {
+    if (!mesh) return fail(HF_EINVAL, std::string(who) + ": null mesh");
+    const int64_t nz = pr->d == 3 ? mesh->dims[2] : 1;
+    if (mesh->dims[0] < 1 || mesh->dims[1] < 1 || nz < 1) return fail(HF_EINVAL, std::string(who) + ": bad mesh dims");
+    const int64_t n_mesh = int64_t(mesh->dims[0]) * mesh->dims[1] * nz;
+    if (mesh->n_local != pr->n_elem || mesh->e_begin < 0 || mesh->e_begin + mesh->n_local > n_mesh)
+        return fail(HF_EINVAL, std::string(who) + ": partition must be n_elem elements inside the mesh");
+    if (mesh->n_local < n_mesh) {
+        const int64_t layer = pr->d == 3 ? int64_t(mesh->dims[0]) * mesh->dims[1] : mesh->dims[0];
+        if (mesh->layer != layer || mesh->e_begin % layer || mesh->n_local % layer || !ghost_lo || !ghost_hi)
+            return fail(HF_EINVAL,
+                        std::string(who) + ": a partition must be whole element layers with both ghost layers");
+    }
+    return HF_OK;
 }
 
 template <class R>
@@ -452,17 +487,7 @@ int hf_fr_project(const hf_problem* pr, const void* u_dev, void* uf_dev, void* s
 int hf_fr_correct(const hf_problem* pr, const hf_mesh* mesh, const void* uf_dev, const void* ghost_lo,
                   const void* ghost_hi, void* divf_dev, void* stream) {
     if (int rc = validate(pr)) return rc;
-    if (!mesh) return fail(HF_EINVAL, "hf_fr_correct: null mesh");
-    const int64_t nz = pr->d == 3 ? mesh->dims[2] : 1;
-    if (mesh->dims[0] < 1 || mesh->dims[1] < 1 || nz < 1) return fail(HF_EINVAL, "hf_fr_correct: bad mesh dims");
-    const int64_t n_mesh = int64_t(mesh->dims[0]) * mesh->dims[1] * nz;
-    if (mesh->n_local != pr->n_elem || mesh->e_begin < 0 || mesh->e_begin + mesh->n_local > n_mesh)
-        return fail(HF_EINVAL, "hf_fr_correct: partition must be n_elem elements inside the mesh");
-    if (mesh->n_local < n_mesh) {
-        const int64_t layer = pr->d == 3 ? int64_t(mesh->dims[0]) * mesh->dims[1] : mesh->dims[0];
-        if (mesh->layer != layer || mesh->e_begin % layer || mesh->n_local % layer || !ghost_lo || !ghost_hi)
-            return fail(HF_EINVAL, "hf_fr_correct: a partition must be whole element layers with both ghost layers");
-    }
+    if (int rc = check_mesh(pr, mesh, ghost_lo, ghost_hi, "hf_fr_correct")) return rc;
     if (pr->n_elem > 0 && (!uf_dev || !divf_dev)) return fail(HF_EINVAL, "hf_fr_correct: null buffer");
     int rc;
     if (pr->precision == HF_FP32) {
@@ -511,9 +536,10 @@ int hf_fr_residual(const hf_problem* pr, const int* dims, const void* u_dev, voi
     ms.e_begin = 0;
     ms.n_local = pr ? pr->n_elem : 0;
     ms.layer = 0;
-    if (pr && int64_t(ms.dims[0]) * ms.dims[1] * ms.dims[2] != pr->n_elem)
-        return fail(HF_EINVAL, "hf_fr_residual: n_elem must equal the mesh's element count");
     if (int rc = validate(pr)) return rc;
+    if (ms.dims[0] < 1 || ms.dims[1] < 1 || ms.dims[2] < 1 || int64_t(ms.dims[0]) * ms.dims[1] * ms.dims[2] != pr->n_elem)
+        return fail(HF_EINVAL, "hf_fr_residual: dims must be >= 1 with product n_elem");
+    if (int rc = check_mesh(pr, &ms, nullptr, nullptr, "hf_fr_residual")) return rc;  // before any launch
     if (pr->n_elem > 0 && (!u_dev || !uf_dev || !divf_dev)) return fail(HF_EINVAL, "hf_fr_residual: null buffer");
     if (u_dev == divf_dev && pr->n_elem > 0) return fail(HF_EINVAL, "hf_fr_residual: in-place not supported");
     if (int rc = hf_fr_divergence_faces(pr, u_dev, uf_dev, divf_dev, stream)) return rc;  // stages 1+2+3+6
@@ -664,6 +690,7 @@ hf_context* hf_context_create(int device) {
     auto* c = new (std::nothrow) hf_context;
     if (!c) return nullptr;
     c->device = device;
+    DeviceGuard guard;
     cudaError_t e = cudaSetDevice(device);
     for (int s = 0; s < hf_context::kSlots && e == cudaSuccess; ++s) {
         e = cudaStreamCreateWithFlags(&c->stream[s], cudaStreamNonBlocking);
@@ -679,6 +706,7 @@ hf_context* hf_context_create(int device) {
 
 void hf_context_destroy(hf_context* c) {
     if (!c) return;
+    DeviceGuard guard;
     cudaSetDevice(c->device);
     for (int s = 0; s < hf_context::kSlots; ++s) {
         if (c->stream[s]) cudaStreamSynchronize(c->stream[s]);
@@ -704,6 +732,19 @@ int hf_fused_divergence_host_batch(hf_context* c, int n_fields, const hf_problem
         if (prs[i].n_elem > 0 && (!u_hosts[i] || !divf_hosts[i]))
             return fail(HF_EINVAL, "hf_fused_divergence_host: null buffer");
     }
+    // in place (u_host == divf_host) is fine: slices are disjoint and each slice's D2H lands
+    // after its own H2D; any other overlap between an input and an output is rejected
+    for (int i = 0; i < n_fields; ++i)
+        for (int j = 0; j < n_fields; ++j) {
+            if (prs[i].n_elem == 0 || prs[j].n_elem == 0 || (i == j && u_hosts[i] == divf_hosts[i])) continue;
+            const auto* a = static_cast<const unsigned char*>(u_hosts[i]);
+            const auto* b = static_cast<const unsigned char*>(divf_hosts[j]);
+            const size_t na = size_t(hf_field_words(&prs[i])) * word_bytes(&prs[i]);
+            const size_t nb = size_t(hf_field_words(&prs[j])) * word_bytes(&prs[j]);
+            if (a < b + nb && b < a + na)
+                return fail(HF_EINVAL, "hf_fused_divergence_host_batch: an input overlaps an output");
+        }
+    DeviceGuard guard;
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
 
@@ -792,8 +833,8 @@ int hf_fused_divergence_host_batch(hf_context* c, int n_fields, const hf_problem
     for (int i = 0; i < n_fields; ++i) {
         if (prs[i].n_elem == 0) continue;
         const size_t total = size_t(hf_field_words(&prs[i])) * word_bytes(&prs[i]);
-        pin(u_hosts[i], total, cudaHostRegisterReadOnly);
-        pin(divf_hosts[i], total, cudaHostRegisterDefault);
+        if (u_hosts[i] != divf_hosts[i]) pin(u_hosts[i], total, cudaHostRegisterReadOnly);
+        pin(divf_hosts[i], total, cudaHostRegisterDefault);  // in place: one read-write registration
     }
 
     int rc = HF_OK;

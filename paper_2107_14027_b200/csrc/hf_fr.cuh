@@ -7,9 +7,11 @@
 //   stage 1  hf_fr_project_kernel: each CTA stages a chunk of NE elements
 //            (bulk copy, as the lines kernel) and extrapolates every a-line of
 //            every variable to xi_a = -1, +1 (Lagrange basis at +-1) -> U_f.
-//   stage 4+5 hf_fr_correct_kernel: per element, the Rusanov common flux at
-//            both ends of every line (own U_f against the neighbour's, wave
-//            speed |V_a| + sqrt(V_a^2 + zeta + nu/T)), the jumps
+//   stage 4+5 hf_fr_correct_kernel: per element, the common flux at both ends
+//            of every line (own U_f against the neighbour's; PAPER.md:856:
+//            Rusanov on the pressure / velocity rows with the inviscid wave
+//            speed |V_a| + sqrt(V_a^2 + zeta), the mean of both sides on the
+//            gradient rows of the hyperbolic diffusion), the jumps
 //            F^I - F_a(U_f) into shared memory, then per solution point
 //            out -= sum_a jac_a (g_L'(xi) jump_(-a) + g_R'(xi) jump_(+a)) over the
 //            fused kernel's -div^D (+ source) in place.
@@ -188,7 +190,7 @@ __device__ __forceinline__ R fr_flux_row(const R (&U)[n_vars_c(DIM)], const Para
 template <class R, int DIM, int A>
 __device__ __forceinline__ R fr_wavespeed(const R (&U)[n_vars_c(DIM)], const Params<R>& p) {
     const R Va = U[1 + A];
-    return fabs(Va) + sqrt(Va * Va + p.zeta + p.nu * p.invT);
+    return fabs(Va) + sqrt(Va * Va + p.zeta);  // inviscid ACM spectral radius
 }
 
 // Jumps F^I - F_A(U_own) at both ends of one A-line, into the shared jump array.
@@ -199,8 +201,9 @@ __device__ __forceinline__ void fr_jump_rows(const R (&Uo)[n_vars_c(DIM)], const
         constexpr int LN = fr_lines<DIM, M>();
         const R fo = fr_flux_row<R, DIM, A, V>(Uo, p), fn = fr_flux_row<R, DIM, A, V>(Un, p);
         // U_L / U_R in the +x_A orientation of the face: own state is U_L on the +A face (s = 1)
-        const R du = s ? (Un[V] - Uo[V]) : (Uo[V] - Un[V]);
-        const R FI = R(0.5) * (fo + fn) - R(0.5) * lam * du;
+        // Rusanov on the hyperbolic rows, the mean on the gradient rows
+        R FI = R(0.5) * (fo + fn);
+        if constexpr (V < 1 + DIM) FI -= R(0.5) * lam * (s ? (Un[V] - Uo[V]) : (Uo[V] - Un[V]));
         jrow[NE * LN * DIM * 2 * V] = FI - fo;
         fr_jump_rows<R, DIM, M, NE, A, V + 1>(Uo, Un, lam, s, p, jrow);
     }
@@ -338,8 +341,9 @@ __device__ __forceinline__ void fr_jump_regs(const R (&Uo)[n_vars_c(DIM)], const
                                              const Params<R>& p, R (&j)[n_vars_c(DIM)]) {
     if constexpr (V < n_vars_c(DIM)) {
         const R fo = fr_flux_row<R, DIM, A, V>(Uo, p), fn = fr_flux_row<R, DIM, A, V>(Un, p);
-        const R du = s ? (Un[V] - Uo[V]) : (Uo[V] - Un[V]);
-        const R FI = R(0.5) * (fo + fn) - R(0.5) * lam * du;
+        // Rusanov on the hyperbolic rows, the mean on the gradient rows
+        R FI = R(0.5) * (fo + fn);
+        if constexpr (V < 1 + DIM) FI -= R(0.5) * lam * (s ? (Un[V] - Uo[V]) : (Uo[V] - Un[V]));
         j[V] = FI - fo;
         fr_jump_regs<R, DIM, A, V + 1>(Uo, Un, lam, s, p, j);
     }

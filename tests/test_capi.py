@@ -147,3 +147,31 @@ def test_new_entry_points_validate_before_touching_the_device():
     assert L.hf_fr_divergence_faces(C.byref(bad), buf, buf, None, None) == HF_EINVAL
     assert L.hf_fused_divergence_host_batch(None, 1, C.byref(pr), None, None) == HF_EINVAL
     assert "null context" in L.hf_last_error().decode()
+
+
+def test_fr_residual_validates_mesh_before_any_launch():
+    """A mesh whose dims multiply to n_elem but are not all >= 1 is rejected before the
+    fused stage-1+2+3+6 kernel runs (so the caller's buffers are untouched)."""
+    L = _lib.load()
+    pr = hf.make_problem(3, 3, 6, 2, Precision.fp64, PhysParams())
+    buf = (C.c_double * 8)()
+    out = (C.c_double * 8)()
+    for dims in ((-2, -3, 1), (0, 6, 1), (2, 3, 2)):
+        d3 = (C.c_int * 3)(*dims)
+        assert L.hf_fr_residual(C.byref(pr), d3, buf, buf, out, None) == HF_EINVAL
+        assert "dims" in L.hf_last_error().decode()
+
+
+def test_host_batch_rejects_overlapping_input_and_output():
+    """Only exact in-place (u_host == divf_host of the same field) is allowed on the host
+    path; partial overlaps are HF_EINVAL before any CUDA call."""
+    L = _lib.load()
+    pr = hf.make_problem(3, 1, 4, 4, Precision.fp64, PhysParams())
+    n = hf.field_words(pr)
+    buf = (C.c_double * (2 * n))()
+    base = C.addressof(buf)
+    us = (C.c_void_p * 1)(base)
+    outs = (C.c_void_p * 1)(base + 8 * 16)
+    ctx_dummy = C.c_void_p(1)  # never dereferenced: the overlap check comes first
+    assert L.hf_fused_divergence_host_batch(ctx_dummy, 1, C.byref(pr), us, outs) == HF_EINVAL
+    assert "overlaps" in L.hf_last_error().decode()

@@ -81,14 +81,20 @@ def test_fr_tgv_periodic_box(cuda):
     assert O.field_rel_error(d, p, n, g, out.double().cpu().numpy(), ref) <= 1e-12
 
 
+# (p, fp32): p3 FP64 takes the jump-array correction kernel; d2 FP32 p2-p8, d2 FP64 p4-p5
+# and d3 FP32 p2 / p5 take the staged one (fr_correct_staged(), hf_fr.cuh)
+@pytest.mark.parametrize("p,fp32", [(3, False), (2, True), (5, True), (4, False), (8, True)])
 @pytest.mark.parametrize("parts", [2, 3])
 @pytest.mark.parametrize("d,dims,g", [(3, (4, 2, 6), 4), (2, (8, 6), 4)])
-def test_fr_layer_partitions_with_ghosts(cuda, d, dims, g, parts):
+def test_fr_layer_partitions_with_ghosts(cuda, d, dims, g, parts, p, fp32):
     """Whole-layer partitions, each corrected with ghost face layers cut from the
     neighbours' face arrays (what the NCCL exchange of multi_gpu.FrSlab delivers),
     reproduce the single-partition residual."""
     import paper_2107_14027_b200 as hf
-    p, fp32 = 3, False
+    if d == 3 and p == 8:
+        pytest.skip("d = 3 stops at p = 7")
+    tol = 1e-5 if fp32 else 1e-12
+    dt = torch.float32 if fp32 else torch.float64
     n = int(np.prod(dims))
     layer = dims[0] * dims[1] if d == 3 else dims[0]
     n_layers = n // layer
@@ -97,7 +103,7 @@ def test_fr_layer_partitions_with_ghosts(cuda, d, dims, g, parts):
     pr_all = _pr(d, p, n, g, fp32, src=True)
     gw = hf.field_words(pr_all) // (n // g)  # words per group
     fw = hf.face_words(pr_all) // (n // g)
-    uf_all = torch.zeros(hf.face_words(pr_all), dtype=torch.float64, device="cuda")
+    uf_all = torch.zeros(hf.face_words(pr_all), dtype=dt, device="cuda")
     hf.fr_project_device(pr_all, _t(U, fp32), uf_all)
     got = np.zeros_like(U)
     bounds = np.linspace(0, n_layers, parts + 1).astype(int)
@@ -106,8 +112,8 @@ def test_fr_layer_partitions_with_ghosts(cuda, d, dims, g, parts):
         e0, ne = l0 * layer, (l1 - l0) * layer
         pr = _pr(d, p, ne, g, fp32, src=True)
         u = _t(U[e0 // g * gw:(e0 + ne) // g * gw], fp32)
-        out = torch.zeros(hf.field_words(pr), dtype=torch.float64, device="cuda")
-        uf = torch.zeros(hf.face_words(pr), dtype=torch.float64, device="cuda")
+        out = torch.zeros(hf.field_words(pr), dtype=dt, device="cuda")
+        uf = torch.zeros(hf.face_words(pr), dtype=dt, device="cuda")
         hf.fused_divergence_device(pr, u, out)
         hf.fr_project_device(pr, u, uf)
         lo = ((l0 - 1) % n_layers) * layer
@@ -117,8 +123,8 @@ def test_fr_layer_partitions_with_ghosts(cuda, d, dims, g, parts):
         ms = hf.make_mesh(dims, d, e0, ne, layer)
         hf.fr_correct_device(pr, ms, uf, out, ghost_lo, ghost_hi)
         torch.cuda.synchronize()
-        got[e0 // g * gw:(e0 + ne) // g * gw] = out.cpu().numpy()
-    assert O.field_rel_error(d, p, n, g, got, ref) <= 1e-12
+        got[e0 // g * gw:(e0 + ne) // g * gw] = out.double().cpu().numpy()
+    assert O.field_rel_error(d, p, n, g, got, ref) <= tol
 
 
 def test_fr_slab_driver_single_rank(cuda):

@@ -94,3 +94,23 @@ def test_host_batch_matches_device_path(cuda):
     for (pr, src, dst), ref in zip(items, refs):
         if pr.n_elem:
             assert torch.equal(dst, ref), (pr.d, pr.p, pr.precision)
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_path_in_place(cuda, pinned):
+    """u_host == divf_host: the result overwrites the input, equal to the out-of-place run."""
+    import paper_2107_14027_b200 as hf
+    from paper_2107_14027_b200 import Precision
+    d, p = 3, 3
+    g = hf.preferred_group(hf.make_problem(d, p, 1, 1, Precision.fp64, PAR))
+    n = int(60 * 2 ** 20 / (13 * 64 * 8)) // g * g
+    pr = hf.make_problem(d, p, n, g, Precision.fp64, PAR, with_source=True)
+    gen = torch.Generator().manual_seed(9)
+    u = torch.rand(hf.field_words(pr), generator=gen, dtype=torch.float64) * 2 - 1
+    ctx = hf.Context(0)
+    ref = torch.zeros_like(u)
+    ctx.run(pr, u.clone(), ref)
+    buf = u.clone().pin_memory() if pinned else u.clone()
+    ctx.run(pr, buf, buf)
+    ctx.close()
+    assert torch.equal(buf, ref)
