@@ -454,26 +454,35 @@ def run_ours(args, R: Ranks):
     # ---- unfused comparator beside it (config 4)
     unfused = None
     if args.workload == "config4":
+        # the unfused comparator (io_model S2 + S3, io_model.hpp:32-33) on the same problem in
+        # its own AoSoA group (hf_preferred_group of HF_METHOD_UNFUSED), same points
         c = cases[0]
-        ws = torch.empty(hf.unfused_workspace_bytes(c["pr"]) // c["u"].element_size(), dtype=c["u"].dtype,
-                         device=dev)
+        from paper_2107_14027_b200 import Method
+        pr_u0 = hf.make_problem(c["d"], c["p"], 1, 1, c["pr"].precision, par, method=Method.unfused)
+        gu = hf.preferred_group(pr_u0)
+        nu_el = max(gu, c["n_elem"] // gu * gu)
+        pr_u = hf.make_problem(c["d"], c["p"], nu_el, gu, c["pr"].precision, par, method=Method.unfused)
+        uu = torch.empty(hf.field_words(pr_u), dtype=c["u"].dtype, device=dev).uniform_(-1.0, 1.0, generator=gen)
+        ou = torch.empty_like(uu)
+        ws = torch.empty(hf.unfused_workspace_bytes(pr_u) // uu.element_size(), dtype=uu.dtype, device=dev)
         for _ in range(3):
-            hf.unfused_divergence_device(c["pr"], c["u"], c["o"], ws, st)
+            hf.unfused_divergence_device(pr_u, uu, ou, ws, st)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
         for _ in range(args.steps):
-            hf.unfused_divergence_device(c["pr"], c["u"], c["o"], ws, st)
+            hf.unfused_divergence_device(pr_u, uu, ou, ws, st)
         b.record(st)
         torch.cuda.synchronize()
         tu = a.elapsed_time(b) * 1e-3 / args.steps
-        ubytes = c["points"] * 8 * hf.n_vars(c["d"]) * c["u"].element_size()  # io_model S2+S3, io_model.hpp:32-33
-        unfused = {"us_per_step": round(tu * 1e6, 2), "gdofs": round(c["points"] / tu / 1e9, 3),
-                   "alg_bytes_per_point": 8 * hf.n_vars(c["d"]) * c["u"].element_size(),
-                   "achieved_GBps": round(ubytes / tu / 1e9, 1), "frac": round(ubytes / tu / 1e9 / peak, 4),
-                   "fused_speedup": round(tu / (case_rows[0]["us_per_launch"] * 1e-6), 3),
-                   "model_speedup": 4.0}
-        step()  # the parity check below reads the fused result
-        torch.cuda.synchronize()
+        upts = nu_el * (c["p"] + 1) ** c["d"]
+        ubpp = 8 * hf.n_vars(c["d"]) * uu.element_size()
+        tf = case_rows[0]["us_per_launch"] * 1e-6 / c["points"] * upts  # fused time for the same points
+        unfused = {"kernels": hf.kernel_info(pr_u)["name"], "group": gu, "points": upts,
+                   "us_per_step": round(tu * 1e6, 2), "gdofs": round(upts / tu / 1e9, 3),
+                   "alg_bytes_per_point": ubpp, "achieved_GBps": round(upts * ubpp / tu / 1e9, 1),
+                   "frac": round(upts * ubpp / tu / 1e9 / peak, 4),
+                   "fused_speedup": round(tu / tf, 3), "model_speedup": 4.0}
+        del uu, ou, ws
 
     # ---- parity (checker, after timing): sampled groups of every case against the CPU oracle
     parity = None

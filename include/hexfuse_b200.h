@@ -202,6 +202,25 @@ HF_API int hf_fused_divergence_host_batch(hf_context* ctx, int n_fields, const h
 HF_API int hf_partition(const hf_problem* pr, int n_parts, int part, int64_t* e_begin, int64_t* n_elem_part,
                  int64_t* word_offset);
 
+/* ---- state blob + sidecar I/O (layout.hpp:155-200) ----
+ * The reference's on-disk field: <path> holds the padded field's words little-endian
+ * (4 B fp32 / 8 B fp64), <path>.json the sidecar {"byte_order","d","group","n_elem",
+ * "p","precision","words"} (field_sidecar, layout.hpp:155-159).  Host only.
+ *   hf_blob_info   import_blob's sidecar half (layout.hpp:179-186): fills d, p, n_elem,
+ *                  group, precision of *shape_out (other fields untouched)
+ *   hf_blob_read   the words into host_words (hf_field_words(pr) words of pr's
+ *                  precision); pr's shape must equal the sidecar's
+ *   hf_blob_write  export_blob (layout.hpp:161-177), byte-identical blob and sidecar
+ *   hf_fused_divergence_blob  in_path -> B200 host path -> out_path: shape from the
+ *                  input sidecar, physics / jac / source / method from *params
+ * Errors as the reference: missing or short files, word-count mismatch HF_ERUNTIME
+ * (std::runtime_error); unknown precision HF_EINVAL (precision_from_string, core.hpp:16-20). */
+HF_API int hf_blob_info(const char* path, hf_problem* shape_out);
+HF_API int hf_blob_read(const char* path, const hf_problem* pr, void* host_words);
+HF_API int hf_blob_write(const char* path, const hf_problem* pr, const void* host_words);
+HF_API int hf_fused_divergence_blob(hf_context* ctx, const hf_problem* params, const char* in_path,
+                                    const char* out_path);
+
 HF_API const char* hf_last_error(void);
 HF_API const char* hf_version(void);
 

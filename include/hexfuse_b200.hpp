@@ -124,6 +124,67 @@ StateField fused_divergence_b200(const StateField& U, const PhysParams& params, 
     return out;
 }
 
+// ---- state blobs (layout.hpp:155-200) through the library's C ABI ----
+// import_blob / export_blob with the reference's on-disk format (flat little-endian words +
+// <path>.json sidecar), byte-identical to the reference's; errors as the reference's.
+template <class StateField>
+StateField import_blob_b200(const std::string& path) {
+    hf_problem pr{};
+    detail::check(hf_blob_info(path.c_str(), &pr), "import_blob");
+    StateField f;
+    f.d = pr.d;
+    f.p = pr.p;
+    f.n_elem = static_cast<int>(pr.n_elem);
+    f.group = pr.group;
+    f.precision = static_cast<decltype(f.precision)>(pr.precision == HF_FP32 ? 0 : 1);
+    const int64_t words = hf_field_words(&pr);
+    f.data.assign(static_cast<std::size_t>(words), 0.0);
+    if (pr.precision == HF_FP32) {
+        std::vector<float> tmp(f.data.size());
+        detail::check(hf_blob_read(path.c_str(), &pr, tmp.data()), "import_blob");
+        std::transform(tmp.begin(), tmp.end(), f.data.begin(), [](float x) { return static_cast<double>(x); });
+    } else {
+        detail::check(hf_blob_read(path.c_str(), &pr, f.data.data()), "import_blob");
+    }
+    return f;
+}
+
+template <class StateField>
+void export_blob_b200(const StateField& f, const std::string& path) {
+    hf_problem pr{};
+    pr.d = f.d;
+    pr.p = f.p;
+    pr.n_elem = f.n_elem;
+    pr.group = f.group;
+    pr.precision = static_cast<int>(f.precision) == 0 ? HF_FP32 : HF_FP64;
+    pr.zeta = pr.T = 1.0;  // shape only; physics is not part of the blob
+    if (pr.precision == HF_FP32) {
+        std::vector<float> tmp(f.data.size());
+        std::transform(f.data.begin(), f.data.end(), tmp.begin(), [](double x) { return static_cast<float>(x); });
+        detail::check(hf_blob_write(path.c_str(), &pr, tmp.data()), "export_blob");
+    } else {
+        detail::check(hf_blob_write(path.c_str(), &pr, f.data.data()), "export_blob");
+    }
+}
+
+// A blob in, the divergence blob out, on the B200 (shape from the input's sidecar).
+template <class PhysParams>
+void fused_divergence_blob(const std::string& in_path, const std::string& out_path, const PhysParams& params,
+                           const std::array<double, 3>& jac, bool with_source, int method = HF_METHOD_AUTO) {
+    params.validate();
+    hf_problem pr{};
+    pr.nu = params.nu;
+    pr.zeta = params.zeta;
+    pr.T = params.T;
+    pr.jac[0] = jac[0];
+    pr.jac[1] = jac[1];
+    pr.jac[2] = jac[2];
+    pr.with_source = with_source ? 1 : 0;
+    pr.method = method;
+    detail::check(hf_fused_divergence_blob(detail::thread_context(), &pr, in_path.c_str(), out_path.c_str()),
+                  "fused_divergence_blob");
+}
+
 // Device-buffer form (the rendered kernel's (n_elements, u, divf) contract, render.hpp:79-80).
 inline void fused_divergence_device(const hf_problem& pr, const void* u_dev, void* divf_dev, void* stream = nullptr) {
     detail::check(hf_fused_divergence(&pr, u_dev, divf_dev, stream), "hf_fused_divergence");

@@ -185,6 +185,9 @@ def ref() -> C.CDLL:
         R.ref_time_oracle_mt.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_double,
                                          C.c_double, C.c_double, _dp, C.c_int, C.c_int]
         R.ref_time_oracle_mt.restype = C.c_double
+        R.ref_export_blob.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, C.c_char_p]
+        R.ref_import_blob.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.c_void_p, C.c_longlong]
+        R.ref_import_blob.restype = C.c_longlong
         R.ref_max_abs_eigenvalue.argtypes = [C.c_int, _dp, C.c_int, C.c_double, C.c_double, C.c_double]
         R.ref_max_abs_eigenvalue.restype = C.c_double
         _ref = R
@@ -463,6 +466,24 @@ def ref_random_field_timing(d, p, n_elem, group, fp32, seed) -> np.ndarray:
     if R.ref_random_field(d, p, n_elem, group, int(fp32), seed, out) != 0:
         raise ValueError(R.ref_last_error().decode())
     return out
+
+
+def ref_export_blob(d, p, n_elem, group, fp32, data, path: str) -> None:
+    """hexfuse::export_blob (layout.hpp:161-177): flat little-endian words + <path>.json."""
+    data = np.ascontiguousarray(data, dtype=np.float64)
+    if ref().ref_export_blob(d, p, n_elem, group, int(fp32), data, path.encode()) != 0:
+        raise RuntimeError(ref().ref_last_error().decode())
+
+
+def ref_import_blob(path: str):
+    """hexfuse::import_blob (layout.hpp:179-200) -> (d, p, n_elem, group, fp32, data float64)."""
+    shape = (C.c_int * 5)()
+    n = ref().ref_import_blob(path.encode(), shape, None, 0)
+    if n < 0:
+        raise RuntimeError(ref().ref_last_error().decode())
+    out = np.zeros(n)
+    ref().ref_import_blob(path.encode(), shape, out.ctypes.data, n)
+    return shape[0], shape[1], shape[2], shape[3], bool(shape[4]), out
 
 
 def ref_gl_derivative(m: int):

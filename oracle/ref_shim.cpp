@@ -15,6 +15,9 @@
 //   ref_gl_derivative      -> gauss_legendre_points + derivative_matrix (operators.hpp:17-74)
 //   ref_time_oracle_mt     -> oracle_divergence on T group-aligned sub-fields, one
 //                             std::thread each (the function is pure)
+//   ref_export_blob        -> hexfuse::export_blob        (layout.hpp:161-177)
+//   ref_import_blob        -> hexfuse::import_blob        (layout.hpp:179-200): shape into
+//                             shape[5] = {d, p, n_elem, group, fp32}, words into `out`
 //   ref_max_abs_eigenvalue -> max |eigenvalues(flux_jacobian(s, params, e_a))|
 //                             (equations.hpp:112-130, eig.hpp:15): pins the Rusanov
 //                             wave speed of the FR interface stage (hexfuse_oracle.c)
@@ -166,6 +169,31 @@ double ref_time_oracle_mt(int d, int p, int n_elem, int group, int fp32, const d
         g_err = e.what();
         return -1.0;
     }
+}
+
+int ref_export_blob(int d, int p, int n_elem, int group, int fp32, const double* data, const char* path) {
+    return guarded([&] {
+        StateField f = make_field(d, p, n_elem, group, fp32);
+        std::memcpy(f.data.data(), data, f.data.size() * sizeof(double));
+        export_blob(f, path);
+    });
+}
+
+// shape[5] = {d, p, n_elem, group, fp32}; `out` (may be null: shape only) receives
+// min(capacity, words) doubles.  Returns the field's word count, < 0 on error.
+long long ref_import_blob(const char* path, int* shape, double* out, long long capacity) {
+    long long words = -1;
+    const int rc = guarded([&] {
+        const StateField f = import_blob(path);
+        shape[0] = f.d;
+        shape[1] = f.p;
+        shape[2] = f.n_elem;
+        shape[3] = f.group;
+        shape[4] = f.precision == Precision::fp32 ? 1 : 0;
+        words = static_cast<long long>(f.data.size());
+        if (out) std::memcpy(out, f.data.data(), static_cast<std::size_t>(std::min(words, capacity)) * sizeof(double));
+    });
+    return rc == 0 ? words : -rc;
 }
 
 double ref_max_abs_eigenvalue(int d, const double* s, int a, double nu, double zeta, double T) {

@@ -21,6 +21,7 @@ from .hexfuse import (  # noqa: F401
     field_sidecar,
     field_words,
     fused_divergence,
+    fused_divergence_blob,
     fused_divergence_device,
     fused_divergence_mapped_device,
     face_words,

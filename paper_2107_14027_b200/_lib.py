@@ -56,6 +56,7 @@ EXPORTED = [
     "hf_geometry_words", "hf_fused_divergence_mapped", "hf_mapped_kernel_info",
     "hf_face_words", "hf_fr_project", "hf_fr_correct", "hf_fr_divergence_faces", "hf_fr_residual",
     "hf_ipc_handle", "hf_ipc_open", "hf_ipc_close",
+    "hf_blob_info", "hf_blob_read", "hf_blob_write", "hf_fused_divergence_blob",
 ]
 
 
@@ -125,6 +126,13 @@ def load() -> C.CDLL:
     L.hf_ipc_handle.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]
     L.hf_ipc_open.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
     L.hf_ipc_close.argtypes = [C.c_void_p]
+    # (bound when present, so that an older build can still be A/B-timed through this package;
+    # tests/test_capi.py checks that the built library exports every declared symbol)
+    if hasattr(L, "hf_blob_info"):
+        L.hf_blob_info.argtypes = [C.c_char_p, P]
+        L.hf_blob_read.argtypes = [C.c_char_p, P, C.c_void_p]
+        L.hf_blob_write.argtypes = [C.c_char_p, P, C.c_void_p]
+        L.hf_fused_divergence_blob.argtypes = [C.c_void_p, P, C.c_char_p, C.c_char_p]
     _lib = L
     return L
 

@@ -27,6 +27,13 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
+}  // namespace
+
+// the error channel shared with hf_blob.cu
+int hf_capi_fail(int code, const std::string& msg) { return fail(code, msg); }
+
+namespace {
+
 int cuda_fail(cudaError_t e, const char* where) {
     return fail(HF_ERUNTIME, std::string(where) + ": " + cudaGetErrorString(e));
 }
@@ -128,8 +135,8 @@ int validate(const hf_problem* pr) {
     if (!(pr->T > 0.0)) return fail(HF_EINVAL, "PhysParams: T must be > 0");
     if (pr->method < HF_METHOD_AUTO || pr->method > HF_METHOD_PLANAR_MANAGED)
         return fail(HF_EINVAL, "hf_problem: unknown method");
-    if ((pr->method == HF_METHOD_PLANAR || pr->method == HF_METHOD_PLANAR_MANAGED) && (pr->d != 3 || pr->p > 6))
-        return fail(HF_EINVAL, "planar method: d must be 3 and p <= 6");
+    if ((pr->method == HF_METHOD_PLANAR || pr->method == HF_METHOD_PLANAR_MANAGED) && pr->d != 3)
+        return fail(HF_EINVAL, "planar method: d must be 3");
     const int64_t words = ipow64(pr->p + 1, pr->d) * (1 + pr->d + pr->d * pr->d) * int64_t(pr->group);
     if (words > (int64_t(1) << 31)) return fail(HF_EINVAL, "hf_problem: group too large");
     return HF_OK;
@@ -281,6 +288,72 @@ hfb::FrParams<R> make_fr_params(const hf_problem* pr, const hf_mesh* mesh, const
     return f;
 }
 
+// lines "variant" of the grouped-chunk kernel (LinesShape GS < NE, hf_dispatch.cuh)
+constexpr int kGroupedVariant = 100;
+
+// A caller's AoSoA group that is not the selected chunk (e.g. the reference's planar group
+// 4*floor(32/m), or a solver's own AoSoA width): the one-chunk variant predicted fastest,
+//   the group itself when a variant has that chunk size (one contiguous chunk), else in
+//   tile mode max over NE of  fill(G, NE) * rows(NE * w) * occupancy(CTAs per SM),
+// calibrated on B200 (tools/tile_probe.py, profiles/r02/tile_probe_d3.jsonl): TMA moves a
+// tile box at about one row per 3 SM cycles whatever the row length up to 32 B, so 16-byte
+// rows cap a kernel near 0.53 of the HBM roofline, 32-byte rows near 0.9, >= 64-byte rows
+// reach it; one resident CTA per SM serialises load, sweeps and store (~0.6); fill is the
+// used fraction of the group's sub-chunks (G = 20 in chunks of 16: 20 / 32).
+// Groups whose stride is not a 16-byte multiple take the guarded path of the selected size.
+template <class R>
+int lines_variant_for_group(const hf_problem* pr, int variant, const hfb::Params<R>& prm, bool faces) {
+    const int w = int(sizeof(R)), m = pr->p + 1, G = pr->group;
+    const int ne0 = hfb::lines_ne0(w, pr->d, m);
+    const int ne_sel = hfb::variant_ne_of(ne0, variant);
+    if (G == ne_sel) return variant;
+    auto available = [&](int v) {
+        int rc;
+        if constexpr (sizeof(R) == 4)
+            rc = pr->d == 3 ? hfb::lines_f32_d3(pr->p, v, false, prm, nullptr, nullptr, true, faces)
+                            : hfb::lines_f32_d2(pr->p, v, false, prm, nullptr, nullptr, true, faces);
+        else
+            rc = pr->d == 3 ? hfb::lines_f64_d3(pr->p, v, false, prm, nullptr, nullptr, true, faces)
+                            : hfb::lines_f64_d2(pr->p, v, false, prm, nullptr, nullptr, true, faces);
+        return rc == 0;
+    };
+    const int cand[4] = {0, 1, 7, 2};
+    for (int v : cand)
+        if (hfb::variant_ne_of(ne0, v) == G && available(v)) return v;
+    // a power-of-two group below the chunk: NE0 / G whole groups per chunk, contiguous
+    if (!faces && G < ne0 && (G & (G - 1)) == 0 && ne0 % G == 0) {
+        int rc;
+        if constexpr (sizeof(R) == 4)
+            rc = pr->d == 3 ? hfb::lines_grouped_f32_d3(pr->p, G, false, prm, nullptr, nullptr, true)
+                            : hfb::lines_grouped_f32_d2(pr->p, G, false, prm, nullptr, nullptr, true);
+        else
+            rc = pr->d == 3 ? hfb::lines_grouped_f64_d3(pr->p, G, false, prm, nullptr, nullptr, true)
+                            : hfb::lines_grouped_f64_d2(pr->p, G, false, prm, nullptr, nullptr, true);
+        if (rc == 0) return kGroupedVariant;
+    }
+    if ((int64_t(G) * w) % 16 != 0) return hfb::is_one_chunk_variant(variant) ? variant : 0;
+    const int64_t np = ipow64(m, pr->d), nv = 1 + pr->d + pr->d * pr->d;
+    int best = -1;
+    double best_score = -1.0;
+    for (int v : cand) {
+        const int ne = hfb::variant_ne_of(ne0, v);
+        if (ne < 1 || (ne * w) % 16 != 0 || !available(v)) continue;
+        const double fill = double(G) / (double((G + ne - 1) / ne) * ne);
+        const int row = ne * w;
+        const double rows = row >= 64 ? 1.0 : row >= 32 ? 0.9 : 0.53;
+        // shared memory of hf_lines_kernel (LinesShape::SMEM) and CTAs per SM (228 KB, 1 KB reserved per CTA)
+        const int64_t smem = 128 + ((ne * np * nv * w + 15) / 16 * 16 + 32) + ne * np * (1 + pr->d) * w;
+        const int64_t bps = (228 * 1024) / (smem + 1024);
+        const double occ = bps >= 3 ? 1.0 : bps == 2 ? 0.95 : 0.6;
+        const double score = fill * rows * occ;
+        if (score > best_score + 1e-9) {
+            best = v;
+            best_score = score;
+        }
+    }
+    return best >= 0 ? best : (hfb::is_one_chunk_variant(variant) ? variant : 0);
+}
+
 // Resolve + launch (dry: describe only).  ws only for the unfused method.
 int dispatch(const hf_problem* pr, const void* u, void* out, void* ws, cudaStream_t st, hfb::KInfo* info, bool dry,
              int force_method = -1, int force_variant = -1, bool faces = false, void* uf = nullptr) {
@@ -296,7 +369,11 @@ int dispatch(const hf_problem* pr, const void* u, void* out, void* ws, cudaStrea
     if (pr->precision == HF_FP32) {
         auto prm = make_params<float>(pr, u, out, ws);
         prm.uf = static_cast<float*>(uf);
-        if (method == HF_METHOD_PLANAR) rc = hfb::planar_f32(pr->p, src, prm, st, info, dry);
+        if (method == HF_METHOD_LINES && force_variant < 0) variant = lines_variant_for_group(pr, variant, prm, faces);
+        if (method == HF_METHOD_LINES && variant == kGroupedVariant)
+            rc = pr->d == 3 ? hfb::lines_grouped_f32_d3(pr->p, pr->group, src, prm, st, info, dry)
+                            : hfb::lines_grouped_f32_d2(pr->p, pr->group, src, prm, st, info, dry);
+        else if (method == HF_METHOD_PLANAR) rc = hfb::planar_f32(pr->p, src, prm, st, info, dry);
         else if (method == HF_METHOD_PLANAR_MANAGED) rc = hfb::planar_managed_f32(pr->p, src, prm, st, info, dry);
         else if (method == HF_METHOD_UNFUSED) rc = hfb::unfused_f32(pr->d, pr->p, src, prm, st, info, dry);
         else rc = pr->d == 3 ? hfb::lines_f32_d3(pr->p, variant, src, prm, st, info, dry, faces)
@@ -304,7 +381,11 @@ int dispatch(const hf_problem* pr, const void* u, void* out, void* ws, cudaStrea
     } else {
         auto prm = make_params<double>(pr, u, out, ws);
         prm.uf = static_cast<double*>(uf);
-        if (method == HF_METHOD_PLANAR) rc = hfb::planar_f64(pr->p, src, prm, st, info, dry);
+        if (method == HF_METHOD_LINES && force_variant < 0) variant = lines_variant_for_group(pr, variant, prm, faces);
+        if (method == HF_METHOD_LINES && variant == kGroupedVariant)
+            rc = pr->d == 3 ? hfb::lines_grouped_f64_d3(pr->p, pr->group, src, prm, st, info, dry)
+                            : hfb::lines_grouped_f64_d2(pr->p, pr->group, src, prm, st, info, dry);
+        else if (method == HF_METHOD_PLANAR) rc = hfb::planar_f64(pr->p, src, prm, st, info, dry);
         else if (method == HF_METHOD_PLANAR_MANAGED) rc = hfb::planar_managed_f64(pr->p, src, prm, st, info, dry);
         else if (method == HF_METHOD_UNFUSED) rc = hfb::unfused_f64(pr->d, pr->p, src, prm, st, info, dry);
         else rc = pr->d == 3 ? hfb::lines_f64_d3(pr->p, variant, src, prm, st, info, dry, faces)
@@ -386,9 +467,14 @@ int hf_preferred_group(const hf_problem* pr) {
     hf_problem q = *pr;
     int method, variant;
     select_method(pr, &method, &variant);
-    if (method == HF_METHOD_UNFUSED) return 32;
-    hfb::KInfo ki;
-    if (dispatch(&q, nullptr, nullptr, nullptr, nullptr, &ki, true)) return -HF_EINVAL;
+    if (method == HF_METHOD_UNFUSED) {  // hfb::unfused_group: direction blocks of <= 48 KB, >= 16-byte rows
+        const int64_t blk = ipow64(pr->p + 1, pr->d) * (1 + pr->d + pr->d * pr->d) * int64_t(word_bytes(pr));
+        int g = 64;
+        while (g > 16 / int(word_bytes(pr)) && g * blk > 48 * 1024) g /= 2;
+        return g;
+    }
+    hfb::KInfo ki;  // the selected variant's chunk, whatever pr->group is
+    if (dispatch(&q, nullptr, nullptr, nullptr, nullptr, &ki, true, method, variant)) return -HF_EINVAL;
     return ki.elems_per_cta;
 }
 

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace hfb {
@@ -47,6 +48,13 @@ struct Params {
     long long n_chunks;       // pipelined kernel: number of full chunks to process
     int group;
     int fast_ok;              // host-verified: bulk-copy alignment holds for full chunks
+    // Tile mode (lines kernel, group != chunk): chunk b is sub-chunk b % sub_per_group of
+    // group b / sub_per_group, a box of NE elements x all rows moved by ONE TMA tensor copy
+    // per direction over the 5-d view {e_l, i, (j,k), v, group} of the AoSoA field.
+    int tile;
+    int sub_per_group;        // ceil(group / NE)
+    CUtensorMap tm_u;         // 64-byte aligned descriptors, read from the parameter space
+    CUtensorMap tm_out;
 };
 
 // FR face array (stage 1 output, hf_fr.cuh): word of (element e, axis a, side s,
@@ -126,6 +134,30 @@ __device__ __forceinline__ void bulk_s2g(void* dst_gmem, const void* src_smem, u
 }
 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+// TMA tensor copies (SASS UTMALDG / UTMASTG) of one 5-d box; `tmap` is the generic
+// address of a CUtensorMap in the __grid_constant__ parameter block.
+__device__ __forceinline__ void tma_load_5d(void* dst_smem, const CUtensorMap* tmap, int c0, int c1, int c2, int c3,
+                                            int c4, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];" ::"r"(smem_u32(dst_smem)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* tmap, int c0, int c1, int c2, int c3, int c4,
+                                             const void* src_smem) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+            reinterpret_cast<uint64_t>(tmap)),
+        "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(src_smem))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* tmap) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
 
 __device__ __forceinline__ void bulk_wait_read_all() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

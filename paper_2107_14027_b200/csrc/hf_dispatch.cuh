@@ -85,6 +85,52 @@ int run_lines_range(int p, int variant, bool src, const Params<R>& prm, cudaStre
     }
 }
 
+// Grouped chunks (hf_lines.cuh, LinesShape GS < NE): the chunk of variant 0 (NE0 elements)
+// made of NE0 / GS whole groups of a caller's power-of-two group GS < NE0, one contiguous
+// byte range.  Returns kUnsupported for a GS that is not instantiated.
+template <class R, int DIM, int M, int GS = 1>
+int lines_grouped_m(int gs, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
+    constexpr int NE = variant_ne<R, DIM, M, 0>();
+    if constexpr (GS >= NE) {
+        return kUnsupported;
+    } else {
+        if (gs == GS) {
+            if constexpr (LinesShape<R, DIM, M, NE, 1, GS>::SMEM > size_t(kMaxSmemPerCta)) return kUnsupported;
+            return src ? int(launch_lines<R, DIM, M, NE, true, 1, false, GS>(prm, st, info, dry))
+                       : int(launch_lines<R, DIM, M, NE, false, 1, false, GS>(prm, st, info, dry));
+        }
+        return lines_grouped_m<R, DIM, M, GS * 2>(gs, src, prm, st, info, dry);
+    }
+}
+
+template <class R, int DIM>
+int run_lines_grouped(int p, int gs, bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
+    if constexpr (DIM == 3) {
+        switch (p) {
+            case 1: return lines_grouped_m<R, 3, 2>(gs, src, prm, st, info, dry);
+            case 2: return lines_grouped_m<R, 3, 3>(gs, src, prm, st, info, dry);
+            case 3: return lines_grouped_m<R, 3, 4>(gs, src, prm, st, info, dry);
+            case 4: return lines_grouped_m<R, 3, 5>(gs, src, prm, st, info, dry);
+            case 5: return lines_grouped_m<R, 3, 6>(gs, src, prm, st, info, dry);
+            case 6: return lines_grouped_m<R, 3, 7>(gs, src, prm, st, info, dry);
+            case 7: return lines_grouped_m<R, 3, 8>(gs, src, prm, st, info, dry);
+            default: return kUnsupported;
+        }
+    } else {
+        switch (p) {
+            case 1: return lines_grouped_m<R, 2, 2>(gs, src, prm, st, info, dry);
+            case 2: return lines_grouped_m<R, 2, 3>(gs, src, prm, st, info, dry);
+            case 3: return lines_grouped_m<R, 2, 4>(gs, src, prm, st, info, dry);
+            case 4: return lines_grouped_m<R, 2, 5>(gs, src, prm, st, info, dry);
+            case 5: return lines_grouped_m<R, 2, 6>(gs, src, prm, st, info, dry);
+            case 6: return lines_grouped_m<R, 2, 7>(gs, src, prm, st, info, dry);
+            case 7: return lines_grouped_m<R, 2, 8>(gs, src, prm, st, info, dry);
+            case 8: return lines_grouped_m<R, 2, 9>(gs, src, prm, st, info, dry);
+            default: return kUnsupported;
+        }
+    }
+}
+
 template <class R, int M>
 int planar_m(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
     constexpr int NE = planar_ne<R, M>();
@@ -101,6 +147,7 @@ int run_planar_impl(int p, bool src, const Params<R>& prm, cudaStream_t st, KInf
         case 4: return planar_m<R, 5>(src, prm, st, info, dry);
         case 5: return planar_m<R, 6>(src, prm, st, info, dry);
         case 6: return planar_m<R, 7>(src, prm, st, info, dry);
+        case 7: return planar_m<R, 8>(src, prm, st, info, dry);
         default: return kUnsupported;
     }
 }
@@ -121,6 +168,7 @@ int run_planar_managed_impl(int p, bool src, const Params<R>& prm, cudaStream_t 
         case 4: return planar_managed_m<R, 5>(src, prm, st, info, dry);
         case 5: return planar_managed_m<R, 6>(src, prm, st, info, dry);
         case 6: return planar_managed_m<R, 7>(src, prm, st, info, dry);
+        case 7: return planar_managed_m<R, 8>(src, prm, st, info, dry);
         default: return kUnsupported;
     }
 }
@@ -204,6 +252,10 @@ HF_LINES_DECL(lines_f64_d3, double)
 HF_LINES_DECL(lines_f32_d2, float)
 HF_LINES_DECL(lines_f64_d2, double)
 #undef HF_LINES_DECL
+int lines_grouped_f32_d3(int p, int gs, bool src, const Params<float>&, cudaStream_t, KInfo*, bool);
+int lines_grouped_f64_d3(int p, int gs, bool src, const Params<double>&, cudaStream_t, KInfo*, bool);
+int lines_grouped_f32_d2(int p, int gs, bool src, const Params<float>&, cudaStream_t, KInfo*, bool);
+int lines_grouped_f64_d2(int p, int gs, bool src, const Params<double>&, cudaStream_t, KInfo*, bool);
 int planar_f32(int p, bool src, const Params<float>&, cudaStream_t, KInfo*, bool);
 int planar_f64(int p, bool src, const Params<double>&, cudaStream_t, KInfo*, bool);
 int planar_managed_f32(int p, bool src, const Params<float>&, cudaStream_t, KInfo*, bool);

@@ -39,16 +39,22 @@ struct KInfo {
 constexpr int kLinesSmemBudget = 72 * 1024;
 constexpr int kMaxSmemPerCta = 227 * 1024;
 
-template <class R, int DIM, int M>
-constexpr int lines_ne_default() {
-    constexpr int min_ne = 16 / int(sizeof(R));  // a chunk row must be a 16-byte multiple
-    int ne = (DIM == 2) ? 128 : 64;
-    while (ne > min_ne && (LinesShape<R, DIM, M, 1>::HDR +
-                           size_t(ne) * ipow_c(M, DIM) * (n_vars_c(DIM) + 1 + DIM) * sizeof(R) >
-                               size_t(kLinesSmemBudget) ||
-                           ne * ipow_c(M, DIM - 1) > 512))
+// NE0 of (word bytes w, d, m); constexpr and callable at run time (the host's choice of a
+// variant for a caller's group, hf_capi.cu) so the two can never disagree.
+constexpr int lines_ne0(int w, int dim, int m) {
+    const int min_ne = 16 / w;  // a chunk row must be a 16-byte multiple
+    int ne = (dim == 2) ? 128 : 64;
+    while (ne > min_ne &&
+           (128 + size_t(ne) * ipow_c(m, dim) * (n_vars_c(dim) + 1 + dim) * size_t(w) > size_t(kLinesSmemBudget) ||
+            ne * ipow_c(m, dim - 1) > 512))
         ne /= 2;
     return ne;
+}
+
+template <class R, int DIM, int M>
+constexpr int lines_ne_default() {
+    static_assert(LinesShape<R, DIM, M, 1>::HDR == 128, "lines_ne0 assumes a 128-byte header");
+    return lines_ne0(int(sizeof(R)), DIM, M);
 }
 
 // Lines variants.  NE0 = lines_ne_default (about three CTAs per SM).
@@ -102,12 +108,16 @@ constexpr bool variant_faces_built() {
 #endif
 }
 
+// The one-chunk-per-CTA variants (NE0, NE0/2, 2*NE0, NE0/4): the chunk sizes the host
+// chooses from for a caller's AoSoA group that is not the selected chunk (tile mode).
+constexpr bool is_one_chunk_variant(int v) { return v == 0 || v == 1 || v == 2 || v == 7; }
+
 template <class R, int DIM, int M, int VARIANT>
 constexpr bool variant_built() {
 #ifdef HF_TUNING
     return true;
 #else
-    if (VARIANT == 0 || VARIANT == 3 || VARIANT == 10) return true;
+    if (is_one_chunk_variant(VARIANT) || VARIANT == 3 || VARIANT == 10) return true;
     for (const SelRow& r : kSelect)
         if (r.d == DIM && r.p == M - 1 && r.prec == (sizeof(R) == 8 ? 1 : 0) && r.method == 2 && r.variant == VARIANT)
             return true;
@@ -118,17 +128,18 @@ template <int VARIANT>
 constexpr bool is_pipe_variant() {
     return !(VARIANT == 0 || VARIANT == 1 || VARIANT == 2 || VARIANT == 7 || VARIANT >= 16);
 }
+constexpr int variant_ne_of(int ne0, int v) {
+    const int ne = (v == 0 || v == 3 || v == 6 || v == 14)                 ? ne0
+                   : (v == 1 || v == 4 || v == 5 || v == 10 || v == 11)    ? ne0 / 2
+                   : (v == 2 || v == 16)                                   ? ne0 * 2
+                   : (v == 17)                                             ? ne0
+                   : (v == 18)                                             ? ne0 * 4
+                                                                           : ne0 / 4;
+    return ne >= 1 ? ne : 0;
+}
 template <class R, int DIM, int M, int VARIANT>
 constexpr int variant_ne() {
-    constexpr int ne0 = lines_ne_default<R, DIM, M>();
-    constexpr int ne = (VARIANT == 0 || VARIANT == 3 || VARIANT == 6 || VARIANT == 14)     ? ne0
-                       : (VARIANT == 1 || VARIANT == 4 || VARIANT == 5 || VARIANT == 10 ||
-                          VARIANT == 11)                                                     ? ne0 / 2
-                       : (VARIANT == 2 || VARIANT == 16)                                     ? ne0 * 2
-                       : (VARIANT == 17)                                                     ? ne0
-                       : (VARIANT == 18)                                                     ? ne0 * 4
-                                                                                             : ne0 / 4;
-    return ne >= 1 ? ne : 0;
+    return variant_ne_of(lines_ne_default<R, DIM, M>(), VARIANT);
 }
 template <int VARIANT>
 constexpr int pipe_stages() {
@@ -171,6 +182,56 @@ inline bool bulk_layout(int group) {
     return (group % NE == 0) && (NE * sizeof(R)) % 16 == 0 && ((long long)group * sizeof(R)) % 16 == 0;
 }
 
+// Tile mode of the lines kernel (hf_lines.cuh): the caller's AoSoA group is not the
+// kernel's chunk, so a chunk is NE elements x all rows of one group -- a strided box that
+// one TMA tensor copy moves per direction.  TMA needs 16-byte global strides (group * w),
+// a 16-byte box row (NE * w) and 16-byte aligned buffers.
+template <class R, int NE>
+inline bool tile_layout(int group) {
+    return group != NE && (NE * sizeof(R)) % 16 == 0 && ((long long)group * sizeof(R)) % 16 == 0;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+inline EncodeTiled encode_tiled_fn() {
+    static EncodeTiled fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            f = nullptr;
+        }
+        return reinterpret_cast<EncodeTiled>(f);
+    }();
+    return fn;
+}
+
+// The 5-d view {e_l: group, i: m, (j,k): m^(d-1), v: n_v, group index: n_groups} of an
+// AoSoA field (layout.hpp:128-134), box {NE, m, m^(d-1), n_v, 1}: the box lands in shared
+// memory as [v][pt][e_l], exactly the chunk layout of the lines kernel.
+template <class R>
+inline bool encode_chunk_map(CUtensorMap* tm, const void* base, int dim, int m, int group, long long n_groups,
+                             int ne) {
+    EncodeTiled enc = encode_tiled_fn();
+    if (!enc) return false;
+    const int nv = n_vars_c(dim);
+    const long long mh = dim == 3 ? (long long)m * m : m;
+    const cuuint64_t w = sizeof(R);
+    const cuuint64_t dims[5] = {cuuint64_t(group), cuuint64_t(m), cuuint64_t(mh), cuuint64_t(nv),
+                                cuuint64_t(n_groups)};
+    const cuuint64_t strides[4] = {group * w, group * w * m, group * w * m * mh, group * w * m * mh * nv};
+    const cuuint32_t box[5] = {cuuint32_t(ne), cuuint32_t(m), cuuint32_t(mh), cuuint32_t(nv), 1};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    const CUresult r = enc(tm, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5,
+                           const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 template <class K>
 inline int set_smem_attr(K kernel, size_t smem) {
     if (smem > 48 * 1024) {
@@ -201,12 +262,15 @@ inline void fill_regs(K kernel, KInfo* info) {
 inline const char* prec_name(size_t w) { return w == 4 ? "fp32" : "fp64"; }
 
 // Launch (or, with dry = true, only describe) the lines kernel.
-template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false>
+template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false, int GS = NE>
 cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
-    using S = LinesShape<R, DIM, M, NE, LPT>;
-    auto kernel = hf_lines_kernel<R, DIM, M, NE, SRC, LPT, FACES>;
-    const long long grid = (p.n_elem + NE - 1) / NE;
-    const bool fast_layout = bulk_layout<R, NE>(p.group);
+    using S = LinesShape<R, DIM, M, NE, LPT, GS>;
+    auto kernel = hf_lines_kernel<R, DIM, M, NE, SRC, LPT, FACES, GS>;
+    const bool tile = GS == NE && tile_layout<R, NE>(p.group) && (p.u == nullptr || (aligned16(p.u) && aligned16(p.out)));
+    const long long n_groups = (p.n_elem + p.group - 1) / p.group;
+    const int sub = (p.group + NE - 1) / NE;
+    const long long grid = tile ? n_groups * sub : (p.n_elem + NE - 1) / NE;
+    const bool fast_layout = tile || (GS == NE ? bulk_layout<R, NE>(p.group) : p.group == GS);
     if (info) {
         info->method = 2;
         info->elems_per_cta = NE;
@@ -214,9 +278,12 @@ cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
         info->shared_bytes = int(S::SMEM);
         info->grid = grid;
         info->bulk_path = fast_layout ? 1 : 0;
-        if (LPT == 1)
-            std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d%s", DIM, M - 1,
-                          prec_name(sizeof(R)), NE, SRC ? "_src" : "");
+        if (GS != NE)
+            std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d_g%d%s", DIM, M - 1,
+                          prec_name(sizeof(R)), NE, GS, SRC ? "_src" : "");
+        else if (LPT == 1)
+            std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d%s%s", DIM, M - 1,
+                          prec_name(sizeof(R)), NE, tile ? "_tile" : "", SRC ? "_src" : "");
         else
             std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d_l%d%s", DIM, M - 1,
                           prec_name(sizeof(R)), NE, LPT, SRC ? "_src" : "");
@@ -224,6 +291,13 @@ cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
     }
     if (dry || p.n_elem == 0) return cudaSuccess;
     p.fast_ok = fast_layout && aligned16(p.u) && aligned16(p.out);
+    if (tile) {
+        p.tile = 1;
+        p.sub_per_group = sub;
+        if (!encode_chunk_map<R>(&p.tm_u, p.u, DIM, M, p.group, n_groups, NE) ||
+            !encode_chunk_map<R>(&p.tm_out, p.out, DIM, M, p.group, n_groups, NE))
+            p.fast_ok = 0;  // every chunk takes the guarded path (same results)
+    }
     if (int e = set_smem_attr(kernel, S::SMEM)) return cudaError_t(e);
     kernel<<<dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st>>>(p);
     return cudaGetLastError();
@@ -421,6 +495,46 @@ cudaError_t launch_mapped(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
     return cudaGetLastError();
 }
 
+// The staged stage-3 kernel takes a layout when one group's direction block (G * NP * NV
+// words) fits a stage of the two-stage ring and moves with 16-byte bulk copies; a thread
+// owns at most 4 (point, element) outputs.  Otherwise the gather kernel hf_div_kernel.
+template <class R, int DIM, int M>
+inline int div_staged_items(const Params<R>& p) {
+    constexpr int NP = ipow_c(M, DIM), NV = n_vars_c(DIM);
+    const long long blk = (long long)p.group * NP * NV * sizeof(R);
+    if (blk % 16 != 0 || 2 * ((blk + 127) / 128 * 128) + 128 > 200 * 1024) return 0;
+    if (p.u != nullptr && !(aligned16(p.ws) && aligned16(p.out))) return 0;
+    const long long items = ((long long)p.group * NP + 255) / 256;
+    return items <= 1 ? 1 : items <= 2 ? 2 : items <= 4 ? 4 : 0;
+}
+
+// the unfused method's own AoSoA group: the largest power of two whose direction block
+// is at most 48 KB (two stages in flight, at least two CTAs per SM), at least 16-byte rows
+template <class R, int DIM, int M>
+constexpr int unfused_group() {
+    int g = 64;
+    while (g > 16 / int(sizeof(R)) && (long long)g * ipow_c(M, DIM) * n_vars_c(DIM) * sizeof(R) > 48 * 1024) g /= 2;
+    return g;
+}
+
+template <class R, int DIM, int M, int ITEMS>
+cudaError_t launch_div_staged(const Params<R>& p, cudaStream_t st) {
+    using S = DivStagedShape<R, DIM, M, ITEMS>;
+    auto kernel = hf_div_staged_kernel<R, DIM, M, ITEMS>;
+    const int blk = p.group * ipow_c(M, DIM) * n_vars_c(DIM) * int(sizeof(R));
+    const size_t smem = S::HDR + 2 * size_t((blk + 127) / 128 * 128);
+    if (int e = set_smem_attr(kernel, smem)) return cudaError_t(e);
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, S::BS, smem) != cudaSuccess || b < 1) {
+        cudaGetLastError();
+        b = 1;
+    }
+    const long long groups = (p.n_elem + p.group - 1) / p.group;
+    const long long slots = (long long)b * num_sms();
+    kernel<<<unsigned(groups < slots ? groups : slots), S::BS, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
 template <class R, int DIM, int M>
 cudaError_t launch_unfused(Params<R> p, bool src, cudaStream_t st, KInfo* info, bool dry) {
     const long long groups = (p.n_elem + p.group - 1) / p.group;
@@ -437,7 +551,14 @@ cudaError_t launch_unfused(Params<R> p, bool src, cudaStream_t st, KInfo* info, 
     }
     if (dry || p.n_elem == 0) return cudaSuccess;
     hf_flux_kernel<R, DIM, M><<<dim3(unsigned(groups)), dim3(kUnfusedBS), 0, st>>>(p);
-    hf_div_kernel<R, DIM, M><<<dim3(unsigned(groups)), dim3(kUnfusedBS), 0, st>>>(p);
+    cudaError_t e = cudaSuccess;
+    switch (div_staged_items<R, DIM, M>(p)) {
+        case 1: e = launch_div_staged<R, DIM, M, 1>(p, st); break;
+        case 2: e = launch_div_staged<R, DIM, M, 2>(p, st); break;
+        case 4: e = launch_div_staged<R, DIM, M, 4>(p, st); break;
+        default: hf_div_kernel<R, DIM, M><<<dim3(unsigned(groups)), dim3(kUnfusedBS), 0, st>>>(p);
+    }
+    if (e != cudaSuccess) return e;
     if (src) hf_source_kernel<R, DIM, M><<<dim3(unsigned(groups)), dim3(kUnfusedBS), 0, st>>>(p);
     return cudaGetLastError();
 }

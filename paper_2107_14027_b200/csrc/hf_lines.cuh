@@ -48,8 +48,14 @@ namespace hfb {
 // threads): larger chunks per block without more threads, for the low-order
 // cases whose per-line work is small and whose bytes in flight per SM are
 // limited by the thread count.
-template <class R, int DIM, int M, int NE, int LPT = 1>
+// GS: the chunk's shared-memory layout.  GS = NE (default): [v][pt][el], the layout of
+// one AoSoA group of NE elements.  GS < NE (NE a multiple of GS): the chunk is NE/GS
+// whole groups of the caller's group size GS, staged as they lie in HBM,
+// [el / GS][v][pt][el % GS] -- one contiguous byte range for any group that divides the
+// chunk (grouped chunk, hf_launch.cuh launch_lines).
+template <class R, int DIM, int M, int NE, int LPT = 1, int GS = NE>
 struct LinesShape {
+    static_assert(NE % GS == 0, "a grouped chunk holds whole groups");
     static constexpr int NV = n_vars_c(DIM);
     static constexpr int NP = ipow_c(M, DIM);
     static constexpr int LINES = NE * ipow_c(M, DIM - 1);
@@ -64,6 +70,23 @@ struct LinesShape {
     using IO = ChunkIO<R, NE, NP * NV, IN_BYTES>;
     static constexpr int BUF_BYTES = IO::BUF_BYTES;  // chunk buffer incl. alignment slack
     static constexpr size_t SMEM = HDR + size_t(BUF_BYTES) + size_t(ACC_WORDS) * sizeof(R);
+    static constexpr int VS = GS * NP;          // word stride between variables
+    static constexpr int BLK = GS * NP * NV;    // one staged group
+    // word of (element, point, variable) in the staged chunk
+    __host__ __device__ static constexpr int word(int el, int pt, int v) {
+        return (el % GS) + GS * pt + VS * v + (el / GS) * BLK;
+    }
+    // The accumulator region keeps the [row][pt][el] layout of NE elements whatever GS is
+    // (its element classes then spread over the banks; a grouped chunk's state region
+    // cannot be re-laid out -- it is the HBM image).  Offset of the line at chunk offset o:
+    __host__ __device__ static constexpr int acc_of(int o) {
+        if constexpr (GS == NE) {
+            return o;
+        } else {
+            const int blk = o / BLK, rem = o - blk * BLK;
+            return blk * GS + rem % GS + NE * (rem / GS);
+        }
+    }
 };
 
 // Whether the chunk starting at word `gbase` can take the bulk path: full chunk,
@@ -78,10 +101,11 @@ __device__ __forceinline__ bool chunk_bulk_ok(const Params<R>& p, long long gbas
 
 // Outputs of one line point (index i of the sweep's line): gradient rows final
 // (+ source), continuity / momentum partials accumulated or finished.
-template <class R, int DIM, int M, int NE, bool SRC, int A, int PHASE>
+template <class R, int DIM, int M, int NE, bool SRC, int A, int PHASE, int GS = NE>
 __device__ __forceinline__ void lines_emit(R* __restrict__ q, R* __restrict__ a, const Params<R>& p, const R (&dV)[DIM],
                                            const R (&dQ)[DIM]) {
-    constexpr int VS = NE * ipow_c(M, DIM);
+    constexpr int VS = GS * ipow_c(M, DIM);   // state rows
+    constexpr int AS = NE * ipow_c(M, DIM);   // accumulator rows
 #pragma unroll
     for (int b = 0; b < DIM; ++b) {
         R o = p.jac_invT[A] * dV[b];
@@ -92,28 +116,28 @@ __device__ __forceinline__ void lines_emit(R* __restrict__ q, R* __restrict__ a,
     if constexpr (PHASE == 0) {
         a[0] = c;
 #pragma unroll
-        for (int b = 0; b < DIM; ++b) a[VS * (1 + b)] = p.jac[A] * dQ[b];
+        for (int b = 0; b < DIM; ++b) a[AS * (1 + b)] = p.jac[A] * dQ[b];
     } else if constexpr (PHASE == 1) {
         a[0] = a[0] + c;
 #pragma unroll
-        for (int b = 0; b < DIM; ++b) a[VS * (1 + b)] = fma(p.jac[A], dQ[b], a[VS * (1 + b)]);
+        for (int b = 0; b < DIM; ++b) a[AS * (1 + b)] = fma(p.jac[A], dQ[b], a[AS * (1 + b)]);
     } else {
         q[0] = -(p.zeta * (a[0] + c));
 #pragma unroll
-        for (int b = 0; b < DIM; ++b) q[VS * (1 + b)] = -fma(p.jac[A], dQ[b], a[VS * (1 + b)]);
+        for (int b = 0; b < DIM; ++b) q[VS * (1 + b)] = -fma(p.jac[A], dQ[b], a[AS * (1 + b)]);
     }
 }
 
 // Word offset (inside a chunk) of the first point of line L of a sweep along A:
 // L = el + NE * r, r enumerating the two fixed indices (layout.hpp:128-134).
-template <int DIM, int M, int NE, int A>
+template <int DIM, int M, int NE, int A, int GS = NE>
 __host__ __device__ constexpr int line_offset(int L) {
     const int el = L % NE;
     const int r = L / NE;
     int base_pt = r;                                  // d3 A=2: r = i + M j;  d2 A=1: r = i
     if (A == 0) base_pt = M * r;                      // d3: r = j + M k;  d2: r = j
     if (DIM == 3 && A == 1) base_pt = (r % M) + M * M * (r / M);  // r = i + M k
-    return el + NE * base_pt;
+    return (el % GS) + GS * base_pt + (el / GS) * GS * ipow_c(M, DIM) * n_vars_c(DIM);
 }
 
 // Bank-conflict-free assignment of a sweep's lines to (iteration, thread).
@@ -128,7 +152,7 @@ __host__ __device__ constexpr int line_offset(int L) {
 // slots (a conflict, but no extra iteration).  With the natural order (L = t,
 // t + NTHR, ...) the y-sweep conflicts whenever NE*m is not a multiple of the
 // bank count (e.g. 2-way at p6 FP64).  Built at compile time; 0xFFFF = idle.
-template <class R, int DIM, int M, int NE, int A, int NTHR>
+template <class R, int DIM, int M, int NE, int A, int NTHR, int GS = NE>
 struct LineMap {
     static constexpr int LINES = NE * ipow_c(M, DIM - 1);
     static constexpr int ITERS = (LINES + NTHR - 1) / NTHR;
@@ -136,9 +160,9 @@ struct LineMap {
     unsigned short off[N];
 };
 
-template <class R, int DIM, int M, int NE, int A, int NTHR>
-constexpr LineMap<R, DIM, M, NE, A, NTHR> make_line_map() {
-    using LM = LineMap<R, DIM, M, NE, A, NTHR>;
+template <class R, int DIM, int M, int NE, int A, int NTHR, int GS = NE>
+constexpr LineMap<R, DIM, M, NE, A, NTHR, GS> make_line_map() {
+    using LM = LineMap<R, DIM, M, NE, A, NTHR, GS>;
     constexpr int B = sizeof(R) == 4 ? 32 : 16;  // bank classes per (half-)warp
     constexpr int HALVES = 32 / B;
     constexpr int NW = NTHR / 32;
@@ -148,7 +172,7 @@ constexpr LineMap<R, DIM, M, NE, A, NTHR> make_line_map() {
     int spill[LM::LINES > 0 ? LM::LINES : 1] = {};
     int n_spill = 0;
     for (int L = 0; L < LM::LINES; ++L) {
-        const int o = line_offset<DIM, M, NE, A>(L);
+        const int o = line_offset<DIM, M, NE, A, GS>(L);
         const int c = o % B;
         const int idx = next[c]++;
         const int it = idx / (NW * HALVES);
@@ -165,20 +189,19 @@ constexpr LineMap<R, DIM, M, NE, A, NTHR> make_line_map() {
     return m;
 }
 
-template <class R, int DIM, int M, int NE, int A, int NTHR>
-__device__ const LineMap<R, DIM, M, NE, A, NTHR> kLineMap = make_line_map<R, DIM, M, NE, A, NTHR>();
+template <class R, int DIM, int M, int NE, int A, int NTHR, int GS = NE>
+__device__ const LineMap<R, DIM, M, NE, A, NTHR, GS> kLineMap = make_line_map<R, DIM, M, NE, A, NTHR, GS>();
 
 // One sweep along axis A.  PHASE: 0 = first sweep, 1 = middle, 2 = last.
 // `o` = the line's first word inside the chunk (line_offset()).
-template <class R, int DIM, int M, int NE, bool SRC, int A, int PHASE>
+template <class R, int DIM, int M, int NE, bool SRC, int A, int PHASE, int GS = NE>
 __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ acc, const Params<R>& p, int o) {
-    using S = LinesShape<R, DIM, M, NE>;
-    constexpr int NP = S::NP;
-    constexpr int VS = NE * NP;  // word stride between variables
+    using S = LinesShape<R, DIM, M, NE, 1, GS>;
+    constexpr int VS = S::VS;  // word stride between variables
     constexpr int STRIDE = (A == 0) ? 1 : (A == 1) ? M : M * M;  // point stride along the line
 
     R* __restrict__ sb = s + o;
-    R* __restrict__ ab = acc + o;
+    R* __restrict__ ab = acc + S::acc_of(o);
 
     const R nu = p.nu;
     using PR = Pair<R>;
@@ -186,7 +209,7 @@ __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ a
     PR W[DIM][M];
 #pragma unroll
     for (int t = 0; t < M; ++t) {
-        const R* q = sb + NE * STRIDE * t;
+        const R* q = sb + GS * STRIDE * t;
         const R P = q[0];
         R V[DIM];
 #pragma unroll
@@ -211,7 +234,7 @@ __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ a
             dV_[b_] = (DP)[b_].x();                                                                            \
             dQ_[b_] = (DP)[b_].y();                                                                            \
         }                                                                                                      \
-        lines_emit<R, DIM, M, NE, SRC, A, PHASE>(sb + NE * STRIDE * (I), ab + NE * STRIDE * (I), p, dV_, dQ_); \
+        lines_emit<R, DIM, M, NE, SRC, A, PHASE, GS>(sb + GS * STRIDE * (I), ab + NE * STRIDE * (I), p, dV_, dQ_); \
     } while (0)
     if constexpr (M < HF_EVEN_ODD_MIN_M) {
 #pragma unroll
@@ -287,19 +310,20 @@ __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ a
 // FACES: FR stage 1 fused in (hf_fr.cuh): before the sweeps overwrite the staged
 // chunk, every a-line of every variable is extrapolated to xi_a = -1, +1 and
 // written to p.uf -- the face projection without a second read of the field.
-template <class R, int DIM, int M, int NE>
+template <class R, int DIM, int M, int NE, int GS = NE>
 __device__ __forceinline__ void lines_project_faces(const R* __restrict__ s, const Params<R>& p, long long E0, int t,
-                                                    int nthr) {
-    constexpr int NP = ipow_c(M, DIM), NV = n_vars_c(DIM), LN = ipow_c(M, DIM - 1);
+                                                    int nthr, int nvalid) {
+    using S = LinesShape<R, DIM, M, NE, 1, GS>;
+    constexpr int NV = n_vars_c(DIM), LN = ipow_c(M, DIM - 1);
     for (int task = t; task < NE * LN * DIM; task += nthr) {
         const int el = task % NE;
         const int l = (task / NE) % LN;
         const int a = task / (NE * LN);
         const long long e = E0 + el;
-        if (e >= p.n_elem) continue;
+        if (el >= nvalid || e >= p.n_elem) continue;
         int pt[M];
 #pragma unroll
-        for (int q = 0; q < M; ++q) pt[q] = el + NE * fr_line_point<DIM, M>(a, l, q);
+        for (int q = 0; q < M; ++q) pt[q] = S::word(el, fr_line_point<DIM, M>(a, l, q), 0);
         const long long ge = e / p.group;
         R* ub = p.uf + ge * p.group * 2 * DIM * LN * NV + (e - ge * p.group) + (long long)p.group * (l + LN * 2 * a);
 #pragma unroll
@@ -307,7 +331,7 @@ __device__ __forceinline__ void lines_project_faces(const R* __restrict__ s, con
             R sm = R(0), sp = R(0);
 #pragma unroll
             for (int q = 0; q < M; ++q) {
-                const R u = s[pt[q] + NE * NP * v];
+                const R u = s[pt[q] + S::VS * v];
                 sm = fma(p.lm[q], u, sm);
                 sp = fma(p.lp[q], u, sp);
             }
@@ -318,10 +342,9 @@ __device__ __forceinline__ void lines_project_faces(const R* __restrict__ s, con
     }
 }
 
-template <class R, int DIM, int M, int NE, bool SRC, int HEADB, int BAR, int NTHR, bool FACES = false>
+template <class R, int DIM, int M, int NE, bool SRC, int HEADB, int BAR, int NTHR, bool FACES = false, int GS = NE>
 __device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const Params<R>& p, int t, int bar_id = 0,
-                                             long long E0 = 0) {
-    using S = LinesShape<R, DIM, M, NE>;
+                                             long long E0 = 0, int nvalid = NE) {
     R* s = reinterpret_cast<R*>(buf + HEADB);
 #ifdef HF_IO_ONLY  // measurement build: chunk traffic only, no sweeps (tools/gpu_ab_io.sh)
     return;
@@ -335,19 +358,19 @@ __device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const P
     auto sweep = [&](auto a_tag, auto phase_tag) {
         constexpr int A = decltype(a_tag)::value;
         constexpr int PH = decltype(phase_tag)::value;
-        using LM = LineMap<R, DIM, M, NE, A, NTHR>;
-        const unsigned short* map = kLineMap<R, DIM, M, NE, A, NTHR>.off;
+        using LM = LineMap<R, DIM, M, NE, A, NTHR, GS>;
+        const unsigned short* map = kLineMap<R, DIM, M, NE, A, NTHR, GS>.off;
 #pragma unroll 1
         for (int k = 0; k < LM::ITERS; ++k) {
             const int o = map[k * NTHR + t];
-            if (o != 0xFFFF) lines_sweep<R, DIM, M, NE, SRC, A, PH>(s, acc, p, o);
+            if (o != 0xFFFF) lines_sweep<R, DIM, M, NE, SRC, A, PH, GS>(s, acc, p, o);
         }
     };
     using I0 = std::integral_constant<int, 0>;
     using I1 = std::integral_constant<int, 1>;
     using I2 = std::integral_constant<int, 2>;
     if constexpr (FACES) {
-        lines_project_faces<R, DIM, M, NE>(s, p, E0, t, NTHR);
+        lines_project_faces<R, DIM, M, NE, GS>(s, p, E0, t, NTHR, nvalid);
         sync();  // every line is read before sweep 0 writes in place
     }
     if constexpr (DIM == 3) {
@@ -365,28 +388,28 @@ __device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const P
 
 // Runtime head (bytes, a multiple of sizeof(R), < 16) -> compile-time HEADB.
 // Chunks whose byte size is a multiple of 16 always start aligned: one instance.
-template <class R, int DIM, int M, int NE, bool SRC, int BAR, int NTHR, bool FACES = false>
+template <class R, int DIM, int M, int NE, bool SRC, int BAR, int NTHR, bool FACES = false, int GS = NE>
 __device__ __forceinline__ void lines_sweeps_at(unsigned char* buf, int head, R* acc, const Params<R>& p, int t,
-                                                int bar_id = 0, long long E0 = 0) {
+                                                int bar_id = 0, long long E0 = 0, int nv = NE) {
     if constexpr (LinesShape<R, DIM, M, NE>::IN_BYTES % 16 == 0) {
-        lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES>(buf, acc, p, t, bar_id, E0);
+        lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES, GS>(buf, acc, p, t, bar_id, E0, nv);
     } else if constexpr (sizeof(R) == 8) {
-        if (head == 0) lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES>(buf, acc, p, t, bar_id, E0);
-        else lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR, FACES>(buf, acc, p, t, bar_id, E0);
+        if (head == 0) lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES, GS>(buf, acc, p, t, bar_id, E0, nv);
+        else lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR, FACES, GS>(buf, acc, p, t, bar_id, E0, nv);
     } else {
         switch (head) {
-            case 0: lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES>(buf, acc, p, t, bar_id, E0); break;
-            case 4: lines_sweeps<R, DIM, M, NE, SRC, 4, BAR, NTHR, FACES>(buf, acc, p, t, bar_id, E0); break;
-            case 8: lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR, FACES>(buf, acc, p, t, bar_id, E0); break;
-            default: lines_sweeps<R, DIM, M, NE, SRC, 12, BAR, NTHR, FACES>(buf, acc, p, t, bar_id, E0); break;
+            case 0: lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES, GS>(buf, acc, p, t, bar_id, E0, nv); break;
+            case 4: lines_sweeps<R, DIM, M, NE, SRC, 4, BAR, NTHR, FACES, GS>(buf, acc, p, t, bar_id, E0, nv); break;
+            case 8: lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR, FACES, GS>(buf, acc, p, t, bar_id, E0, nv); break;
+            default: lines_sweeps<R, DIM, M, NE, SRC, 12, BAR, NTHR, FACES, GS>(buf, acc, p, t, bar_id, E0, nv); break;
         }
     }
 }
 
-template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false>
-__global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT>::BS)
+template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false, int GS = NE>
+__global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT, GS>::BS)
     hf_lines_kernel(const __grid_constant__ Params<R> p) {
-    using S = LinesShape<R, DIM, M, NE, LPT>;
+    using S = LinesShape<R, DIM, M, NE, LPT, GS>;
     constexpr int BS = S::BS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     using IO = typename S::IO;
@@ -395,13 +418,27 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT>::BS)
     R* acc = reinterpret_cast<R*>(buf + S::BUF_BYTES);
 
     const int tid = threadIdx.x;
-    const long long E0 = (p.chunk0 + static_cast<long long>(blockIdx.x)) * NE;
-    const long long grp = E0 / p.group;
+    // chunk -> first element E0 and its nvalid elements: NE consecutive elements, or in
+    // tile mode sub-chunk `sub` of group `grp` (the group's last sub-chunk may be short)
+    const long long b = p.chunk0 + static_cast<long long>(blockIdx.x);
+    long long grp, E0;
+    int sub = 0, nvalid = NE;
+    if (p.tile) {
+        grp = b / p.sub_per_group;
+        sub = static_cast<int>(b - grp * p.sub_per_group);
+        E0 = grp * p.group + sub * NE;
+        nvalid = p.group - sub * NE < NE ? p.group - sub * NE : NE;
+    } else {
+        E0 = b * NE;
+        grp = E0 / p.group;
+    }
     const int el0 = static_cast<int>(E0 - grp * p.group);
     const long long gbase = grp * p.group_words + el0;
-    const bool contiguous = (p.group == NE);
-    const bool fast = chunk_bulk_ok<R, S::IN_WORDS>(p, gbase, E0 + NE <= p.n_elem, contiguous);
-    const int head = fast ? IO::head_bytes(p.u + gbase, contiguous) : 0;
+    // one contiguous byte range: the chunk is one group (GS = NE) or NE / GS whole groups
+    const bool contiguous = (p.group == GS);
+    const bool full = E0 + nvalid <= p.n_elem;
+    const bool fast = p.tile ? (p.fast_ok && full) : chunk_bulk_ok<R, S::IN_WORDS>(p, gbase, full, contiguous);
+    const int head = (fast && !p.tile) ? IO::head_bytes(p.u + gbase, contiguous) : 0;
     R* s = reinterpret_cast<R*>(smem_raw + S::HDR);  // guarded path (head == 0)
 
     // ---------------- stage the chunk into shared memory ----------------
@@ -411,7 +448,12 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT>::BS)
             fence_mbar_init();
         }
         __syncthreads();
-        if (tid < 32) {
+        if (p.tile) {
+            if (tid == 0) {  // one TMA tensor copy: the box {NE, m, m^(d-1), n_v, 1}; e_l >= group zero-filled
+                mbar_arrive_expect_tx(bar, uint32_t(S::IN_BYTES));
+                tma_load_5d(buf, &p.tm_u, sub * NE, 0, 0, 0, static_cast<int>(grp), bar);
+            }
+        } else if (tid < 32) {
             if (tid == 0) mbar_arrive_expect_tx(bar, IO::tx_bytes(p.u + gbase, contiguous));
             __syncwarp();
             IO::load(buf, p.u + gbase, p.group, contiguous, bar, tid);
@@ -419,11 +461,12 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT>::BS)
         mbar_wait_parity(bar, 0);
     } else {
         for (int idx = tid; idx < S::IN_WORDS; idx += BS) {
-            const int el = idx % NE;
-            const int row = idx / NE;
+            const int blk = idx / S::BLK, rem = idx - blk * S::BLK;  // staged word -> (el, row)
+            const int el = blk * GS + rem % GS;
+            const int row = rem / GS;
             const long long e = E0 + el;
             R v = R(0);
-            if (e < p.n_elem) {
+            if (el < nvalid && e < p.n_elem) {
                 const long long ge = e / p.group;
                 v = ld_stream(p.u + ge * p.group_words + (e - ge * p.group) + static_cast<long long>(p.group) * row);
             }
@@ -433,23 +476,30 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT>::BS)
     }
 
     // ---------------- d sweeps ----------------
-    lines_sweeps_at<R, DIM, M, NE, SRC, 0, BS, FACES>(buf, head, acc, p, tid, 0, E0);
+    lines_sweeps_at<R, DIM, M, NE, SRC, 0, BS, FACES, GS>(buf, head, acc, p, tid, 0, E0, nvalid);
 
     // ---------------- write the finished chunk ----------------
     if (fast) {
         fence_proxy_async_smem();
         __syncthreads();
-        if (tid < 32) {
+        if (p.tile) {
+            if (tid == 0) {  // elements past the group's end are clipped by the tensor map
+                tma_store_5d(&p.tm_out, sub * NE, 0, 0, 0, static_cast<int>(grp), buf);
+                bulk_commit();
+                bulk_wait_read_all();
+            }
+        } else if (tid < 32) {
             IO::store(p.out + gbase, buf, p.group, contiguous, tid);
             bulk_wait_read_all();
         }
     } else {
         __syncthreads();
         for (int idx = tid; idx < S::IN_WORDS; idx += BS) {
-            const int el = idx % NE;
-            const int row = idx / NE;
+            const int blk = idx / S::BLK, rem = idx - blk * S::BLK;
+            const int el = blk * GS + rem % GS;
+            const int row = rem / GS;
             const long long e = E0 + el;
-            if (e < p.n_elem) {
+            if (el < nvalid && e < p.n_elem) {
                 const long long ge = e / p.group;
                 p.out[ge * p.group_words + (e - ge * p.group) + static_cast<long long>(p.group) * row] = s[idx];
             }

@@ -25,7 +25,6 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
-import json
 import threading
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -203,30 +202,36 @@ def field_sidecar(f: StateField) -> dict:
             "precision": f.precision.name, "words": f.total_words(), "byte_order": "little"}
 
 
+def _shape_problem(f: StateField) -> hf_problem:
+    return make_problem(f.d, f.p, f.n_elem, f.group, f.precision, PhysParams())
+
+
 def export_blob(f: StateField, path: str) -> None:
-    """layout.hpp:163-177: flat little-endian words + <path>.json sidecar."""
-    dt = "<f4" if f.precision == Precision.fp32 else "<f8"
-    f.data.astype(dt).tofile(path)
-    with open(path + ".json", "w") as fh:
-        fh.write(json.dumps(field_sidecar(f), indent=2) + "\n")
+    """layout.hpp:161-177 through hf_blob_write: flat little-endian words + <path>.json
+    sidecar, byte-identical to the reference's export_blob."""
+    words = np.ascontiguousarray(f.words())
+    check(_lib.load().hf_blob_write(path.encode(), C.byref(_shape_problem(f)), words.ctypes.data), "export_blob")
 
 
 def import_blob(path: str) -> StateField:
-    """layout.hpp:179-200"""
-    try:
-        with open(path + ".json") as fh:
-            j = json.load(fh)
-    except OSError:
-        raise HexfuseError(f"import_blob: missing sidecar {path}.json")
-    f = StateField(j["d"], j["p"], j["n_elem"], j["group"], Precision[j["precision"]])
-    if f.total_words() != j["words"]:
-        raise HexfuseError("import_blob: sidecar word count mismatch")
-    dt = "<f4" if f.precision == Precision.fp32 else "<f8"
-    raw = np.fromfile(path, dtype=dt)
-    if raw.size < f.total_words():
-        raise HexfuseError("import_blob: short read")
-    f.data = raw[: f.total_words()].astype(np.float64)
+    """layout.hpp:179-200 through hf_blob_info / hf_blob_read."""
+    pr = hf_problem()
+    pr.zeta = pr.T = 1.0
+    check(_lib.load().hf_blob_info(path.encode(), C.byref(pr)), "import_blob")
+    f = StateField(pr.d, pr.p, pr.n_elem, pr.group, Precision(pr.precision))
+    raw = np.zeros(f.total_words(), dtype=np.float32 if f.precision == Precision.fp32 else np.float64)
+    check(_lib.load().hf_blob_read(path.encode(), C.byref(pr), raw.ctypes.data), "import_blob")
+    f.data = raw.astype(np.float64)
     return f
+
+
+def fused_divergence_blob(in_path: str, out_path: str, params: PhysParams, jac: Sequence[float] = (1.0, 1.0, 1.0),
+                          with_source: bool = False, method: Method = Method.auto) -> None:
+    """A state blob in, its divergence blob out (hf_fused_divergence_blob, the host path)."""
+    params.validate()
+    pr = make_problem(3, 1, 0, 1, Precision.fp64, params, jac, with_source, method)
+    check(_lib.load().hf_fused_divergence_blob(_context()._h, C.byref(pr), in_path.encode(), out_path.encode()),
+          "hf_fused_divergence_blob")
 
 
 def field_rel_error(got: StateField, ref: StateField) -> float:

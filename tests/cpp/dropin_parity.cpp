@@ -77,6 +77,42 @@ int main() {
             }
         }
     }
+    // state blobs (layout.hpp:155-200): the reference's export_blob read back through the B200
+    // library bit-exactly, a blob-in / blob-out divergence read by the reference's import_blob,
+    // and the B200 library's export byte-identical to the reference's
+    for (Precision prec : {Precision::fp64, Precision::fp32}) {
+        ElementConfig c;
+        c.p = 3;
+        c.n_elem = 45;
+        c.block_threads = 128;
+        c.precision = prec;
+        c.method = Method::PlanarUnmanaged;
+        const StateField U = random_field(c, 31);
+        const std::string a = "/tmp/hexfuse_b200_dropin_a.bin", b = "/tmp/hexfuse_b200_dropin_b.bin",
+                          r = "/tmp/hexfuse_b200_dropin_r.bin";
+        export_blob(U, a);
+        const StateField V = hexfuse_b200::import_blob_b200<StateField>(a);
+        bool same = V.d == U.d && V.p == U.p && V.n_elem == U.n_elem && V.group == U.group &&
+                    V.precision == U.precision && V.data == U.data;
+        hexfuse_b200::fused_divergence_blob(a, b, par, {1.0, 0.5, 2.0}, true);
+        const StateField out = import_blob(b);
+        const double e = field_rel_error(out, oracle_divergence(U, par, {1.0, 0.5, 2.0}, true));
+        hexfuse_b200::export_blob_b200(U, r);
+        auto slurp = [](const std::string& f) {
+            std::FILE* h = std::fopen(f.c_str(), "rb");
+            std::string t;
+            char buf[4096];
+            size_t n;
+            while (h && (n = std::fread(buf, 1, sizeof buf, h)) > 0) t.append(buf, n);
+            if (h) std::fclose(h);
+            return t;
+        };
+        same = same && slurp(a) == slurp(r) && slurp(a + ".json") == slurp(r + ".json");
+        const double tol = prec == Precision::fp32 ? 1e-5 : 1e-12;
+        std::printf("blob %s import/export %s, divergence err=%.3e %s\n", to_string(prec), same ? "bit-exact" : "DIFFER",
+                    e, same && e <= tol ? "ok" : "FAIL");
+        failures += same && e <= tol ? 0 : 1;
+    }
     // error mapping: invalid params -> std::invalid_argument, like the reference
     try {
         hexfuse_b200::fused_divergence_b200(U, PhysParams{-1.0, 2.5, 1.0}, {1, 1, 1}, false);

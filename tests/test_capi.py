@@ -98,7 +98,11 @@ def test_selection_and_kernel_info_without_device():
                 assert meth in (Method.lines, Method.planar)
                 info = hf.kernel_info(pr)
                 g = hf.preferred_group(pr)
-                assert g == info["elems_per_cta"] >= 1
+                # group 1 (element-major storage): a one-element chunk when a variant has it,
+                # else whole one-element groups per chunk (grouped chunk) -- contiguous either way
+                assert g >= 1 and info["bulk_path"]
+                assert info["elems_per_cta"] == 1 or info["name"].endswith("_g1"), info["name"]
+                assert hf.kernel_info(hf.make_problem(d, p, 1000, g, prec, PhysParams()))["elems_per_cta"] == g
                 assert info["shared_bytes"] <= 227 * 1024
                 assert info["block_threads"] % 32 == 0
                 # with group == elements per CTA every full chunk is one contiguous range: bulk path

@@ -114,3 +114,27 @@ def test_host_path_in_place(cuda, pinned):
     ctx.run(pr, buf, buf)
     ctx.close()
     assert torch.equal(buf, ref)
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+def test_blob_in_divergence_blob_out(cuda, tmp_path, fp32):
+    """hf_fused_divergence_blob: a blob the reference's export_blob wrote (or the library's
+    byte-identical one where the reference is absent) -> the B200 host path -> a result
+    blob equal to the oracle's divergence."""
+    import paper_2107_14027_b200 as hf
+    from paper_2107_14027_b200 import Precision
+    d, p, n, g = 3, 3, 45, 32
+    U = O.random_field(d, p, n, g, fp32, 31)
+    src = str(tmp_path / "u.bin")
+    if O.ref_available():
+        O.ref_export_blob(d, p, n, g, fp32, U, src)
+    else:
+        hf.export_blob(hf.StateField(d, p, n, g, Precision.fp32 if fp32 else Precision.fp64, U), src)
+    dst = str(tmp_path / "div.bin")
+    hf.fused_divergence_blob(src, dst, PAR, (1.0, 0.5, 2.0), with_source=True)
+    out = hf.import_blob(dst)
+    assert (out.d, out.p, out.n_elem, out.group) == (d, p, n, g)
+    ref = O.oracle_divergence(d, p, n, g, U, PAR.nu, PAR.zeta, PAR.T, (1.0, 0.5, 2.0), True)
+    assert O.field_rel_error(d, p, n, g, out.data, ref) <= (1e-5 if fp32 else 1e-12)
+    real = np.broadcast_to((np.arange(g) < n - g)[None, :], (13 * 64, g)).reshape(-1)
+    assert np.all(out.data[-13 * 64 * g:][~real] == 0.0)  # padding of the partial group comes back zero

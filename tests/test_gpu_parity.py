@@ -241,3 +241,37 @@ def test_empty_problems_are_no_ops(cuda):
             U = hf.StateField(d, p, 0, 4, prec)
             out = hf.fused_divergence(U, PAR, with_source=True)
             assert out.n_elem == 0 and out.data.size == 0
+
+
+# ---------------------------------------------------------------- caller-chosen AoSoA groups (tile mode)
+# The reference's own groups: planar 4*floor(32/m) (p1 64, p2 40, p3 32, p4 24, p5 20, p6 16)
+# and the preset lines blocks (fp64 p3 192/16 = 12, p4 200/25 = 8; layout.hpp:76-85,
+# presets.hpp:25-37), plus odd groups whose stride rules TMA out (guarded path).
+@pytest.mark.parametrize("fp32", [False, True])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6])
+def test_caller_groups_d3(cuda, p, fp32):
+    import paper_2107_14027_b200 as hf
+    from paper_2107_14027_b200 import Precision
+    groups = sorted({64, 40, 32, 24, 20, 16, 12, 8, 4 * (32 // (p + 1)), 15, 5, 4, 2, 1})
+    for gi, g in enumerate(groups):
+        n = 2 * g + (g // 2 + 1) + 150  # full chunks of every chunk size + a partial last group
+        U = _field(3, p, n, g, fp32, 4000 + 10 * p + gi)
+        check_parity(3, p, n, g, fp32, U, with_source=(gi % 2 == 0))
+    pr = hf.make_problem(3, p, 100, 40, Precision.fp32 if fp32 else Precision.fp64, PAR)
+    name = hf.kernel_info(pr)["name"]
+    assert "_tile" in name or "ne40" in name, name
+
+
+@pytest.mark.parametrize("p", [1, 3, 5, 8])
+def test_caller_groups_d2(cuda, p):
+    for gi, g in enumerate((12, 24, 40, 64, 7, 1, 2, 4)):
+        n = 3 * g + 2 + 260
+        for fp32 in (True, False):
+            U = _field(2, p, n, g, fp32, 6000 + p + gi)
+            check_parity(2, p, n, g, fp32, U, with_source=fp32, jac=(1.0, 0.5, 0.0))
+
+
+def test_tile_mode_with_misaligned_buffers_takes_the_guarded_path(cuda):
+    """An 8-byte offset (not 16) rules TMA out: same results through the guarded path."""
+    U = _field(3, 3, 70, 32, False, 8)
+    check_parity(3, 3, 70, 32, False, U, offset_bytes=8)

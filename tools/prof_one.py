@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--points", type=float, default=1e7)
     ap.add_argument("--launches", type=int, default=3)
     ap.add_argument("--src", action="store_true")
+    ap.add_argument("--group", type=int, default=0, help="AoSoA group (default: the kernel's chunk)")
     a = ap.parse_args()
     prec = Precision[a.prec]
     method = Method[a.method]
@@ -36,6 +37,8 @@ def main():
         g = hf.preferred_group(pr0)
     else:
         g = hf.variant_info(pr0, method, a.variant)["elems_per_cta"] if method != Method.unfused else 32
+    if a.group > 0:
+        g = a.group
     npt = (a.p + 1) ** a.d
     n = max(g, int(a.points / npt) // g * g)
     pr = hf.make_problem(a.d, a.p, n, g, prec, par, with_source=a.src, method=method)
