@@ -292,15 +292,18 @@ hfb::FrParams<R> make_fr_params(const hf_problem* pr, const hf_mesh* mesh, const
 constexpr int kGroupedVariant = 100;
 
 // A caller's AoSoA group that is not the selected chunk (e.g. the reference's planar group
-// 4*floor(32/m), or a solver's own AoSoA width): the one-chunk variant predicted fastest,
-//   the group itself when a variant has that chunk size (one contiguous chunk), else in
-//   tile mode max over NE of  fill(G, NE) * rows(NE * w) * occupancy(CTAs per SM),
-// calibrated on B200 (tools/tile_probe.py, profiles/r02/tile_probe_d3.jsonl): TMA moves a
-// tile box at about one row per 3 SM cycles whatever the row length up to 32 B, so 16-byte
-// rows cap a kernel near 0.53 of the HBM roofline, 32-byte rows near 0.9, >= 64-byte rows
-// reach it; one resident CTA per SM serialises load, sweeps and store (~0.6); fill is the
-// used fraction of the group's sub-chunks (G = 20 in chunks of 16: 20 / 32).
-// Groups whose stride is not a 16-byte multiple take the guarded path of the selected size.
+// 4*floor(32/m), or a solver's own AoSoA width): the chunk predicted fastest among
+//   exact    a one-chunk variant whose chunk is the group (one contiguous range),
+//   grouped  NE0 / G whole groups per chunk (a power-of-two group below NE0; contiguous),
+//   tile     a strided box of NE elements of one group, one TMA tensor copy per direction,
+// scored  fill(G, NE) * rows(NE * w) * occupancy(CTAs per SM), calibrated on B200
+// (tools/tile_probe.py, profiles/r02/tile_probe_d3.jsonl): TMA moves a tile box at about
+// one row per 3 SM cycles whatever the row length up to 32 B, so 16-byte rows cap a kernel
+// near 0.53 of the HBM roofline, 32-byte rows near 0.9, >= 64-byte rows (and contiguous
+// chunks) reach it; one resident CTA per SM serialises load, sweeps and store (~0.6); fill
+// is the used fraction of the group's sub-chunks (G = 20 in chunks of 16: 20 / 32).  Ties go
+// to exact, then grouped, then tile.  Groups whose stride is not a 16-byte multiple and
+// match no chunk take the guarded path of the selected chunk size.
 template <class R>
 int lines_variant_for_group(const hf_problem* pr, int variant, const hfb::Params<R>& prm, bool faces) {
     const int w = int(sizeof(R)), m = pr->p + 1, G = pr->group;
@@ -317,10 +320,23 @@ int lines_variant_for_group(const hf_problem* pr, int variant, const hfb::Params
                             : hfb::lines_f64_d2(pr->p, v, false, prm, nullptr, nullptr, true, faces);
         return rc == 0;
     };
+    const int64_t np = ipow64(m, pr->d), nv = 1 + pr->d + pr->d * pr->d;
+    auto occupancy = [&](int ne) {  // shared memory of hf_lines_kernel (LinesShape::SMEM), 228 KB per SM
+        const int64_t smem = 128 + ((ne * np * nv * w + 15) / 16 * 16 + 32) + ne * np * (1 + pr->d) * w;
+        const int64_t bps = (228 * 1024) / (smem + 1024);
+        return bps >= 3 ? 1.0 : bps == 2 ? 0.95 : 0.6;
+    };
+    int best = -1;
+    double best_score = -1.0;
+    auto consider = [&](int v, double score) {
+        if (score > best_score + 1e-9) {
+            best = v;
+            best_score = score;
+        }
+    };
     const int cand[4] = {0, 1, 7, 2};
     for (int v : cand)
-        if (hfb::variant_ne_of(ne0, v) == G && available(v)) return v;
-    // a power-of-two group below the chunk: NE0 / G whole groups per chunk, contiguous
+        if (hfb::variant_ne_of(ne0, v) == G && available(v)) consider(v, occupancy(G));
     if (!faces && G < ne0 && (G & (G - 1)) == 0 && ne0 % G == 0) {
         int rc;
         if constexpr (sizeof(R) == 4)
@@ -329,29 +345,19 @@ int lines_variant_for_group(const hf_problem* pr, int variant, const hfb::Params
         else
             rc = pr->d == 3 ? hfb::lines_grouped_f64_d3(pr->p, G, false, prm, nullptr, nullptr, true)
                             : hfb::lines_grouped_f64_d2(pr->p, G, false, prm, nullptr, nullptr, true);
-        if (rc == 0) return kGroupedVariant;
+        if (rc == 0) consider(kGroupedVariant, occupancy(ne0));
     }
-    if ((int64_t(G) * w) % 16 != 0) return hfb::is_one_chunk_variant(variant) ? variant : 0;
-    const int64_t np = ipow64(m, pr->d), nv = 1 + pr->d + pr->d * pr->d;
-    int best = -1;
-    double best_score = -1.0;
-    for (int v : cand) {
-        const int ne = hfb::variant_ne_of(ne0, v);
-        if (ne < 1 || (ne * w) % 16 != 0 || !available(v)) continue;
-        const double fill = double(G) / (double((G + ne - 1) / ne) * ne);
-        const int row = ne * w;
-        const double rows = row >= 64 ? 1.0 : row >= 32 ? 0.9 : 0.53;
-        // shared memory of hf_lines_kernel (LinesShape::SMEM) and CTAs per SM (228 KB, 1 KB reserved per CTA)
-        const int64_t smem = 128 + ((ne * np * nv * w + 15) / 16 * 16 + 32) + ne * np * (1 + pr->d) * w;
-        const int64_t bps = (228 * 1024) / (smem + 1024);
-        const double occ = bps >= 3 ? 1.0 : bps == 2 ? 0.95 : 0.6;
-        const double score = fill * rows * occ;
-        if (score > best_score + 1e-9) {
-            best = v;
-            best_score = score;
+    if ((int64_t(G) * w) % 16 == 0) {
+        for (int v : cand) {
+            const int ne = hfb::variant_ne_of(ne0, v);
+            if (ne < 1 || ne == G || (ne * w) % 16 != 0 || !available(v)) continue;
+            const double fill = double(G) / (double((G + ne - 1) / ne) * ne);
+            const int row = ne * w;
+            consider(v, fill * (row >= 64 ? 1.0 : row >= 32 ? 0.9 : 0.53) * occupancy(ne));
         }
     }
-    return best >= 0 ? best : (hfb::is_one_chunk_variant(variant) ? variant : 0);
+    if (best >= 0) return best;
+    return hfb::is_one_chunk_variant(variant) ? variant : 0;
 }
 
 // Resolve + launch (dry: describe only).  ws only for the unfused method.

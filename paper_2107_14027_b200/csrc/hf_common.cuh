@@ -164,6 +164,13 @@ __device__ __forceinline__ void bulk_wait_read_all() {
 }
 
 
+// Programmatic dependent launch (launch_kernel in hf_launch.cuh sets the attribute): a
+// kernel may be scheduled while the previous kernel of its stream drains; it waits for
+// that kernel's completion and memory flush before its first global access.  No-ops for
+// an ordinary launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // make generic-proxy shared-memory writes visible to the async proxy (bulk store)
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

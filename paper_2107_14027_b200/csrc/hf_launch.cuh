@@ -13,6 +13,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "hf_common.cuh"
@@ -232,6 +233,38 @@ inline bool encode_chunk_map(CUtensorMap* tm, const void* base, int dim, int m, 
     return r == CUDA_SUCCESS;
 }
 
+// Kernel launch with programmatic dependent launch (PDL): consecutive fused launches on
+// a stream overlap one kernel's launch and ramp-up with the previous one's tail; the
+// kernels wait (griddepcontrol.wait) before touching HBM, so stream order is kept.
+// HF_PDL=0 in the environment launches without the attribute (A/B measurements).
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("HF_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <class R>
+inline cudaError_t launch_kernel(void (*kernel)(Params<R>), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                 const Params<R>& p) {
+    if (!pdl_enabled()) {
+        kernel<<<grid, block, smem, st>>>(p);
+        return cudaGetLastError();
+    }
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, p);
+}
+
 template <class K>
 inline int set_smem_attr(K kernel, size_t smem) {
     if (smem > 48 * 1024) {
@@ -298,9 +331,15 @@ cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
             !encode_chunk_map<R>(&p.tm_out, p.out, DIM, M, p.group, n_groups, NE))
             p.fast_ok = 0;  // every chunk takes the guarded path (same results)
     }
-    if (int e = set_smem_attr(kernel, S::SMEM)) return cudaError_t(e);
-    kernel<<<dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st>>>(p);
-    return cudaGetLastError();
+    size_t smem = S::SMEM;
+#ifdef HF_OCC_PROBE  // measurement build: HF_LINES_MAXCTA=N pads shared memory to <= N CTAs per SM
+    if (const char* cap = std::getenv("HF_LINES_MAXCTA")) {
+        const size_t want = (228 * 1024) / size_t(std::atoi(cap)) - 1024;
+        if (want > smem && want <= size_t(kMaxSmemPerCta)) smem = want;
+    }
+#endif
+    if (int e = set_smem_attr(kernel, smem)) return cudaError_t(e);
+    return launch_kernel<R>(kernel, dim3(unsigned(grid)), dim3(S::BS), smem, st, p);
 }
 
 inline int num_sms() {
@@ -372,16 +411,14 @@ cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dr
     if (!p.fast_ok || n_full == 0) return launch_lines<R, DIM, M, NE, SRC, 1, FACES>(p, st, nullptr, false);
     p.chunk0 = 0;
     p.n_chunks = n_full;
-    kernel<<<dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st>>>(p);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_kernel<R>(kernel, dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st, p);
     if (e != cudaSuccess) return e;
     const long long n_chunks = (p.n_elem + NE - 1) / NE;
     if (n_full < n_chunks) {  // the partial (or allocation-final) chunk(s)
         auto tail = hf_lines_kernel<R, DIM, M, NE, SRC, 1, FACES>;
         if (int e2 = set_smem_attr(tail, L::SMEM)) return cudaError_t(e2);
         p.chunk0 = n_full;
-        tail<<<unsigned(n_chunks - n_full), L::BS, L::SMEM, st>>>(p);
-        e = cudaGetLastError();
+        e = launch_kernel<R>(tail, dim3(unsigned(n_chunks - n_full)), dim3(L::BS), L::SMEM, st, p);
     }
     return e;
 }

@@ -418,6 +418,8 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT, GS>::BS)
     R* acc = reinterpret_cast<R*>(buf + S::BUF_BYTES);
 
     const int tid = threadIdx.x;
+    pdl_launch_dependents();  // the next kernel of the stream may take SM slots as chunks retire
+    pdl_wait();               // ... and this one reads / writes HBM only after the previous kernel
     // chunk -> first element E0 and its nvalid elements: NE consecutive elements, or in
     // tile mode sub-chunk `sub` of group `grp` (the group's last sub-chunk may be short)
     const long long b = p.chunk0 + static_cast<long long>(blockIdx.x);

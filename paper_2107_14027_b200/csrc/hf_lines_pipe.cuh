@@ -106,6 +106,8 @@ __global__ void __launch_bounds__(PipeShape<R, DIM, M, NE, STAGES, GROUPS>::BS)
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
+    pdl_launch_dependents();
+    pdl_wait();
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);

@@ -59,7 +59,7 @@ int main() {
     // every reference kernel method (layout.hpp:18) through method_of(): planar, managed planar, lines
     for (Method m : {Method::PlanarUnmanaged, Method::PlanarManaged, Method::Lines}) {
         for (Precision prec : {Precision::fp64, Precision::fp32}) {
-            for (int p : {2, 5}) {
+            for (int p : {2, 5, 7}) {
                 ElementConfig c;
                 c.p = p;
                 c.n_elem = 97;

@@ -28,12 +28,14 @@ def load_launches(path):
     return list(per.values())
 
 
-def main(csv_path, bench_path, out_path):
+def main(csv_path, bench_path, out_path, steps=None):
+    """`steps`: the leading step-major steps of the launch list to use (bench.py's warm-up
+    steps; its roofline pass is case-major)."""
     launches = load_launches(csv_path)
     bench = json.loads(open(bench_path).read().strip().splitlines()[-1])
     cases = bench["cases"]
     n = len(cases)
-    steps = len(launches) // n
+    steps = int(steps) if steps else len(launches) // n
     out = {"source": {"launch_list": csv_path, "bench_line": bench_path,
                       "note": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
                               "--clock-control none (cold-cache, serialised launches; compare shares, not "
@@ -66,4 +68,4 @@ def main(csv_path, bench_path, out_path):
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:5])

@@ -123,14 +123,15 @@ def main():
     ap.add_argument("--variants", default=None, help="comma list of lines variants (default: 0..18)")
     ap.add_argument("--no-planar", action="store_true")
     ap.add_argument("--from-files", nargs="*", default=None, help="write the table from saved jsonl rows")
+    ap.add_argument("--ncu-files", nargs="*", default=None, help="tools/select_ncu.py rows (tie-breaker)")
     args = ap.parse_args()
     if args.from_files:
-        table_from_files(args.from_files)
+        table_from_files(args.from_files, args.ncu_files)
         return
     rows = []
     fh = open(args.out, "w") if args.out else None
     for d in [int(x) for x in args.dims.split(",")]:
-        pmax = 6 if d == 3 else 8
+        pmax = 7 if d == 3 else 8
         for prec in (Precision.fp32, Precision.fp64):
             for p in ([int(x) for x in args.ps.split(",")] if args.ps else range(1, pmax + 1)):
                 vs = [int(x) for x in args.variants.split(",")] if args.variants else range(19)
@@ -156,15 +157,21 @@ def main():
 # code alternate by chunk alignment) ran at 158 us in one context and 200 us in another on
 # the same box; the ring kernel is stable at 164 us.
 OVERRIDES = {(3, 6, "fp32"): 3}
+TIE = 0.0075
 
 
-def write_table(rows, points, raw="profiles/select_r01_*.jsonl"):
+def write_table(rows, points, raw="profiles/select_r01_*.jsonl", ncu=None, raw_ncu=None):
+    """Fastest median (CUDA events) wins; candidates within TIE (0.75 %, the round-robin
+    sweep's resolution) of the fastest are ranked by their ncu counters when an ncu pass is
+    given (tools/select_ncu.py): fewest shared-memory bank conflicts per shared wavefront,
+    then DRAM reads closest to the algorithmic reads, then time."""
+    ncu = ncu or {}
     best = {}
+    by_key = {}
     for r in rows:
         if r["method"] == "unfused":
             continue
         key = (r["d"], r["p"], r["precision"])
-        cur = best.get(key)
         score = r["alg_GBps"] * (1.02 if r["method"] == "lines" else 1.0)
         # grouped rings (10-15) must win clearly: their sweep medians did not carry over to the
         # bench's sequence of different kernels (d3 p1 FP64: 6626 in the sweep, 6356 in bench r01c)
@@ -174,8 +181,21 @@ def write_table(rows, points, raw="profiles/select_r01_*.jsonl"):
             if r["method"] == "lines" and r["variant"] == OVERRIDES[key]:
                 best[key] = (float("inf"), r)
             continue
-        if cur is None or score > cur[0]:
-            best[key] = (score, r)
+        by_key.setdefault(key, []).append((score, r))
+    for key, cands in by_key.items():
+        if key in best:
+            continue
+        top = max(sc for sc, _ in cands)
+        close = [(sc, r) for sc, r in cands if sc >= (1.0 - TIE) * top]
+
+        def rank(item):
+            sc, r = item
+            n = ncu.get((r["d"], r["p"], r["precision"], r["method"], r["variant"]))
+            if not n:
+                return (0.0, 0.0, -sc)
+            ratio = n.get("read_alg_ratio") or n.get("traffic_alg_ratio") or 1.0
+            return (round(n.get("conflict_per_wavefront") or 0.0, 2), round(abs(ratio - 1.0), 2), -sc)
+        best[key] = min(close, key=rank)
     path = os.path.join(ROOT, "paper_2107_14027_b200", "csrc", "hf_select_table.inc")
     with open(path, "w") as f:
         f.write("// hf_select_table.inc -- measured method selection (replaces the reference's\n"
@@ -186,23 +206,34 @@ def write_table(rows, points, raw="profiles/select_r01_*.jsonl"):
                 "// 3 (NE0,2,1) 4 (NE0/2,3,1) 5 (NE0/2,2,1) 6 (NE0,3,1) 8 (NE0/4,3,1) 9 (NE0/4,4,1)\n"
                 "// 10 (NE0/2,4,2) 11 (NE0/2,6,3) 12 (NE0/4,8,4) 13 (NE0/4,6,2) 14 (NE0,4,2) 15 (NE0/4,6,3);\n"
                 "// 16/17/18 = one chunk per CTA with (2*NE0, 2), (NE0, 2), (4*NE0, 4) (elements, lines per thread).\n"
-                "// Generated by tools/select_methods.py from on-GPU measurements (achieved\n"
-                f"// HBM GB/s, median of 20 launches at ~{points:.0e} points per configuration;\n"
-                f"// raw rows in {raw}).\n")
+                "// Generated by tools/select_methods.py from on-GPU measurements: achieved HBM GB/s\n"
+                f"// (CUDA-event median at ~{points:.0e} points per configuration; raw rows in {raw})" +
+                (f",\n// candidates within {100 * TIE:.2f} % ranked by ncu counters (bank conflicts per shared wavefront,\n"
+                 f"// then DRAM reads / algorithmic reads; tools/select_ncu.py, {raw_ncu})" if ncu else "") + ".\n")
         for (d, p, prec), (_, r) in sorted(best.items()):
             m = {"planar": 1, "lines": 2, "planar_managed": 4}[r["method"]]
+            n = ncu.get((d, p, prec, r["method"], r["variant"]))
+            extra = (f", DRAM reads {n.get('read_alg_ratio', n['traffic_alg_ratio']):.3f}x alg, "
+                     f"bank conflicts/wavefront {n['conflict_per_wavefront']}" if n else "")
             f.write(f"    {{{d}, {p}, {0 if prec == 'fp32' else 1}, {m}, {r['variant']}}},"
-                    f"  // {r['kernel']}: {r['alg_GBps']:.0f} GB/s, {r['gdofs']:.2f} GDoF/s\n")
+                    f"  // {r['kernel']}: {r['alg_GBps']:.0f} GB/s, {r['gdofs']:.2f} GDoF/s{extra}\n")
     print("wrote", path)
 
 
-def table_from_files(paths):
+def table_from_files(paths, ncu_paths=()):
     rows = []
     raw = ", ".join(p for p in paths if p.startswith("profiles/")) or "profiles/"
     for pth in paths:
         with open(pth) as fh:
             rows += [json.loads(x) for x in fh if x.strip()]
-    write_table(rows, rows[0]["points"] if rows else 1e7, raw)
+    ncu = {}
+    for pth in ncu_paths or ():
+        with open(pth) as fh:
+            for x in fh:
+                if x.strip():
+                    n = json.loads(x)
+                    ncu[(n["d"], n["p"], n["precision"], n["method"], n["variant"])] = n
+    write_table(rows, rows[0]["points"] if rows else 1e7, raw, ncu, ", ".join(ncu_paths or ()))
 
 
 if __name__ == "__main__":
