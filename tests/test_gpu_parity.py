@@ -275,3 +275,33 @@ def test_tile_mode_with_misaligned_buffers_takes_the_guarded_path(cuda):
     """An 8-byte offset (not 16) rules TMA out: same results through the guarded path."""
     U = _field(3, 3, 70, 32, False, 8)
     check_parity(3, 3, 70, 32, False, U, offset_bytes=8)
+
+
+# ---------------------------------------------------------------- stream order under programmatic dependent launch
+@pytest.mark.parametrize("d,p,fp32", [(3, 3, False), (3, 6, False), (2, 2, True), (3, 1, True)])
+def test_dependent_back_to_back_launches(cuda, d, p, fp32):
+    """The fused kernels are launched with programmatic dependent launch (hf_launch.cuh
+    launch_kernel): a launch may start while the previous kernel drains, and waits
+    (griddepcontrol.wait) before touching HBM.  Chain u -> o1 -> o2 -> o3 back to back with
+    no host synchronisation: each stage must read its predecessor's finished output."""
+    import torch
+    import paper_2107_14027_b200 as hf
+    from paper_2107_14027_b200 import Precision
+    prec = Precision.fp32 if fp32 else Precision.fp64
+    g = hf.preferred_group(hf.make_problem(d, p, 1, 1, prec, PAR))
+    n = 40 * g + 3
+    par = PhysParams(1.0 / 1600.0, 2.5, 1.0)
+    pr = hf.make_problem(d, p, n, g, prec, par)
+    U = _field(d, p, n, g, fp32, 4242)
+    dt = torch.float32 if fp32 else torch.float64
+    bufs = [torch.from_numpy(U).to(dt).cuda()] + [torch.zeros(U.size, dtype=dt, device="cuda") for _ in range(3)]
+    for k in range(3):
+        hf.fused_divergence_device(pr, bufs[k], bufs[k + 1])
+    torch.cuda.synchronize()
+    ref = U
+    for k in range(3):
+        # the device computes each stage from the previous stage's rounded output
+        ref_in = bufs[k].double().cpu().numpy()
+        ref = O.oracle_divergence(d, p, n, g, ref_in, par.nu, par.zeta, par.T)
+        err = O.field_rel_error(d, p, n, g, bufs[k + 1].double().cpu().numpy(), ref)
+        assert err <= (1e-5 if fp32 else 1e-12), f"stage {k + 1}: {err:.3e}"
