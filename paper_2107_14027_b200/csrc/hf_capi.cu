@@ -405,6 +405,14 @@ int dispatch(const hf_problem* pr, const void* u, void* out, void* ws, cudaStrea
 
 size_t word_bytes(const hf_problem* pr) { return pr->precision == HF_FP32 ? 4 : 8; }
 
+// The kernels read u while other CTAs write divf: the two fields must not share a byte.
+bool fields_overlap(const hf_problem* pr, const void* u, const void* out) {
+    const int64_t gw = int64_t(pr->group) * ipow64(pr->p + 1, pr->d) * (1 + pr->d + pr->d * pr->d);
+    const uintptr_t bytes = uintptr_t(((pr->n_elem + pr->group - 1) / pr->group) * gw) * word_bytes(pr);
+    const uintptr_t a = reinterpret_cast<uintptr_t>(u), b = reinterpret_cast<uintptr_t>(out);
+    return bytes > 0 && a < b + bytes && b < a + bytes;
+}
+
 }  // namespace
 
 // =============================================================================================
@@ -491,7 +499,8 @@ int hf_fused_divergence(const hf_problem* pr, const void* u_dev, void* divf_dev,
     if (method == HF_METHOD_UNFUSED)
         return fail(HF_EINVAL, "hf_fused_divergence: use hf_unfused_divergence for the unfused method");
     if (pr->n_elem > 0 && (!u_dev || !divf_dev)) return fail(HF_EINVAL, "hf_fused_divergence: null buffer");
-    if (u_dev == divf_dev && pr->n_elem > 0) return fail(HF_EINVAL, "hf_fused_divergence: in-place not supported");
+    if (pr->n_elem > 0 && fields_overlap(pr, u_dev, divf_dev))
+        return fail(HF_EINVAL, "hf_fused_divergence: in-place not supported (u and divf overlap)");
     return dispatch(pr, u_dev, divf_dev, nullptr, static_cast<cudaStream_t>(stream), nullptr, false);
 }
 
@@ -518,8 +527,8 @@ int hf_fused_divergence_mapped(const hf_problem* pr, const void* u_dev, const vo
     if (int rc = validate(pr)) return rc;
     if (pr->n_elem > 0 && (!u_dev || !divf_dev || !geom_dev))
         return fail(HF_EINVAL, "hf_fused_divergence_mapped: null buffer");
-    if (u_dev == divf_dev && pr->n_elem > 0)
-        return fail(HF_EINVAL, "hf_fused_divergence_mapped: in-place not supported");
+    if (pr->n_elem > 0 && fields_overlap(pr, u_dev, divf_dev))
+        return fail(HF_EINVAL, "hf_fused_divergence_mapped: in-place not supported (u and divf overlap)");
     const bool src = pr->with_source != 0;
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     int rc;
@@ -600,7 +609,8 @@ int hf_fr_divergence_faces(const hf_problem* pr, const void* u_dev, void* uf_dev
     if (int rc = validate(pr)) return rc;
     if (pr->n_elem > 0 && (!u_dev || !uf_dev || !divf_dev))
         return fail(HF_EINVAL, "hf_fr_divergence_faces: null buffer");
-    if (u_dev == divf_dev && pr->n_elem > 0) return fail(HF_EINVAL, "hf_fr_divergence_faces: in-place not supported");
+    if (pr->n_elem > 0 && fields_overlap(pr, u_dev, divf_dev))
+        return fail(HF_EINVAL, "hf_fr_divergence_faces: in-place not supported (u and divf overlap)");
     // stages 1+2+3+6 in one pass of the lines kernel (faces written beside the divergence);
     // the separate stage-1 kernel where no fused form is built (e.g. a planar selection)
 #ifdef HF_FACES_AB
@@ -633,7 +643,8 @@ int hf_fr_residual(const hf_problem* pr, const int* dims, const void* u_dev, voi
         return fail(HF_EINVAL, "hf_fr_residual: dims must be >= 1 with product n_elem");
     if (int rc = check_mesh(pr, &ms, nullptr, nullptr, "hf_fr_residual")) return rc;  // before any launch
     if (pr->n_elem > 0 && (!u_dev || !uf_dev || !divf_dev)) return fail(HF_EINVAL, "hf_fr_residual: null buffer");
-    if (u_dev == divf_dev && pr->n_elem > 0) return fail(HF_EINVAL, "hf_fr_residual: in-place not supported");
+    if (pr->n_elem > 0 && fields_overlap(pr, u_dev, divf_dev))
+        return fail(HF_EINVAL, "hf_fr_residual: in-place not supported (u and divf overlap)");
     if (int rc = hf_fr_divergence_faces(pr, u_dev, uf_dev, divf_dev, stream)) return rc;  // stages 1+2+3+6
     return hf_fr_correct(pr, &ms, uf_dev, nullptr, nullptr, divf_dev, stream);  // stages 4+5
 }

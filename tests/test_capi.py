@@ -179,3 +179,15 @@ def test_host_batch_rejects_overlapping_input_and_output():
     ctx_dummy = C.c_void_p(1)  # never dereferenced: the overlap check comes first
     assert L.hf_fused_divergence_host_batch(ctx_dummy, 1, C.byref(pr), us, outs) == HF_EINVAL
     assert "overlaps" in L.hf_last_error().decode()
+
+
+def test_overlapping_device_fields_are_rejected_before_launch():
+    """u and divf may not share a byte (the kernels read u while other CTAs write divf);
+    checked on the addresses alone, before any CUDA call."""
+    L = _lib.load()
+    pr = hf.make_problem(3, 2, 10, 4, Precision.fp64, PhysParams())
+    nbytes = hf.field_words(pr) * 8
+    base = 1 << 20
+    for off in (0, 8, nbytes - 8):
+        assert L.hf_fused_divergence(C.byref(pr), base, base + off, None) == HF_EINVAL
+        assert "overlap" in L.hf_last_error().decode()
