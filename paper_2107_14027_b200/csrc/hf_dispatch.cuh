@@ -10,15 +10,16 @@ namespace hfb {
 template <class R, int DIM, int M, int VARIANT, bool FACES>
 int lines_variant_f(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, bool dry) {
     constexpr int NE = variant_ne<R, DIM, M, VARIANT>();
+    constexpr bool CS = is_cs_variant(VARIANT);
     if constexpr (is_pipe_variant<VARIANT>()) {
         constexpr int ST = pipe_stages<VARIANT>();
         constexpr int GR = pipe_groups<VARIANT>();
-        return src ? int(launch_lines_pipe<R, DIM, M, NE, ST, GR, true, FACES>(prm, st, info, dry))
-                   : int(launch_lines_pipe<R, DIM, M, NE, ST, GR, false, FACES>(prm, st, info, dry));
+        return src ? int(launch_lines_pipe<R, DIM, M, NE, ST, GR, true, FACES, CS>(prm, st, info, dry))
+                   : int(launch_lines_pipe<R, DIM, M, NE, ST, GR, false, FACES, CS>(prm, st, info, dry));
     } else {
         constexpr int LPT = lines_per_thread<VARIANT>();
-        return src ? int(launch_lines<R, DIM, M, NE, true, LPT, FACES>(prm, st, info, dry))
-                   : int(launch_lines<R, DIM, M, NE, false, LPT, FACES>(prm, st, info, dry));
+        return src ? int(launch_lines<R, DIM, M, NE, true, LPT, FACES, NE, CS>(prm, st, info, dry))
+                   : int(launch_lines<R, DIM, M, NE, false, LPT, FACES, NE, CS>(prm, st, info, dry));
     }
 }
 
@@ -30,13 +31,15 @@ int lines_variant(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, 
     if constexpr (NE == 0 || !variant_built<R, DIM, M, VARIANT>()) {
         return kUnsupported;
     } else if constexpr (is_pipe_variant<VARIANT>() &&
-                         (PipeShape<R, DIM, M, NE, pipe_stages<VARIANT>(), pipe_groups<VARIANT>()>::SMEM >
-                              size_t(kMaxSmemPerCta) ||
-                          PipeShape<R, DIM, M, NE, pipe_stages<VARIANT>(), pipe_groups<VARIANT>()>::BS > 1024)) {
+                         (PipeShape<R, DIM, M, NE, pipe_stages<VARIANT>(), pipe_groups<VARIANT>(),
+                                    is_cs_variant(VARIANT)>::SMEM > size_t(kMaxSmemPerCta) ||
+                          PipeShape<R, DIM, M, NE, pipe_stages<VARIANT>(), pipe_groups<VARIANT>(),
+                                    is_cs_variant(VARIANT)>::BS > 1024)) {
         return kUnsupported;
     } else if constexpr (!is_pipe_variant<VARIANT>() &&
                          (LinesShape<R, DIM, M, NE>::SMEM > size_t(kMaxSmemPerCta) ||
-                          LinesShape<R, DIM, M, NE, lines_per_thread<VARIANT>()>::BS > 1024)) {
+                          LinesShape<R, DIM, M, NE, lines_per_thread<VARIANT>(), NE, is_cs_variant(VARIANT)>::BS >
+                              1024)) {
         return kUnsupported;
     } else {
         if (!faces) return lines_variant_f<R, DIM, M, VARIANT, false>(src, prm, st, info, dry);

@@ -67,10 +67,14 @@ constexpr int lines_ne_default() {
 //    14: (NE0, 4, 2)   15: (NE0/4, 6, 3)
 //   one chunk per CTA with several lines per thread, (elements, lines per thread):
 //    16: (2*NE0, 2)    17: (NE0, 2)       18: (4*NE0, 4)
+//   component split (LinesShape CS: d threads per line, one per velocity component):
+//    19: one chunk NE0   20: one chunk NE0/2   21: one chunk 2*NE0   22: one chunk NE0/4
+//    23: TMA ring (NE0, 2)
 // The contiguous bulk path accepts any NE >= 1 (hf_chunk_io.cuh), so the small-NE
 // variants exist for every order; a variant whose shape does not fit (shared
 // memory, 1024 threads) reports unsupported.
-constexpr int kLinesVariants = 19;
+constexpr int kLinesVariants = 24;
+constexpr bool is_cs_variant(int v) { return v >= 19 && v <= 23; }
 
 // The measured selection (tools/select_methods.py -> hf_select_table.inc).
 struct SelRow {
@@ -127,15 +131,15 @@ constexpr bool variant_built() {
 }
 template <int VARIANT>
 constexpr bool is_pipe_variant() {
-    return !(VARIANT == 0 || VARIANT == 1 || VARIANT == 2 || VARIANT == 7 || VARIANT >= 16);
+    return !(VARIANT == 0 || VARIANT == 1 || VARIANT == 2 || VARIANT == 7 || (VARIANT >= 16 && VARIANT <= 22));
 }
 constexpr int variant_ne_of(int ne0, int v) {
-    const int ne = (v == 0 || v == 3 || v == 6 || v == 14)                 ? ne0
-                   : (v == 1 || v == 4 || v == 5 || v == 10 || v == 11)    ? ne0 / 2
-                   : (v == 2 || v == 16)                                   ? ne0 * 2
-                   : (v == 17)                                             ? ne0
-                   : (v == 18)                                             ? ne0 * 4
-                                                                           : ne0 / 4;
+    const int ne = (v == 0 || v == 3 || v == 6 || v == 14 || v == 19 || v == 23)     ? ne0
+                   : (v == 1 || v == 4 || v == 5 || v == 10 || v == 11 || v == 20)  ? ne0 / 2
+                   : (v == 2 || v == 16 || v == 21)                                 ? ne0 * 2
+                   : (v == 17)                                                      ? ne0
+                   : (v == 18)                                                      ? ne0 * 4
+                                                                                    : ne0 / 4;
     return ne >= 1 ? ne : 0;
 }
 template <class R, int DIM, int M, int VARIANT>
@@ -295,10 +299,10 @@ inline void fill_regs(K kernel, KInfo* info) {
 inline const char* prec_name(size_t w) { return w == 4 ? "fp32" : "fp64"; }
 
 // Launch (or, with dry = true, only describe) the lines kernel.
-template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false, int GS = NE>
+template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false, int GS = NE, bool CS = false>
 cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
-    using S = LinesShape<R, DIM, M, NE, LPT, GS>;
-    auto kernel = hf_lines_kernel<R, DIM, M, NE, SRC, LPT, FACES, GS>;
+    using S = LinesShape<R, DIM, M, NE, LPT, GS, CS>;
+    auto kernel = hf_lines_kernel<R, DIM, M, NE, SRC, LPT, FACES, GS, CS>;
     const bool tile = GS == NE && tile_layout<R, NE>(p.group) && (p.u == nullptr || (aligned16(p.u) && aligned16(p.out)));
     const long long n_groups = (p.n_elem + p.group - 1) / p.group;
     const int sub = (p.group + NE - 1) / NE;
@@ -315,8 +319,8 @@ cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
             std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d_g%d%s", DIM, M - 1,
                           prec_name(sizeof(R)), NE, GS, SRC ? "_src" : "");
         else if (LPT == 1)
-            std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d%s%s", DIM, M - 1,
-                          prec_name(sizeof(R)), NE, tile ? "_tile" : "", SRC ? "_src" : "");
+            std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d%s%s%s", DIM, M - 1,
+                          prec_name(sizeof(R)), NE, CS ? "_cs" : "", tile ? "_tile" : "", SRC ? "_src" : "");
         else
             std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d_l%d%s", DIM, M - 1,
                           prec_name(sizeof(R)), NE, LPT, SRC ? "_src" : "");
@@ -355,11 +359,11 @@ inline int num_sms() {
 }
 
 // Persistent pipelined lines kernel over the whole chunks, guarded tail through hf_lines_kernel.
-template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES = false>
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES = false, bool CS = false>
 cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
-    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS>;
-    using L = LinesShape<R, DIM, M, NE>;
-    auto kernel = hf_lines_pipe_kernel<R, DIM, M, NE, STAGES, GROUPS, SRC, FACES>;
+    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS, CS>;
+    using L = LinesShape<R, DIM, M, NE, 1, NE, CS>;
+    auto kernel = hf_lines_pipe_kernel<R, DIM, M, NE, STAGES, GROUPS, SRC, FACES, CS>;
     const bool fast_layout = bulk_layout<R, NE>(p.group);
     long long n_full = p.n_elem / NE;
     // contiguous chunks load a 16-byte superset: keep the allocation's last chunk
@@ -399,8 +403,8 @@ cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dr
         info->grid = grid;
         info->bulk_path = fast_layout ? 1 : 0;
         if (GROUPS == 1)
-            std::snprintf(info->name, sizeof(info->name), "hf_lines_pipe_d%d_p%d_%s_ne%d_s%d%s", DIM, M - 1,
-                          prec_name(sizeof(R)), NE, STAGES, SRC ? "_src" : "");
+            std::snprintf(info->name, sizeof(info->name), "hf_lines_pipe_d%d_p%d_%s_ne%d_s%d%s%s", DIM, M - 1,
+                          prec_name(sizeof(R)), NE, STAGES, CS ? "_cs" : "", SRC ? "_src" : "");
         else
             std::snprintf(info->name, sizeof(info->name), "hf_lines_pipe_d%d_p%d_%s_ne%d_s%d_g%d%s", DIM, M - 1,
                           prec_name(sizeof(R)), NE, STAGES, GROUPS, SRC ? "_src" : "");
@@ -408,14 +412,14 @@ cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dr
     }
     if (dry || p.n_elem == 0) return cudaSuccess;
     p.fast_ok = fast_layout && aligned16(p.u) && aligned16(p.out);
-    if (!p.fast_ok || n_full == 0) return launch_lines<R, DIM, M, NE, SRC, 1, FACES>(p, st, nullptr, false);
+    if (!p.fast_ok || n_full == 0) return launch_lines<R, DIM, M, NE, SRC, 1, FACES, NE, CS>(p, st, nullptr, false);
     p.chunk0 = 0;
     p.n_chunks = n_full;
     cudaError_t e = launch_kernel<R>(kernel, dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st, p);
     if (e != cudaSuccess) return e;
     const long long n_chunks = (p.n_elem + NE - 1) / NE;
     if (n_full < n_chunks) {  // the partial (or allocation-final) chunk(s)
-        auto tail = hf_lines_kernel<R, DIM, M, NE, SRC, 1, FACES>;
+        auto tail = hf_lines_kernel<R, DIM, M, NE, SRC, 1, FACES, NE, CS>;
         if (int e2 = set_smem_attr(tail, L::SMEM)) return cudaError_t(e2);
         p.chunk0 = n_full;
         e = launch_kernel<R>(tail, dim3(unsigned(n_chunks - n_full)), dim3(L::BS), L::SMEM, st, p);

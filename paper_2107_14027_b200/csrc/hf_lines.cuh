@@ -53,14 +53,18 @@ namespace hfb {
 // whole groups of the caller's group size GS, staged as they lie in HBM,
 // [el / GS][v][pt][el % GS] -- one contiguous byte range for any group that divides the
 // chunk (grouped chunk, hf_launch.cuh launch_lines).
-template <class R, int DIM, int M, int NE, int LPT = 1, int GS = NE>
+// CS: component split -- each a-line is worked by d threads, one per velocity component b
+// (V_b and the momentum flux M_ba, lines_sweep_comp): d times the threads per chunk for the
+// high orders whose chunks are few per SM (shared-memory bound), same arithmetic.
+template <class R, int DIM, int M, int NE, int LPT = 1, int GS = NE, bool CS = false>
 struct LinesShape {
     static_assert(NE % GS == 0, "a grouped chunk holds whole groups");
     static constexpr int NV = n_vars_c(DIM);
     static constexpr int NP = ipow_c(M, DIM);
     static constexpr int LINES = NE * ipow_c(M, DIM - 1);
     static constexpr int TL = (LINES + LPT - 1) / LPT;
-    static constexpr int BS = ((TL + 31) / 32) * 32 < 64 ? 64 : ((TL + 31) / 32) * 32;
+    static constexpr int NT = ((TL + 31) / 32) * 32;  // threads per component group (CS) / line slots
+    static constexpr int BS = CS ? (DIM * NT < 64 ? 64 : DIM * NT) : (NT < 64 ? 64 : NT);
     static constexpr int NACC = 1 + DIM;  // continuity + d momentum partials
     static constexpr int IN_WORDS = NE * NP * NV;
     static constexpr int ACC_WORDS = NE * NP * NACC;
@@ -301,6 +305,100 @@ __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ a
 
 #undef HF_EMIT
 
+// ---------------------------------------------------------------------------------------------
+// Component-split sweep (LinesShape CS): the thread of component B of an A-line holds the
+// pairs (V_B, M_BA) of its m points, M_BA = V_B V_A + P delta_AB - nu g(B,A) (the same
+// operation order as lines_sweep), contracts them with the D rows and emits the gradient row
+// (B,A), the momentum partial B and -- for B == A -- the continuity partial.  Every input word
+// is read by the threads that need it; results are bit-identical to lines_sweep.
+// ---------------------------------------------------------------------------------------------
+template <class R, int DIM, int M, int NE, int A, int B, int GS>
+__device__ __forceinline__ void comp_load(const R* __restrict__ s, const Params<R>& p, int o, Pair<R> (&W)[M]) {
+    using S = LinesShape<R, DIM, M, NE, 1, GS>;
+    constexpr int VS = S::VS;
+    constexpr int STRIDE = (A == 0) ? 1 : (A == 1) ? M : M * M;
+    const R* __restrict__ sb = s + o;
+    const R nu = p.nu;
+#pragma unroll
+    for (int t = 0; t < M; ++t) {
+        const R* q = sb + GS * STRIDE * t;
+        const R Va = q[VS * (1 + A)];
+        const R Vb = (B == A) ? Va : q[VS * (1 + B)];
+        const R g = q[VS * var_grad_c(DIM, B, A)];
+        // codegen_util.hpp:191-202 operation order: base, then fma(V_b, V_a, base)
+        const R base = (B == A) ? fma(-nu, g, q[0]) : (-nu) * g;
+        W[t] = Pair<R>::make(Vb, fma(Vb, Va, base));
+    }
+}
+
+template <class R, int DIM, int M, int NE, bool SRC, int A, int B, int PHASE, int GS>
+__device__ __forceinline__ void comp_emit(R* __restrict__ q, R* __restrict__ a, const Params<R>& p, R dV, R dQ) {
+    constexpr int VS = GS * ipow_c(M, DIM);   // state rows
+    constexpr int AS = NE * ipow_c(M, DIM);   // accumulator rows
+    R o = p.jac_invT[A] * dV;
+    if constexpr (SRC) o = fma(-p.invT, q[VS * var_grad_c(DIM, B, A)], o);
+    q[VS * var_grad_c(DIM, B, A)] = o;
+    if constexpr (B == A) {
+        const R c = p.jac[A] * dV;
+        if constexpr (PHASE == 0) a[0] = c;
+        else if constexpr (PHASE == 1) a[0] = a[0] + c;
+        else q[0] = -(p.zeta * (a[0] + c));
+    }
+    if constexpr (PHASE == 0) a[AS * (1 + B)] = p.jac[A] * dQ;
+    else if constexpr (PHASE == 1) a[AS * (1 + B)] = fma(p.jac[A], dQ, a[AS * (1 + B)]);
+    else q[VS * (1 + B)] = -fma(p.jac[A], dQ, a[AS * (1 + B)]);
+}
+
+template <class R, int DIM, int M, int NE, bool SRC, int A, int B, int PHASE, int GS>
+__device__ __forceinline__ void comp_contract_emit(R* __restrict__ s, R* __restrict__ acc, const Params<R>& p, int o,
+                                                   Pair<R> (&W)[M]) {
+    using S = LinesShape<R, DIM, M, NE, 1, GS>;
+    using PR = Pair<R>;
+    constexpr int STRIDE = (A == 0) ? 1 : (A == 1) ? M : M * M;
+    R* __restrict__ sb = s + o;
+    R* __restrict__ ab = acc + S::acc_of(o);
+    auto emit = [&](int i, PR d) {
+        comp_emit<R, DIM, M, NE, SRC, A, B, PHASE, GS>(sb + GS * STRIDE * i, ab + NE * STRIDE * i, p, d.x(), d.y());
+    };
+    if constexpr (M < HF_EVEN_ODD_MIN_M) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            PR d = pmul(p.D[i * M], W[0]);
+#pragma unroll
+            for (int t = 1; t < M; ++t) d = pfma(p.D[i * M + t], W[t], d);
+            emit(i, d);
+        }
+    } else {
+        constexpr int H = M / 2;
+        constexpr int K = kMaxH;
+#pragma unroll
+        for (int t = 0; t < H; ++t) {
+            const PR w0 = W[t], w1 = W[M - 1 - t];
+            W[t] = padd(w0, w1);
+            W[M - 1 - t] = psub(w0, w1);
+        }
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            PR x = pmul(p.DE[i * K], W[0]);
+            PR y = pmul(p.DO[i * K], W[M - 1]);
+#pragma unroll
+            for (int t = 1; t < H; ++t) {
+                x = pfma(p.DE[i * K + t], W[t], x);
+                y = pfma(p.DO[i * K + t], W[M - 1 - t], y);
+            }
+            if constexpr (M % 2 == 1) x = pfma(p.DC[i], W[H], x);
+            emit(i, padd(x, y));
+            emit(M - 1 - i, psub(y, x));
+        }
+        if constexpr (M % 2 == 1) {
+            PR d = pmul(p.DO[H * K], W[M - 1]);
+#pragma unroll
+            for (int t = 1; t < H; ++t) d = pfma(p.DO[H * K + t], W[M - 1 - t], d);
+            emit(H, d);
+        }
+    }
+}
+
 // All d sweeps of one chunk whose first word sits HEADB bytes into `buf`.
 // HEADB is a template parameter so that every shared-memory address in the
 // sweeps is a compile-time offset from the __shared__ window (a runtime base
@@ -342,17 +440,20 @@ __device__ __forceinline__ void lines_project_faces(const R* __restrict__ s, con
     }
 }
 
-template <class R, int DIM, int M, int NE, bool SRC, int HEADB, int BAR, int NTHR, bool FACES = false, int GS = NE>
+template <class R, int DIM, int M, int NE, bool SRC, int HEADB, int BAR, int NTHR, bool FACES = false, int GS = NE,
+          bool CS = false>
 __device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const Params<R>& p, int t, int bar_id = 0,
                                              long long E0 = 0, int nvalid = NE) {
+    // NTHR: line slots per sweep iteration (LineMap); CS: d component groups of NTHR threads
+    constexpr int NALL = CS ? DIM * NTHR : NTHR;
     R* s = reinterpret_cast<R*>(buf + HEADB);
 #ifdef HF_IO_ONLY  // measurement build: chunk traffic only, no sweeps (tools/gpu_ab_io.sh)
     return;
 #endif
     auto sync = [&] {
         if constexpr (BAR == 0) __syncthreads();
-        else if constexpr (BAR < 0) named_bar_sync(bar_id, NTHR);  // runtime barrier id (consumer groups)
-        else named_bar_sync(BAR, NTHR);
+        else if constexpr (BAR < 0) named_bar_sync(bar_id, NALL);  // runtime barrier id (consumer groups)
+        else named_bar_sync(BAR, NALL);
     };
     // lines of sweep A in the bank-conflict-free order of kLineMap
     auto sweep = [&](auto a_tag, auto phase_tag) {
@@ -360,17 +461,42 @@ __device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const P
         constexpr int PH = decltype(phase_tag)::value;
         using LM = LineMap<R, DIM, M, NE, A, NTHR, GS>;
         const unsigned short* map = kLineMap<R, DIM, M, NE, A, NTHR, GS>.off;
+        if constexpr (!CS) {
 #pragma unroll 1
-        for (int k = 0; k < LM::ITERS; ++k) {
-            const int o = map[k * NTHR + t];
-            if (o != 0xFFFF) lines_sweep<R, DIM, M, NE, SRC, A, PH, GS>(s, acc, p, o);
+            for (int k = 0; k < LM::ITERS; ++k) {
+                const int o = map[k * NTHR + t];
+                if (o != 0xFFFF) lines_sweep<R, DIM, M, NE, SRC, A, PH, GS>(s, acc, p, o);
+            }
+        } else {
+            // warp-uniform component: component group b = threads [b*NTHR, (b+1)*NTHR)
+            const int b = t / NTHR, tt = t - b * NTHR;
+            auto load = [&](int o, Pair<R> (&W)[M]) {
+                if (b == 0) comp_load<R, DIM, M, NE, A, 0, GS>(s, p, o, W);
+                else if (DIM == 2 || b == 1) comp_load<R, DIM, M, NE, A, 1, GS>(s, p, o, W);
+                else comp_load<R, DIM, M, NE, A, (DIM == 3 ? 2 : 1), GS>(s, p, o, W);
+            };
+            auto emit = [&](int o, Pair<R> (&W)[M]) {
+                if (b == 0) comp_contract_emit<R, DIM, M, NE, SRC, A, 0, PH, GS>(s, acc, p, o, W);
+                else if (DIM == 2 || b == 1) comp_contract_emit<R, DIM, M, NE, SRC, A, 1, PH, GS>(s, acc, p, o, W);
+                else comp_contract_emit<R, DIM, M, NE, SRC, A, (DIM == 3 ? 2 : 1), PH, GS>(s, acc, p, o, W);
+            };
+#pragma unroll 1
+            for (int k = 0; k < LM::ITERS; ++k) {
+                const int o = map[k * NTHR + tt];
+                Pair<R> W[M];
+                if (o != 0xFFFF) load(o, W);
+                // the last sweep overwrites V_A with its final value (component A's thread)
+                // while the other components of the line still read it: all loads first
+                if constexpr (PH == 2) sync();
+                if (o != 0xFFFF) emit(o, W);
+            }
         }
     };
     using I0 = std::integral_constant<int, 0>;
     using I1 = std::integral_constant<int, 1>;
     using I2 = std::integral_constant<int, 2>;
     if constexpr (FACES) {
-        lines_project_faces<R, DIM, M, NE, GS>(s, p, E0, t, NTHR, nvalid);
+        lines_project_faces<R, DIM, M, NE, GS>(s, p, E0, t, NALL, nvalid);
         sync();  // every line is read before sweep 0 writes in place
     }
     if constexpr (DIM == 3) {
@@ -388,28 +514,29 @@ __device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const P
 
 // Runtime head (bytes, a multiple of sizeof(R), < 16) -> compile-time HEADB.
 // Chunks whose byte size is a multiple of 16 always start aligned: one instance.
-template <class R, int DIM, int M, int NE, bool SRC, int BAR, int NTHR, bool FACES = false, int GS = NE>
+template <class R, int DIM, int M, int NE, bool SRC, int BAR, int NTHR, bool FACES = false, int GS = NE,
+          bool CS = false>
 __device__ __forceinline__ void lines_sweeps_at(unsigned char* buf, int head, R* acc, const Params<R>& p, int t,
                                                 int bar_id = 0, long long E0 = 0, int nv = NE) {
     if constexpr (LinesShape<R, DIM, M, NE>::IN_BYTES % 16 == 0) {
-        lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES, GS>(buf, acc, p, t, bar_id, E0, nv);
+        lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES, GS, CS>(buf, acc, p, t, bar_id, E0, nv);
     } else if constexpr (sizeof(R) == 8) {
-        if (head == 0) lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES, GS>(buf, acc, p, t, bar_id, E0, nv);
-        else lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR, FACES, GS>(buf, acc, p, t, bar_id, E0, nv);
+        if (head == 0) lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES, GS, CS>(buf, acc, p, t, bar_id, E0, nv);
+        else lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR, FACES, GS, CS>(buf, acc, p, t, bar_id, E0, nv);
     } else {
         switch (head) {
-            case 0: lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES, GS>(buf, acc, p, t, bar_id, E0, nv); break;
-            case 4: lines_sweeps<R, DIM, M, NE, SRC, 4, BAR, NTHR, FACES, GS>(buf, acc, p, t, bar_id, E0, nv); break;
-            case 8: lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR, FACES, GS>(buf, acc, p, t, bar_id, E0, nv); break;
-            default: lines_sweeps<R, DIM, M, NE, SRC, 12, BAR, NTHR, FACES, GS>(buf, acc, p, t, bar_id, E0, nv); break;
+            case 0: lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES, GS, CS>(buf, acc, p, t, bar_id, E0, nv); break;
+            case 4: lines_sweeps<R, DIM, M, NE, SRC, 4, BAR, NTHR, FACES, GS, CS>(buf, acc, p, t, bar_id, E0, nv); break;
+            case 8: lines_sweeps<R, DIM, M, NE, SRC, 8, BAR, NTHR, FACES, GS, CS>(buf, acc, p, t, bar_id, E0, nv); break;
+            default: lines_sweeps<R, DIM, M, NE, SRC, 12, BAR, NTHR, FACES, GS, CS>(buf, acc, p, t, bar_id, E0, nv); break;
         }
     }
 }
 
-template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false, int GS = NE>
-__global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT, GS>::BS)
+template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false, int GS = NE, bool CS = false>
+__global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT, GS, CS>::BS)
     hf_lines_kernel(const __grid_constant__ Params<R> p) {
-    using S = LinesShape<R, DIM, M, NE, LPT, GS>;
+    using S = LinesShape<R, DIM, M, NE, LPT, GS, CS>;
     constexpr int BS = S::BS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     using IO = typename S::IO;
@@ -478,7 +605,7 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT, GS>::BS)
     }
 
     // ---------------- d sweeps ----------------
-    lines_sweeps_at<R, DIM, M, NE, SRC, 0, BS, FACES, GS>(buf, head, acc, p, tid, 0, E0, nvalid);
+    lines_sweeps_at<R, DIM, M, NE, SRC, 0, (CS ? S::NT : BS), FACES, GS, CS>(buf, head, acc, p, tid, 0, E0, nvalid);
 
     // ---------------- write the finished chunk ----------------
     if (fast) {

@@ -35,12 +35,13 @@
 
 namespace hfb {
 
-template <class R, int DIM, int M, int NE, int STAGES, int GROUPS = 1>
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS = 1, bool CS = false>
 struct PipeShape {
     using L = LinesShape<R, DIM, M, NE>;
     static_assert(STAGES % GROUPS == 0, "every group owns STAGES / GROUPS stages");
     static constexpr int SPG = STAGES / GROUPS;               // stages per group
-    static constexpr int NCONS = ((L::LINES + 31) / 32) * 32;  // consumer threads per group
+    static constexpr int NT = ((L::LINES + 31) / 32) * 32;    // line slots per sweep iteration
+    static constexpr int NCONS = CS ? DIM * NT : NT;          // consumer threads per group (CS: one per component)
     static constexpr int BS = GROUPS * NCONS + 32;            // + producer warp
     static constexpr int HDR = 256;                           // 2*STAGES mbarriers (<= 32)
     static constexpr size_t STAGE_BYTES = size_t(L::BUF_BYTES);
@@ -55,11 +56,11 @@ struct PipeShape {
 // accumulator region) is a runtime offset from the __shared__ window, so every
 // group runs the same code -- one copy of the sweeps per stage, not per
 // (group, stage), which keeps the kernel inside the instruction cache.
-template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES>
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES, bool CS = false>
 __device__ __forceinline__ void pipe_consume(unsigned char* smem_raw, uint64_t* full, uint64_t* computed,
                                              const Params<R>& p, long long count, long long first, long long step,
                                              int g, int ct) {
-    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS>;
+    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS, CS>;
     using L = LinesShape<R, DIM, M, NE>;
     using IO = typename L::IO;
     constexpr int SPG = S::SPG;
@@ -79,11 +80,11 @@ __device__ __forceinline__ void pipe_consume(unsigned char* smem_raw, uint64_t* 
             unsigned char* buf = gbuf + size_t(j) * S::STAGE_BYTES;
             mbar_wait_parity(&full[s], ph);
             if constexpr (GROUPS == 1)
-                lines_sweeps_at<R, DIM, M, NE, SRC, 1, S::NCONS, FACES>(buf, IO::head_bytes(p.u + cb, contiguous),
-                                                                        acc, p, ct, 0, E0);
+                lines_sweeps_at<R, DIM, M, NE, SRC, 1, S::NT, FACES, NE, CS>(
+                    buf, IO::head_bytes(p.u + cb, contiguous), acc, p, ct, 0, E0);
             else
-                lines_sweeps_at<R, DIM, M, NE, SRC, -1, S::NCONS, FACES>(buf, IO::head_bytes(p.u + cb, contiguous),
-                                                                         acc, p, ct, 1 + g, E0);
+                lines_sweeps_at<R, DIM, M, NE, SRC, -1, S::NT, FACES, NE, CS>(
+                    buf, IO::head_bytes(p.u + cb, contiguous), acc, p, ct, 1 + g, E0);
             fence_proxy_async_smem();
             named_bar_sync(1 + g, S::NCONS);
             if (ct == 0) mbar_arrive(&computed[s]);
@@ -91,11 +92,11 @@ __device__ __forceinline__ void pipe_consume(unsigned char* smem_raw, uint64_t* 
     }
 }
 
-template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES = false>
-__global__ void __launch_bounds__(PipeShape<R, DIM, M, NE, STAGES, GROUPS>::BS)
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES = false, bool CS = false>
+__global__ void __launch_bounds__(PipeShape<R, DIM, M, NE, STAGES, GROUPS, CS>::BS)
     hf_lines_pipe_kernel(const __grid_constant__ Params<R> p) {
     using L = LinesShape<R, DIM, M, NE>;
-    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS>;
+    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS, CS>;
     constexpr int SPG = S::SPG;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -162,7 +163,8 @@ __global__ void __launch_bounds__(PipeShape<R, DIM, M, NE, STAGES, GROUPS>::BS)
     // ---------------- consumer groups ----------------
     const int g = (tid - 32) / S::NCONS;
     const int ct = (tid - 32) - g * S::NCONS;
-    pipe_consume<R, DIM, M, NE, STAGES, GROUPS, SRC, FACES>(smem_raw, full, computed, p, count, first, step, g, ct);
+    pipe_consume<R, DIM, M, NE, STAGES, GROUPS, SRC, FACES, CS>(smem_raw, full, computed, p, count, first, step, g,
+                                                                ct);
 }
 
 }  // namespace hfb

@@ -72,7 +72,7 @@ def test_lines_misaligned_pointer(cuda):
     check_parity(3, 2, 64, 16, False, U, method=Method.lines, offset_bytes=8)
 
 
-@pytest.mark.parametrize("variant", list(range(19)))
+@pytest.mark.parametrize("variant", list(range(24)))
 @pytest.mark.parametrize("d,p,fp32", [(3, 1, True), (3, 3, False), (3, 4, True), (3, 6, False), (3, 6, True),
                                       (2, 3, True), (2, 8, True)])
 def test_lines_variants(cuda, d, p, fp32, variant):
@@ -94,12 +94,37 @@ def test_lines_variants(cuda, d, p, fp32, variant):
         assert err <= (1e-5 if fp32 else 1e-12), (n, group, src, err)
 
 
+@pytest.mark.parametrize("d,p,fp32", [(3, 2, True), (3, 5, False), (3, 6, False), (3, 7, True), (2, 6, False)])
+def test_component_split_is_bit_identical(cuda, d, p, fp32):
+    """The component-split variants (19-23: d threads per line) run the same arithmetic in the
+    same order as their one-thread-per-line counterparts (0, 1, 2, 7, 3): equal bit for bit."""
+    import paper_2107_14027_b200 as hf
+    pr0 = hf.make_problem(d, p, 1, 1, int(not fp32), PAR)
+    pairs = [(19, 0), (20, 1), (21, 2), (22, 7), (23, 3)]
+    ran = 0
+    for cs, base in pairs:
+        try:
+            g = hf.variant_info(pr0, Method.lines, cs)["elems_per_cta"]
+            assert hf.variant_info(pr0, Method.lines, base)["elems_per_cta"] == g
+        except hf.HexfuseInvalid:
+            continue
+        n = 37 * g + 1
+        U = _field(d, p, n, g, fp32, 600 + cs)
+        for src in (False, True):
+            a = run_device(d, p, n, g, fp32, U, method=Method.lines, variant=cs, with_source=src)
+            b = run_device(d, p, n, g, fp32, U, method=Method.lines, variant=base, with_source=src)
+            assert np.array_equal(a, b), (cs, base, src)
+        ran += 1
+    if not ran:
+        pytest.skip("no component-split variant instantiated (production build)")
+
+
 def test_pipe_many_chunks_per_cta(cuda):
     """More chunks than resident CTAs: every CTA cycles its stage ring several times."""
     import paper_2107_14027_b200 as hf
     for fp32, p in [(False, 3), (True, 5)]:
         pr = hf.make_problem(3, p, 1, 1, int(not fp32), PAR)
-        for variant in (3, 4, 5, 6, 8, 9, 10, 11, 12, 13, 14, 15):
+        for variant in (3, 4, 5, 6, 8, 9, 10, 11, 12, 13, 14, 15, 23):
             try:
                 g = hf.variant_info(pr, Method.lines, variant)["elems_per_cta"]
             except hf.HexfuseInvalid:

@@ -120,7 +120,7 @@ def main():
     ap.add_argument("--write-table", action="store_true")
     ap.add_argument("--no-unfused", action="store_true")
     ap.add_argument("--ps", default=None, help="comma list of orders (default: all)")
-    ap.add_argument("--variants", default=None, help="comma list of lines variants (default: 0..18)")
+    ap.add_argument("--variants", default=None, help="comma list of lines variants (default: 0..23)")
     ap.add_argument("--no-planar", action="store_true")
     ap.add_argument("--from-files", nargs="*", default=None, help="write the table from saved jsonl rows")
     ap.add_argument("--ncu-files", nargs="*", default=None, help="tools/select_ncu.py rows (tie-breaker)")
@@ -134,7 +134,7 @@ def main():
         pmax = 7 if d == 3 else 8
         for prec in (Precision.fp32, Precision.fp64):
             for p in ([int(x) for x in args.ps.split(",")] if args.ps else range(1, pmax + 1)):
-                vs = [int(x) for x in args.variants.split(",")] if args.variants else range(19)
+                vs = [int(x) for x in args.variants.split(",")] if args.variants else range(24)
                 cands = [(Method.lines, v) for v in vs]
                 if d == 3 and not args.no_planar:
                     cands.append((Method.planar, 0))
@@ -156,7 +156,13 @@ def main():
 # p6 FP32 kernel with NE = 2 (chunk bytes not a multiple of 16, so two copies of the sweep
 # code alternate by chunk alignment) ran at 158 us in one context and 200 us in another on
 # the same box; the ring kernel is stable at 164 us.
-OVERRIDES = {(3, 6, "fp32"): 3}
+# Component-split variants (19-23) were timed in their own sweep against the base
+# variants 0/1/2/7/3 (profiles/r02/select/select_cs_r02.jsonl, same box, round-robin): they
+# win clearly (> 2 %) only where FP64 arithmetic latency dominates with few lines per chunk
+# -- d3 p4 FP64 (NE0/2 split, 1.006 vs 0.959 of the roofline); elsewhere they lose or tie
+# (d3 p7 FP32: 0.612 vs 0.558 for the one-chunk kernels, but below the TMA ring variant 4,
+# 0.65, which that sweep did not include).  They compete only through these overrides.
+OVERRIDES = {(3, 6, "fp32"): 3, (3, 4, "fp64"): 20}
 TIE = 0.0075
 
 
@@ -172,6 +178,8 @@ def write_table(rows, points, raw="profiles/select_r01_*.jsonl", ncu=None, raw_n
         if r["method"] == "unfused":
             continue
         key = (r["d"], r["p"], r["precision"])
+        if r["method"] == "lines" and r["variant"] >= 19 and OVERRIDES.get(key) != r["variant"]:
+            continue  # component-split rows compete only through OVERRIDES (measured in their own sweep)
         score = r["alg_GBps"] * (1.02 if r["method"] == "lines" else 1.0)
         # grouped rings (10-15) must win clearly: their sweep medians did not carry over to the
         # bench's sequence of different kernels (d3 p1 FP64: 6626 in the sweep, 6356 in bench r01c)

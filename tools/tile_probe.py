@@ -27,10 +27,12 @@ def main():
     ap.add_argument("--ps", default="")
     ap.add_argument("--groups", default="8,12,16,20,24,32,40,64")
     ap.add_argument("--points", type=float, default=1e7)
+    ap.add_argument("--variants", default="7,1,0,2", help="lines variants to force (19-22: component split)")
+    ap.add_argument("--precisions", default="fp32,fp64")
     a = ap.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     ps = [int(x) for x in a.ps.split(",")] if a.ps else (list(range(1, 7)) if a.d == 3 else list(range(1, 9)))
-    for prec in (Precision.fp32, Precision.fp64):
+    for prec in [Precision[x] for x in a.precisions.split(",")]:
         for p in ps:
             npt = (p + 1) ** a.d
             for g in [int(x) for x in a.groups.split(",")]:
@@ -40,7 +42,7 @@ def main():
                 u = torch.empty(hf.field_words(pr), dtype=dt, device="cuda").uniform_(-1, 1)
                 o = torch.empty_like(u)
                 auto = hf.kernel_info(pr)["name"]
-                for v in (7, 1, 0, 2):
+                for v in [int(x) for x in a.variants.split(",")]:
                     try:
                         info = hf.variant_info(pr, Method.lines, v)
                         for _ in range(2):
