@@ -357,6 +357,21 @@ int lines_variant_for_group(const hf_problem* pr, int variant, const hfb::Params
         }
     }
     if (best >= 0) return best;
+    // guarded path (a group that is not a 16-byte stride and no chunk size): every staged word
+    // is one cp.async copy, so the contiguous run per row (min(NE, G) words) and the resident
+    // CTAs decide -- measured 0.33-0.70 for G = 3, 5, 7, 15 (profiles/r02/groups_odd_*.jsonl)
+    double best_g = -1.0;
+    for (int v : cand) {
+        const int ne = hfb::variant_ne_of(ne0, v);
+        if (ne < 1 || !available(v)) continue;
+        const double run = std::min(1.0, double(std::min(ne, G)) * w / 64.0);
+        const double score = run * occupancy(ne);
+        if (score > best_g + 1e-9) {
+            best = v;
+            best_g = score;
+        }
+    }
+    if (best >= 0) return best;
     return hfb::is_one_chunk_variant(variant) ? variant : 0;
 }
 

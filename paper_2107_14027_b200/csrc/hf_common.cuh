@@ -135,6 +135,18 @@ __device__ __forceinline__ void bulk_s2g(void* dst_gmem, const void* src_smem, u
 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 
+// one word (4 or 8 bytes) global -> shared, async (LDGSTS)
+template <class R>
+__device__ __forceinline__ void cp_async_word(R* dst_smem, const R* src_gmem) {
+    if constexpr (sizeof(R) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 // TMA tensor copies (SASS UTMALDG / UTMASTG) of one 5-d box; `tmap` is the generic
 // address of a CUtensorMap in the __grid_constant__ parameter block.
 __device__ __forceinline__ void tma_load_5d(void* dst_smem, const CUtensorMap* tmap, int c0, int c1, int c2, int c3,

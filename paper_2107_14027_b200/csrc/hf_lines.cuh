@@ -569,6 +569,7 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT, GS, CS>::BS)
     const bool fast = p.tile ? (p.fast_ok && full) : chunk_bulk_ok<R, S::IN_WORDS>(p, gbase, full, contiguous);
     const int head = (fast && !p.tile) ? IO::head_bytes(p.u + gbase, contiguous) : 0;
     R* s = reinterpret_cast<R*>(smem_raw + S::HDR);  // guarded path (head == 0)
+    __shared__ long long ebase[NE];                   // guarded path: element word bases, -1 = absent
 
     // ---------------- stage the chunk into shared memory ----------------
     if (fast) {
@@ -589,18 +590,30 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT, GS, CS>::BS)
         }
         mbar_wait_parity(bar, 0);
     } else {
+        // guarded path (any group, alignment or partial chunk): the element's word base once per
+        // element (the 64-bit group arithmetic), then one cp.async word copy per staged word
+        // (LDGSTS: no register round trip, many in flight; consecutive threads read
+        // consecutive words of a row wherever the group allows)
+        for (int el = tid; el < NE; el += BS) {
+            const long long e = E0 + el;
+            long long b = -1;
+            if (el < nvalid && e < p.n_elem) {
+                const long long ge = e / p.group;
+                b = ge * p.group_words + (e - ge * p.group);
+            }
+            ebase[el] = b;
+        }
+        __syncthreads();
+        const long long G = p.group;
         for (int idx = tid; idx < S::IN_WORDS; idx += BS) {
             const int blk = idx / S::BLK, rem = idx - blk * S::BLK;  // staged word -> (el, row)
             const int el = blk * GS + rem % GS;
             const int row = rem / GS;
-            const long long e = E0 + el;
-            R v = R(0);
-            if (el < nvalid && e < p.n_elem) {
-                const long long ge = e / p.group;
-                v = ld_stream(p.u + ge * p.group_words + (e - ge * p.group) + static_cast<long long>(p.group) * row);
-            }
-            s[idx] = v;
+            const long long b = ebase[el];
+            if (b >= 0) cp_async_word(s + idx, p.u + b + G * row);
+            else s[idx] = R(0);
         }
+        cp_async_wait_all();
         __syncthreads();
     }
 
@@ -623,15 +636,13 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT, GS, CS>::BS)
         }
     } else {
         __syncthreads();
+        const long long G = p.group;
         for (int idx = tid; idx < S::IN_WORDS; idx += BS) {
             const int blk = idx / S::BLK, rem = idx - blk * S::BLK;
             const int el = blk * GS + rem % GS;
             const int row = rem / GS;
-            const long long e = E0 + el;
-            if (el < nvalid && e < p.n_elem) {
-                const long long ge = e / p.group;
-                p.out[ge * p.group_words + (e - ge * p.group) + static_cast<long long>(p.group) * row] = s[idx];
-            }
+            const long long b = ebase[el];
+            if (b >= 0) __stcs(p.out + b + G * row, s[idx]);
         }
     }
 }
