@@ -94,7 +94,7 @@ def test_lines_variants(cuda, d, p, fp32, variant):
         assert err <= (1e-5 if fp32 else 1e-12), (n, group, src, err)
 
 
-@pytest.mark.parametrize("d,p,fp32", [(3, 2, True), (3, 5, False), (3, 6, False), (3, 7, True), (2, 6, False)])
+@pytest.mark.parametrize("d,p,fp32", [(3, 4, False), (3, 2, True), (3, 5, False), (3, 6, False), (3, 7, True), (2, 6, False)])
 def test_component_split_is_bit_identical(cuda, d, p, fp32):
     """The component-split variants (19-23: d threads per line) run the same arithmetic in the
     same order as their one-thread-per-line counterparts (0, 1, 2, 7, 3): equal bit for bit."""
