@@ -330,3 +330,36 @@ def test_dependent_back_to_back_launches(cuda, d, p, fp32):
         ref = O.oracle_divergence(d, p, n, g, ref_in, par.nu, par.zeta, par.T)
         err = O.field_rel_error(d, p, n, g, bufs[k + 1].double().cpu().numpy(), ref)
         assert err <= (1e-5 if fp32 else 1e-12), f"stage {k + 1}: {err:.3e}"
+
+
+def test_cuda_graph_capture_and_replay(cuda):
+    """The launch path is capture-safe (no host synchronisation, no allocation; the
+    programmatic-dependent-launch attribute becomes a graph edge): launches captured into
+    a CUDA graph replay to the same bits as stream launches, for the one-chunk, the TMA-ring,
+    the component-split and the tile-mode kernels."""
+    import torch
+    import paper_2107_14027_b200 as hf
+    from paper_2107_14027_b200 import Precision
+    cases = []
+    for d, p, prec, g in [(3, 3, Precision.fp64, None), (3, 6, Precision.fp64, None), (3, 4, Precision.fp64, None),
+                          (3, 2, Precision.fp32, 24), (2, 5, Precision.fp32, None)]:
+        g = g or hf.preferred_group(hf.make_problem(d, p, 1, 1, prec, PAR))
+        n = 20 * g + 1
+        pr = hf.make_problem(d, p, n, g, prec, PAR, with_source=True)
+        dt = torch.float32 if prec == Precision.fp32 else torch.float64
+        u = torch.empty(hf.field_words(pr), dtype=dt, device="cuda").uniform_(-1, 1)
+        cases.append((pr, u, torch.zeros_like(u), torch.zeros_like(u)))
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for pr, u, o, _ in cases:
+            hf.fused_divergence_device(pr, u, o, st)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=st):
+        for pr, u, _, og in cases:
+            hf.fused_divergence_device(pr, u, og, st)
+    with torch.cuda.stream(st):
+        graph.replay()
+    torch.cuda.synchronize()
+    for pr, u, o, og in cases:
+        assert torch.equal(o, og), hf.kernel_info(pr)["name"]
