@@ -355,10 +355,15 @@ def run_ours(args, R: Ranks):
         step()
     torch.cuda.synchronize()
 
-    # ---- per-launch durations for the roofline: K steps with a CUDA-event pair around every
-    # launch (the events keep consecutive launches apart, so this is the conservative figure)
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in cases]
-          for _ in range(args.steps)]
+    # ---- per-launch durations for the roofline, just before the timed region: every case K
+    # times, in blocks of ROOF_BLOCK launches back to back between one CUDA-event pair on the
+    # launching stream (inside a block consecutive launches overlap launch and ramp-up as in
+    # the timed region), the blocks round-robin over the cases so that every case sees the
+    # same mix of clock and thermal state
+    ROOF_BLOCK = 5
+    blocks = [(c_i, min(ROOF_BLOCK, args.steps - k0)) for k0 in range(0, args.steps, ROOF_BLOCK)
+              for c_i in range(len(cases))]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in blocks]
     # ---- timed region (value): K steps (a step = every case once) launched back to back with
     # one event pair around all of them -- consecutive launches overlap launch and ramp-up with
     # the previous kernel's tail (programmatic dependent launch, hf_launch.cuh launch_kernel)
@@ -366,11 +371,12 @@ def run_ours(args, R: Ranks):
     with ClockSampler(local_rank) as clk:
         R.barrier()
         torch.cuda.synchronize()
-        for k in range(args.steps):
-            for i, c in enumerate(cases):
-                ev[k][i][0].record(st)
+        for (c_i, reps), (a, b) in zip(blocks, ev):
+            c = cases[c_i]
+            a.record(st)
+            for _ in range(reps):
                 hf.fused_divergence_device(c["pr"], c["u"], c["o"], st)
-                ev[k][i][1].record(st)
+            b.record(st)
         torch.cuda.synchronize()
         R.barrier()
         torch.cuda.synchronize()
@@ -381,8 +387,9 @@ def run_ours(args, R: Ranks):
         torch.cuda.synchronize()
         R.barrier()
     elapsed = R.max(t0.elapsed_time(t1) * 1e-3)
-    per_case = [sum(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps)) * 1e-3 / args.steps
-                for i in range(len(cases))]
+    per_case = [0.0] * len(cases)
+    for (c_i, reps), (a, b) in zip(blocks, ev):
+        per_case[c_i] += a.elapsed_time(b) * 1e-3 / args.steps
     points_rank = sum(c["points"] for c in cases)
     points_all = R.sum(points_rank)
     value = points_all * args.steps / elapsed / 1e9
@@ -527,7 +534,8 @@ def run_ours(args, R: Ranks):
             "roofline": roofline, "cases": case_rows, "e2e": e2e, "parity": parity, "cpu_baseline": cpu,
             "gpu_launches": args.steps * launches, "gpu_launches_roofline_pass": args.steps * launches,
             "timing": "value: K steps back to back between one CUDA-event pair (max over ranks); roofline and "
-                      "cases: a K-step pass just before it with an event pair around every launch",
+                      "cases: just before it, each case K times in blocks of 5 back-to-back launches between "
+                      "an event pair, the blocks round-robin over the cases",
             "clocks": clk.summary(),
         }
         if unfused:
