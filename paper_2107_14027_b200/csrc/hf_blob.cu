@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <string>
 #include <vector>
@@ -66,7 +67,7 @@ bool parse_sidecar(const std::string& text, std::map<std::string, std::string>& 
             const size_t j0 = i;
             if (i < text.size() && text[i] == '-') ++i;
             while (i < text.size() && std::isdigit(static_cast<unsigned char>(text[i]))) ++i;
-            if (i == j0 || (i == j0 + 1 && text[j0] == '-')) return false;
+            if (i == j0 || (i == j0 + 1 && text[j0] == '-') || i - j0 > 18) return false;  // fits int64
             num[key] = std::stoll(text.substr(j0, i - j0));
         }
         ws();
@@ -105,7 +106,13 @@ int hf_blob_info(const char* path, hf_problem* shape_out) {
     std::fclose(f);
     std::map<std::string, std::string> str;
     std::map<std::string, int64_t> num;
-    if (!parse_sidecar(text, str, num)) return fail(HF_ERUNTIME, "import_blob: malformed sidecar " + side);
+    bool parsed = false;
+    try {  // nothing may escape the C ABI
+        parsed = parse_sidecar(text, str, num);
+    } catch (const std::exception&) {
+        parsed = false;
+    }
+    if (!parsed) return fail(HF_ERUNTIME, "import_blob: malformed sidecar " + side);
     for (const char* k : {"d", "p", "n_elem", "group", "words"})
         if (!num.count(k)) return fail(HF_ERUNTIME, std::string("import_blob: sidecar lacks \"") + k + "\"");
     if (!str.count("precision")) return fail(HF_ERUNTIME, "import_blob: sidecar lacks \"precision\"");

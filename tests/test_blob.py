@@ -76,4 +76,7 @@ def test_blob_errors_map_to_the_reference_exception_classes(tmp_path):
     open(path + ".json", "w").write("{ not json")
     with pytest.raises(HexfuseError, match="malformed"):
         hf.import_blob(path)
+    open(path + ".json", "w").write(side.replace('"words": ', '"words": 99999999999999999999999'))
+    with pytest.raises(HexfuseError, match="malformed"):  # no exception escapes the C ABI
+        hf.import_blob(path)
     assert not os.path.exists(str(tmp_path / "never.bin.json"))
