@@ -660,6 +660,40 @@ int hf_fr_residual(const hf_problem* pr, const int* dims, const void* u_dev, voi
     if (pr->n_elem > 0 && (!u_dev || !uf_dev || !divf_dev)) return fail(HF_EINVAL, "hf_fr_residual: null buffer");
     if (pr->n_elem > 0 && fields_overlap(pr, u_dev, divf_dev))
         return fail(HF_EINVAL, "hf_fr_residual: in-place not supported (u and divf overlap)");
+    // Where measured faster (hfb::fr_residual_fused): stage 1 (the faces), then ONE lines kernel
+    // for stages 2+3+6 and 4+5 -- the residual leaves shared memory once (hf_lines_fr_kernel).
+    // Elsewhere the pair: stages 1+2+3+6 in the lines kernel, then the correction kernel.
+    static const int forced = [] {  // HF_FR_FUSED=0 / 1 forces the pair / the one-pass form (A/B runs)
+        const char* e = std::getenv("HF_FR_FUSED");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    bool fused = forced == 1;
+    if (forced < 0) {
+        const auto prm0 = make_params<float>(pr, nullptr, nullptr, nullptr);
+        const auto prm1 = make_params<double>(pr, nullptr, nullptr, nullptr);
+        fused = (pr->precision == HF_FP32 ? hfb::fr_f32(5, pr->d, pr->p, prm0, hfb::FrParams<float>{}, nullptr, nullptr)
+                                          : hfb::fr_f64(5, pr->d, pr->p, prm1, hfb::FrParams<double>{}, nullptr, nullptr)) == 1;
+    }
+    if (fused && pr->n_elem > 0) {
+        if (int rc = hf_fr_project(pr, u_dev, uf_dev, stream)) return rc;  // stage 1
+        int rc;
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int which = pr->with_source ? 4 : 3;
+        if (pr->precision == HF_FP32) {
+            const auto prm = make_params<float>(pr, u_dev, divf_dev, nullptr);
+            const auto fp = make_fr_params<float>(pr, &ms, uf_dev, nullptr, nullptr);
+            rc = hfb::fr_f32(which, pr->d, pr->p, prm, fp, nullptr, st);
+        } else {
+            const auto prm = make_params<double>(pr, u_dev, divf_dev, nullptr);
+            const auto fp = make_fr_params<double>(pr, &ms, uf_dev, nullptr, nullptr);
+            rc = hfb::fr_f64(which, pr->d, pr->p, prm, fp, nullptr, st);
+        }
+        if (rc == 0) return HF_OK;
+        if (rc > 0) return cuda_fail(cudaError_t(rc), "hf_fr_residual: fused stages 2-6");
+        // no fused form for this (d, p): stages 2+3+6, then 4+5 (the faces are written)
+        if (int r2 = hf_fused_divergence(pr, u_dev, divf_dev, stream)) return r2;
+        return hf_fr_correct(pr, &ms, uf_dev, nullptr, nullptr, divf_dev, stream);
+    }
     if (int rc = hf_fr_divergence_faces(pr, u_dev, uf_dev, divf_dev, stream)) return rc;  // stages 1+2+3+6
     return hf_fr_correct(pr, &ms, uf_dev, nullptr, nullptr, divf_dev, stream);  // stages 4+5
 }

@@ -25,6 +25,7 @@
 
 #include <cstdlib>
 
+#include "hf_launch.cuh"
 #include "hf_lines.cuh"
 
 namespace hfb {
@@ -349,23 +350,112 @@ __device__ __forceinline__ void fr_jump_regs(const R (&Uo)[n_vars_c(DIM)], const
     }
 }
 
+// Stages 4+5 on a chunk of NE elements resident in shared memory (layout [v][pt][el], the
+// elements E0 .. E0+ne-1): per axis one thread per (element, A-line) loads the own and the
+// neighbour face values at both line ends (the neighbour's from f.uf or a ghost layer),
+// forms the jumps F^I - F_A(U_own) in registers and applies
+// out(t) -= jac_A (g_L'(x_t) jump_- + g_R'(x_t) jump_+) in place, one axis after the other.
+// `before_update` runs once per thread ahead of its first shared-memory update (the staged
+// correction kernel waits there for its chunk).  Ends with a CTA barrier.
+template <class R, int DIM, int M, int NE, int BS, class Before>
+__device__ __forceinline__ void fr_correct_smem(R* __restrict__ sm, const Params<R>& p, const FrParams<R>& f,
+                                                long long E0, int ne, int tid, Before&& before_update) {
+    constexpr int NV = n_vars_c(DIM), LN = fr_lines<DIM, M>(), NP = ipow_c(M, DIM), FW = 2 * DIM * LN * NV;
+    __shared__ const R* own_f[NE];
+    __shared__ const R* nbr_f[NE][DIM][2];
+    const int G = int(p.group);
+    const int VS = G * 2 * DIM * LN;
+    for (int q = tid; q < ne * 2 * DIM; q += BS) {
+        const int el = q % ne, side = q / ne, A = side >> 1, s = side & 1;
+        const long long e = E0 + el;
+        const long long eg = f.mesh.e_begin + e;
+        const long long nx = f.mesh.dims[0], ny = f.mesh.dims[1];
+        const long long n_mesh = nx * ny * (DIM == 3 ? f.mesh.dims[2] : 1);
+        long long cx = eg % nx, cy = (eg / nx) % ny, cz = DIM == 3 ? eg / (nx * ny) : 0;
+        const int step = s ? 1 : -1;
+        if (A == 0) cx = (cx + step + nx) % nx;
+        else if (A == 1) cy = (cy + step + ny) % ny;
+        else cz = (cz + step + f.mesh.dims[2]) % f.mesh.dims[2];
+        const long long en = cx + nx * (cy + ny * cz);
+        long long enl;
+        const R* nb = fr_faces_of(f, en, n_mesh, &enl);
+        nbr_f[el][A][s] = nb + fr_elem_base(enl, G, FW) + (long long)G * LN * (1 - s + 2 * A);
+        if (side == 0) own_f[el] = f.uf + fr_elem_base(e, G, FW);
+    }
+    __syncthreads();
+    bool waited = false;
+    auto axis = [&](auto a_tag) {
+        constexpr int A = decltype(a_tag)::value;
+        for (int task = tid; task < NE * LN; task += BS) {
+            const int el = task % NE;
+            const int l = task / NE;
+            if (el >= ne) continue;
+            R jm[NV], jp[NV];
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const R* ow = own_f[el] + G * (l + LN * (s + 2 * A));
+                const R* nw = nbr_f[el][A][s] + G * l;
+                R Uo[NV], Un[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    Uo[v] = ow[VS * v];
+                    Un[v] = nw[VS * v];
+                }
+                const R lam = fmax(fr_wavespeed<R, DIM, A>(Uo, p), fr_wavespeed<R, DIM, A>(Un, p));
+                if (s == 0) fr_jump_regs<R, DIM, A>(Uo, Un, lam, 0, p, jm);
+                else fr_jump_regs<R, DIM, A>(Uo, Un, lam, 1, p, jp);
+            }
+            if (!waited) {
+                before_update();
+                waited = true;
+            }
+            R* ln = sm + el + NE * fr_line_point<DIM, M>(A, l, 0);
+            constexpr int TS = NE * (A == 0 ? 1 : (A == 1 ? M : M * M));
+            const R ja = p.jac[A];
+#pragma unroll
+            for (int t = 0; t < M; ++t) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    R* q = ln + TS * t + NE * NP * v;
+                    *q = *q - ja * fma(f.gl[t], jm[v], f.gr[t] * jp[v]);
+                }
+            }
+        }
+        __syncthreads();
+    };
+    axis(std::integral_constant<int, 0>{});
+    axis(std::integral_constant<int, 1>{});
+    if constexpr (DIM == 3) axis(std::integral_constant<int, 2>{});
+}
+
+// Stages 2+3+6 and 4+5 in one pass (hf_fr_residual): the lines kernel's chunk, after the
+// sweeps, gets the interface correction in shared memory and leaves it once -- the residual
+// is written once instead of written, read back and rewritten by a second kernel.  The faces
+// (stage 1) come from a projection launched just before (hf_fr_project_kernel).
+template <class R, int DIM, int M, int NE, bool SRC>
+__global__ void __launch_bounds__(LinesShape<R, DIM, M, NE>::BS)
+    hf_lines_fr_kernel(const __grid_constant__ Params<R> p, const __grid_constant__ FrParams<R> f) {
+    constexpr int BS = LinesShape<R, DIM, M, NE>::BS;
+    lines_chunk<R, DIM, M, NE, SRC, 1, false, NE, false>(p, [&](R* sm, long long E0, int nvalid, int tid) {
+        const long long left = p.n_elem - E0;
+        const int ne = int(left < nvalid ? left : nvalid);
+        fr_correct_smem<R, DIM, M, NE, BS>(sm, p, f, E0, ne, tid, [] {});
+    });
+}
+
 template <class R, int DIM, int M, int NE>
 __global__ void __launch_bounds__(FrCorrStagedShape<R, DIM, M, NE>::BS)
     hf_fr_correct_staged_kernel(const __grid_constant__ Params<R> p, const __grid_constant__ FrParams<R> f) {
     using S = FrCorrStagedShape<R, DIM, M, NE>;
     using L = typename S::L;
     using IO = typename L::IO;
-    constexpr int NV = S::NV, LN = S::LN, BS = S::BS, NP = ipow_c(M, DIM), FW = 2 * DIM * LN * NV;
+    constexpr int BS = S::BS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
     unsigned char* buf = smem_raw + S::HDR;
-    __shared__ const R* own_f[NE];
-    __shared__ const R* nbr_f[NE][DIM][2];
     const int tid = threadIdx.x;
     const long long E0 = static_cast<long long>(blockIdx.x) * NE;
     const int ne = int(p.n_elem - E0 < NE ? p.n_elem - E0 : NE);
-    const int G = int(p.group);
-    const int VS = G * 2 * DIM * LN;
     const long long grp = E0 / p.group;
     const long long gbase = grp * p.group_words + (E0 - grp * p.group);
     const bool contiguous = (p.group == NE);
@@ -395,67 +485,9 @@ __global__ void __launch_bounds__(FrCorrStagedShape<R, DIM, M, NE>::BS)
             s0[idx] = v;
         }
     }
-    for (int q = tid; q < ne * 2 * DIM; q += BS) {
-        const int el = q % ne, side = q / ne, A = side >> 1, s = side & 1;
-        const long long e = E0 + el;
-        const long long eg = f.mesh.e_begin + e;
-        const long long nx = f.mesh.dims[0], ny = f.mesh.dims[1];
-        const long long n_mesh = nx * ny * (DIM == 3 ? f.mesh.dims[2] : 1);
-        long long cx = eg % nx, cy = (eg / nx) % ny, cz = DIM == 3 ? eg / (nx * ny) : 0;
-        const int step = s ? 1 : -1;
-        if (A == 0) cx = (cx + step + nx) % nx;
-        else if (A == 1) cy = (cy + step + ny) % ny;
-        else cz = (cz + step + f.mesh.dims[2]) % f.mesh.dims[2];
-        const long long en = cx + nx * (cy + ny * cz);
-        long long enl;
-        const R* nb = fr_faces_of(f, en, n_mesh, &enl);
-        nbr_f[el][A][s] = nb + fr_elem_base(enl, G, FW) + (long long)G * LN * (1 - s + 2 * A);
-        if (side == 0) own_f[el] = f.uf + fr_elem_base(e, G, FW);
-    }
-    __syncthreads();
-    R* sm = reinterpret_cast<R*>(buf + head);
-
-    auto axis = [&](auto a_tag) {
-        constexpr int A = decltype(a_tag)::value;
-        for (int task = tid; task < NE * LN; task += BS) {
-            const int el = task % NE;
-            const int l = task / NE;
-            if (el >= ne) continue;
-            R jm[NV], jp[NV];
-#pragma unroll
-            for (int s = 0; s < 2; ++s) {
-                const R* ow = own_f[el] + G * (l + LN * (s + 2 * A));
-                const R* nw = nbr_f[el][A][s] + G * l;
-                R Uo[NV], Un[NV];
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    Uo[v] = ow[VS * v];
-                    Un[v] = nw[VS * v];
-                }
-                const R lam = fmax(fr_wavespeed<R, DIM, A>(Uo, p), fr_wavespeed<R, DIM, A>(Un, p));
-                if (s == 0) fr_jump_regs<R, DIM, A>(Uo, Un, lam, 0, p, jm);
-                else fr_jump_regs<R, DIM, A>(Uo, Un, lam, 1, p, jp);
-            }
-            if constexpr (A == 0) {
-                if (fast) mbar_wait_parity(bar, 0);  // the chunk has landed (idempotent per thread)
-            }
-            R* ln = sm + el + NE * fr_line_point<DIM, M>(A, l, 0);
-            constexpr int TS = NE * (A == 0 ? 1 : (A == 1 ? M : M * M));
-            const R ja = p.jac[A];
-#pragma unroll
-            for (int t = 0; t < M; ++t) {
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    R* q = ln + TS * t + NE * NP * v;
-                    *q = *q - ja * fma(f.gl[t], jm[v], f.gr[t] * jp[v]);
-                }
-            }
-        }
-        __syncthreads();
-    };
-    axis(std::integral_constant<int, 0>{});
-    axis(std::integral_constant<int, 1>{});
-    if constexpr (DIM == 3) axis(std::integral_constant<int, 2>{});
+    fr_correct_smem<R, DIM, M, NE, BS>(reinterpret_cast<R*>(buf + head), p, f, E0, ne, tid, [&] {
+        if (fast) mbar_wait_parity(bar, 0);  // the chunk has landed (overlapped with the face loads)
+    });
 
     if (fast) {
         fence_proxy_async_smem();
@@ -508,7 +540,7 @@ int fr_project_launch(const Params<R>& prm, const FrParams<R>& fp, R* uf, cudaSt
     p.fast_ok = (p.group == NE || (p.group % NE == 0 && (NE * sizeof(R)) % 16 == 0 &&
                                    ((long long)p.group * sizeof(R)) % 16 == 0)) &&
                 (reinterpret_cast<uintptr_t>(p.u) & 15u) == 0;
-    if (S::SMEM > 48 * 1024) {
+    if (S::SMEM > 40 * 1024) {  // (static shared memory counts against the default 48 KB)
         cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM));
         if (e != cudaSuccess) return int(e);
     }
@@ -530,7 +562,7 @@ template <class R, int DIM, int M, int NE>
 int fr_correct_launch(const Params<R>& prm, const FrParams<R>& fp, cudaStream_t st) {
     using S = FrCorrShape<R, DIM, M, NE>;
     auto kernel = hf_fr_correct_kernel<R, DIM, M, NE>;
-    if (S::SMEM > 48 * 1024) {
+    if (S::SMEM > 40 * 1024) {  // (static shared memory counts against the default 48 KB)
         cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM));
         if (e != cudaSuccess) return int(e);
     }
@@ -546,7 +578,7 @@ int fr_correct_staged_launch(const Params<R>& prm, const FrParams<R>& fp, cudaSt
     p.fast_ok = (p.group == NE || (p.group % NE == 0 && (NE * sizeof(R)) % 16 == 0 &&
                                    ((long long)p.group * sizeof(R)) % 16 == 0)) &&
                 (reinterpret_cast<uintptr_t>(p.out) & 15u) == 0;
-    if (S::SMEM > 48 * 1024) {
+    if (S::SMEM > 40 * 1024) {  // (static shared memory counts against the default 48 KB)
         cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM));
         if (e != cudaSuccess) return int(e);
     }
@@ -563,6 +595,63 @@ int fr_correct_staged_dispatch(const Params<R>& prm, const FrParams<R>& fp, cuda
     return fr_correct_staged_launch<R, DIM, M, NE>(prm, fp, st);
 }
 
+// The one-chunk lines variant the fused residual kernel uses: the selected variant when it is
+// a one-chunk form (a component-split one maps to its base chunk), else variant 0.
+template <class R, int DIM, int M>
+constexpr int fr_fused_variant() {
+    for (const SelRow& r : kSelect)
+        if (r.d == DIM && r.p == M - 1 && r.prec == (sizeof(R) == 8 ? 1 : 0) && r.method == 2) {
+            if (is_one_chunk_variant(r.variant)) return r.variant;
+            if (r.variant == 19) return 0;
+            if (r.variant == 20) return 1;
+            if (r.variant == 21) return 2;
+            if (r.variant == 22) return 7;
+        }
+    return 0;
+}
+
+template <class R, int DIM, int M, int NE, bool SRC>
+int lines_fr_launch(Params<R> p, const FrParams<R>& f, cudaStream_t st) {
+    using S = LinesShape<R, DIM, M, NE>;
+    auto kernel = hf_lines_fr_kernel<R, DIM, M, NE, SRC>;
+    const bool tile = tile_layout<R, NE>(p.group) && aligned16(p.u) && aligned16(p.out);
+    const long long n_groups = (p.n_elem + p.group - 1) / p.group;
+    const int sub = (p.group + NE - 1) / NE;
+    const long long grid = tile ? n_groups * sub : (p.n_elem + NE - 1) / NE;
+    p.fast_ok = (tile || bulk_layout<R, NE>(p.group)) && aligned16(p.u) && aligned16(p.out);
+    if (tile) {
+        p.tile = 1;
+        p.sub_per_group = sub;
+        if (!encode_chunk_map<R>(&p.tm_u, p.u, DIM, M, p.group, n_groups, NE) ||
+            !encode_chunk_map<R>(&p.tm_out, p.out, DIM, M, p.group, n_groups, NE))
+            p.fast_ok = 0;
+    }
+    if (int e = set_smem_attr(kernel, S::SMEM)) return e;
+    return int(launch_kernel(kernel, dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st, p, f));
+}
+
+// (d, p, precision) where the one-pass residual (projection, then the lines kernel with the
+// correction in shared memory) beats the pair (lines kernel with the faces, then the
+// correction kernel) by >= 2 % on one box (1e7 points, profiles/r02/ext_r02_fr_fused_ab.jsonl):
+// d3 FP64 p1 / p2 / p6 (1.04-1.14x), d3 FP32 p6 (1.04-1.06x), d2 FP32 p2-p8 (1.03-1.09x),
+// d2 FP64 p2-p4, p6-p8 (1.04-1.13x).  Elsewhere the pair (up to 5 % faster at d3 FP32 p1).
+template <class R, int DIM, int M>
+constexpr bool fr_residual_fused() {
+    constexpr int p = M - 1;
+    if constexpr (DIM == 3) return sizeof(R) == 8 ? (p == 1 || p == 2 || p == 6) : p == 6;
+    else return sizeof(R) == 4 ? p >= 2 : (p >= 2 && p != 5);
+}
+
+template <class R, int DIM, int M>
+int lines_fr_dispatch(const Params<R>& prm, const FrParams<R>& fp, bool src, cudaStream_t st) {
+    constexpr int NE = variant_ne<R, DIM, M, fr_fused_variant<R, DIM, M>()>();
+    if constexpr (NE < 1 || LinesShape<R, DIM, M, NE>::SMEM > size_t(kMaxSmemPerCta)) {
+        return -1;
+    } else {
+        return src ? lines_fr_launch<R, DIM, M, NE, true>(prm, fp, st) : lines_fr_launch<R, DIM, M, NE, false>(prm, fp, st);
+    }
+}
+
 template <class R, int DIM, int M>
 int fr_correct_dispatch_jumps(const Params<R>& prm, const FrParams<R>& fp, cudaStream_t st);
 
@@ -577,8 +666,11 @@ constexpr bool fr_correct_staged() {
 
 template <class R, int DIM, int M>
 int fr_stage(int which, const Params<R>& prm, const FrParams<R>& fp, R* uf, cudaStream_t st) {
+    if (which == 5) return fr_residual_fused<R, DIM, M>() ? 1 : 0;
     if (prm.n_elem == 0) return 0;
     if (which == 1) return fr_project_dispatch<R, DIM, M>(prm, fp, uf, st);
+    if (which == 3 || which == 4) return lines_fr_dispatch<R, DIM, M>(prm, fp, which == 4, st);  // 4: with source
+    if (which == 5) return fr_residual_fused<R, DIM, M>() ? 1 : 0;  // query: the one-pass residual is preferred
 #ifdef HF_FR_AB
     if (const char* ev = std::getenv("HF_FR_STAGED"))
         return ev[0] == '1' ? fr_correct_staged_dispatch<R, DIM, M>(prm, fp, st)

@@ -249,11 +249,11 @@ inline bool pdl_enabled() {
     return on;
 }
 
-template <class R>
-inline cudaError_t launch_kernel(void (*kernel)(Params<R>), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                                 const Params<R>& p) {
+template <class... Args>
+inline cudaError_t launch_kernel(void (*kernel)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                 const Args&... args) {
     if (!pdl_enabled()) {
-        kernel<<<grid, block, smem, st>>>(p);
+        kernel<<<grid, block, smem, st>>>(args...);
         return cudaGetLastError();
     }
     cudaLaunchAttribute at[1];
@@ -266,12 +266,14 @@ inline cudaError_t launch_kernel(void (*kernel)(Params<R>), dim3 grid, dim3 bloc
     cfg.stream = st;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kernel, p);
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 template <class K>
 inline int set_smem_attr(K kernel, size_t smem) {
-    if (smem > 48 * 1024) {
+    // the default 48 KB limit counts static + dynamic shared memory; the kernels' static
+    // arrays (element bases, FR face pointers) stay below 8 KB, so opt in from 40 KB of dynamic
+    if (smem > 40 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return int(e);
     }
@@ -343,7 +345,7 @@ cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
     }
 #endif
     if (int e = set_smem_attr(kernel, smem)) return cudaError_t(e);
-    return launch_kernel<R>(kernel, dim3(unsigned(grid)), dim3(S::BS), smem, st, p);
+    return launch_kernel(kernel, dim3(unsigned(grid)), dim3(S::BS), smem, st, p);
 }
 
 inline int num_sms() {
@@ -415,14 +417,14 @@ cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dr
     if (!p.fast_ok || n_full == 0) return launch_lines<R, DIM, M, NE, SRC, 1, FACES, NE, CS>(p, st, nullptr, false);
     p.chunk0 = 0;
     p.n_chunks = n_full;
-    cudaError_t e = launch_kernel<R>(kernel, dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st, p);
+    cudaError_t e = launch_kernel(kernel, dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st, p);
     if (e != cudaSuccess) return e;
     const long long n_chunks = (p.n_elem + NE - 1) / NE;
     if (n_full < n_chunks) {  // the partial (or allocation-final) chunk(s)
         auto tail = hf_lines_kernel<R, DIM, M, NE, SRC, 1, FACES, NE, CS>;
         if (int e2 = set_smem_attr(tail, L::SMEM)) return cudaError_t(e2);
         p.chunk0 = n_full;
-        e = launch_kernel<R>(tail, dim3(unsigned(n_chunks - n_full)), dim3(L::BS), L::SMEM, st, p);
+        e = launch_kernel(tail, dim3(unsigned(n_chunks - n_full)), dim3(L::BS), L::SMEM, st, p);
     }
     return e;
 }

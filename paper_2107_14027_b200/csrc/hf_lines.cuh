@@ -533,9 +533,15 @@ __device__ __forceinline__ void lines_sweeps_at(unsigned char* buf, int head, R*
     }
 }
 
-template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false, int GS = NE, bool CS = false>
-__global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT, GS, CS>::BS)
-    hf_lines_kernel(const __grid_constant__ Params<R> p) {
+// No work between the sweeps and the store (the plain fused kernel).
+struct NoChunkHook {};
+
+// One chunk of the lines kernel: stage, sweeps, [hook], store.  `hook(chunk, E0, nvalid, tid)`
+// runs on the finished divergence in shared memory (layout [v][pt][el] of NE elements, GS ==
+// NE) between two CTA barriers -- the FR interface correction of hf_fr.cuh uses it to apply
+// stages 4+5 before the chunk leaves shared memory.
+template <class R, int DIM, int M, int NE, bool SRC, int LPT, bool FACES, int GS, bool CS, class Hook>
+__device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
     using S = LinesShape<R, DIM, M, NE, LPT, GS, CS>;
     constexpr int BS = S::BS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -619,6 +625,10 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT, GS, CS>::BS)
 
     // ---------------- d sweeps ----------------
     lines_sweeps_at<R, DIM, M, NE, SRC, 0, (CS ? S::NT : BS), FACES, GS, CS>(buf, head, acc, p, tid, 0, E0, nvalid);
+    if constexpr (!std::is_same_v<std::decay_t<Hook>, NoChunkHook>) {
+        __syncthreads();
+        hook(reinterpret_cast<R*>(buf + head), E0, nvalid, tid);
+    }
 
     // ---------------- write the finished chunk ----------------
     if (fast) {
@@ -645,6 +655,12 @@ __global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT, GS, CS>::BS)
             if (b >= 0) __stcs(p.out + b + G * row, s[idx]);
         }
     }
+}
+
+template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false, int GS = NE, bool CS = false>
+__global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT, GS, CS>::BS)
+    hf_lines_kernel(const __grid_constant__ Params<R> p) {
+    lines_chunk<R, DIM, M, NE, SRC, LPT, FACES, GS, CS>(p, NoChunkHook{});
 }
 
 }  // namespace hfb

@@ -149,9 +149,12 @@ def test_fr_slab_driver_single_rank(cuda):
 @pytest.mark.parametrize("d,p,dims,g", [(3, 1, (4, 4, 2), None), (3, 3, (3, 4, 4), None), (3, 6, (2, 3, 3), None),
                                         (2, 4, (8, 6), None), (3, 4, (3, 2, 5), 1)])
 def test_fused_stage1_equals_separate_stages(cuda, d, p, dims, g, fp32):
-    """hf_fr_residual writes the faces from inside the fused kernel (FR stage 1
-    fused into the lines kernel's staged chunk): faces and residual bit-identical
-    to the separate hf_fused_divergence + hf_fr_project + hf_fr_correct path."""
+    """hf_fr_residual (stage 1, then stages 2+3+6 and 4+5 in one lines kernel that corrects
+    its chunk in shared memory) and the stand-alone stages 1+2+3+6 entry point (the
+    multi-GPU drivers' first step) against the separate hf_fused_divergence +
+    hf_fr_project + hf_fr_correct path: faces bit-identical; the residual bit-identical for
+    the stand-alone entry and equal to rounding (the correction applied axis by axis in
+    shared memory instead of as one sum) for hf_fr_residual."""
     import paper_2107_14027_b200 as hf
     from paper_2107_14027_b200 import Precision
     prec = Precision.fp32 if fp32 else Precision.fp64
@@ -172,7 +175,8 @@ def test_fused_stage1_equals_separate_stages(cuda, d, p, dims, g, fp32):
     hf.fr_correct_device(pr, hf.make_mesh(dims, d), uf_b, out_b)
     torch.cuda.synchronize()
     assert torch.equal(uf_a, uf_b)
-    assert torch.equal(out_a, out_b)
+    scale = max(1.0, float(out_b.abs().max()))
+    assert float((out_a - out_b).abs().max()) / scale <= (2e-6 if fp32 else 1e-14)
     # the stand-alone stages 1+2+3+6 entry point (the multi-GPU drivers' first step)
     out_c = torch.zeros_like(out_a)
     uf_c = torch.zeros_like(uf_a)

@@ -1,8 +1,9 @@
 """GPU: the FR right-hand side on layer slabs with the ghost layers read from the
 neighbours' memory through CUDA IPC (multi_gpu.FrPeers) -- two (three) processes
 sharing the one GPU of the test box stand in for ranks on NVLink-connected GPUs;
-the result must equal the single-partition residual bit-for-bit... up to the
-summation order, which is the same kernel's: exactly equal."""
+the result must equal the single-partition residual (to rounding where the single-device
+path takes the one-pass residual, whose correction is summed in another order) and the
+oracle at 1e-12."""
 import os
 import socket
 
@@ -84,5 +85,8 @@ def test_fr_ghost_layers_from_peer_memory(cuda, world):
     for pr_ in procs:
         pr_.join(timeout=60)
     assert len(out[0]) == 2, out
+    # equal to the single-device residual to rounding: where hf_fr_residual takes the one-pass
+    # form (hf_fr.cuh fr_residual_fused) its correction is applied axis by axis, the slab
+    # path's correction kernel may sum the axes first
     for diff_device, err_oracle in out[0]:
-        assert diff_device == 0.0 and err_oracle <= 1e-12, out[0]
+        assert diff_device <= 1e-13 and err_oracle <= 1e-12, out[0]
