@@ -309,7 +309,11 @@ cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
     const long long n_groups = (p.n_elem + p.group - 1) / p.group;
     const int sub = (p.group + NE - 1) / NE;
     const long long grid = tile ? n_groups * sub : (p.n_elem + NE - 1) / NE;
-    const bool fast_layout = tile || (GS == NE ? bulk_layout<R, NE>(p.group) : p.group == GS);
+    // grouped chunks: one contiguous image, or (S::PADW) one exact copy per group -- then every
+    // group must start 16-byte aligned (group_words * w a multiple of 16, aligned buffers)
+    const bool fast_layout =
+        tile || (GS == NE ? bulk_layout<R, NE>(p.group)
+                          : p.group == GS && (S::PADW == 0 || (p.group_words * (long long)sizeof(R)) % 16 == 0));
     if (info) {
         info->method = 2;
         info->elems_per_cta = NE;

@@ -44,6 +44,16 @@
 
 namespace hfb {
 
+// Padding (words) after each staged group of a grouped chunk (GS < NE): when the group's
+// byte size is an even multiple of 16, successive groups would start in only a few bank
+// classes (e.g. element-major p3: 832 words = 0 mod 32, every element in the same class),
+// so each group is staged at a stride that is an odd multiple of 16 bytes (one bulk copy
+// per group).  Groups whose size is not a multiple of 16 bytes stay one contiguous image.
+constexpr int grouped_pad_words(int w, int blk_words) {
+    if ((blk_words * w) % 16 != 0 || ((blk_words * w) / 16) % 2 == 1) return 0;
+    return 16 / w;
+}
+
 // LPT: lines per thread of the one-chunk-per-CTA kernel (block = LINES / LPT
 // threads): larger chunks per block without more threads, for the low-order
 // cases whose per-line work is small and whose bytes in flight per SM are
@@ -72,13 +82,25 @@ struct LinesShape {
     static constexpr int IN_BYTES = IN_WORDS * int(sizeof(R));
     static constexpr int ROW_BYTES = NE * int(sizeof(R));
     using IO = ChunkIO<R, NE, NP * NV, IN_BYTES>;
-    static constexpr int BUF_BYTES = IO::BUF_BYTES;  // chunk buffer incl. alignment slack
-    static constexpr size_t SMEM = HDR + size_t(BUF_BYTES) + size_t(ACC_WORDS) * sizeof(R);
     static constexpr int VS = GS * NP;          // word stride between variables
-    static constexpr int BLK = GS * NP * NV;    // one staged group
+    static constexpr int BLK = GS * NP * NV;    // one group in HBM
+    static constexpr int PADW = GS < NE ? grouped_pad_words(int(sizeof(R)), BLK) : 0;
+    static constexpr int BLKP = BLK + PADW;     // one staged group (padded: one bulk copy per group)
+    static constexpr int BUF_BYTES =            // chunk buffer incl. alignment slack
+        PADW ? ((NE / GS) * BLKP * int(sizeof(R)) + 15) / 16 * 16 : IO::BUF_BYTES;
+    static constexpr size_t SMEM = HDR + size_t(BUF_BYTES) + size_t(ACC_WORDS) * sizeof(R);
     // word of (element, point, variable) in the staged chunk
     __host__ __device__ static constexpr int word(int el, int pt, int v) {
-        return (el % GS) + GS * pt + VS * v + (el / GS) * BLK;
+        return (el % GS) + GS * pt + VS * v + (el / GS) * BLKP;
+    }
+    // staged position of the li-th word of the chunk's HBM image (li = group * BLK + rem)
+    __host__ __device__ static constexpr int staged(int li) {
+        if constexpr (PADW == 0) {
+            return li;
+        } else {
+            const int b = li / BLK;
+            return li + b * PADW;
+        }
     }
     // The accumulator region keeps the [row][pt][el] layout of NE elements whatever GS is
     // (its element classes then spread over the banks; a grouped chunk's state region
@@ -87,7 +109,7 @@ struct LinesShape {
         if constexpr (GS == NE) {
             return o;
         } else {
-            const int blk = o / BLK, rem = o - blk * BLK;
+            const int blk = o / BLKP, rem = o - blk * BLKP;
             return blk * GS + rem % GS + NE * (rem / GS);
         }
     }
@@ -105,17 +127,19 @@ __device__ __forceinline__ bool chunk_bulk_ok(const Params<R>& p, long long gbas
 
 // Outputs of one line point (index i of the sweep's line): gradient rows final
 // (+ source), continuity / momentum partials accumulated or finished.
-template <class R, int DIM, int M, int NE, bool SRC, int A, int PHASE, int GS = NE>
+// GRAD = false: the caller stores the gradient rows itself (vectorised x-lines, lines_sweep).
+template <class R, int DIM, int M, int NE, bool SRC, int A, int PHASE, int GS = NE, bool GRAD = true>
 __device__ __forceinline__ void lines_emit(R* __restrict__ q, R* __restrict__ a, const Params<R>& p, const R (&dV)[DIM],
                                            const R (&dQ)[DIM]) {
     constexpr int VS = GS * ipow_c(M, DIM);   // state rows
     constexpr int AS = NE * ipow_c(M, DIM);   // accumulator rows
+    if constexpr (GRAD)
 #pragma unroll
-    for (int b = 0; b < DIM; ++b) {
-        R o = p.jac_invT[A] * dV[b];
-        if constexpr (SRC) o = fma(-p.invT, q[VS * var_grad_c(DIM, b, A)], o);
-        q[VS * var_grad_c(DIM, b, A)] = o;
-    }
+        for (int b = 0; b < DIM; ++b) {
+            R o = p.jac_invT[A] * dV[b];
+            if constexpr (SRC) o = fma(-p.invT, q[VS * var_grad_c(DIM, b, A)], o);
+            q[VS * var_grad_c(DIM, b, A)] = o;
+        }
     const R c = p.jac[A] * dV[A];
     if constexpr (PHASE == 0) {
         a[0] = c;
@@ -134,14 +158,27 @@ __device__ __forceinline__ void lines_emit(R* __restrict__ q, R* __restrict__ a,
 
 // Word offset (inside a chunk) of the first point of line L of a sweep along A:
 // L = el + NE * r, r enumerating the two fixed indices (layout.hpp:128-134).
-template <int DIM, int M, int NE, int A, int GS = NE>
+template <int DIM, int M, int NE, int A, int GS = NE, int BLKS = GS * ipow_c(M, DIM) * n_vars_c(DIM)>
 __host__ __device__ constexpr int line_offset(int L) {
     const int el = L % NE;
     const int r = L / NE;
     int base_pt = r;                                  // d3 A=2: r = i + M j;  d2 A=1: r = i
     if (A == 0) base_pt = M * r;                      // d3: r = j + M k;  d2: r = j
     if (DIM == 3 && A == 1) base_pt = (r % M) + M * M * (r / M);  // r = i + M k
-    return (el % GS) + GS * base_pt + (el / GS) * GS * ipow_c(M, DIM) * n_vars_c(DIM);
+    return (el % GS) + GS * base_pt + (el / GS) * BLKS;
+}
+
+// Vector width (words) of an x-line row read in an element-major chunk (GS = 1): every line
+// starts at a multiple of M words inside its element's staged block, whose stride BLKP and
+// the variable stride VS are byte multiples of the vector too.  1 = scalar reads.
+template <class R, int M, int GS, int BLKP, int VS, int A>
+__host__ __device__ constexpr int x_line_vec() {
+    if (A != 0 || GS != 1) return 1;
+    for (int vb = 16; vb > int(sizeof(R)); vb /= 2) {
+        const int vw = vb / int(sizeof(R));
+        if (M % vw == 0 && (BLKP * int(sizeof(R))) % vb == 0 && (VS * int(sizeof(R))) % vb == 0) return vw;
+    }
+    return 1;
 }
 
 // Bank-conflict-free assignment of a sweep's lines to (iteration, thread).
@@ -167,7 +204,10 @@ struct LineMap {
 template <class R, int DIM, int M, int NE, int A, int NTHR, int GS = NE>
 constexpr LineMap<R, DIM, M, NE, A, NTHR, GS> make_line_map() {
     using LM = LineMap<R, DIM, M, NE, A, NTHR, GS>;
-    constexpr int B = sizeof(R) == 4 ? 32 : 16;  // bank classes per (half-)warp
+    using S = LinesShape<R, DIM, M, NE, 1, GS>;
+    // vectorised x-lines (x_line_vec): a VW-word access, 128 / (VW * sizeof(R)) lanes per wavefront
+    constexpr int VW = x_line_vec<R, M, GS, S::BLKP, S::VS, A>();
+    constexpr int B = VW > 1 ? 128 / (VW * int(sizeof(R))) : sizeof(R) == 4 ? 32 : 16;  // bank classes per phase
     constexpr int HALVES = 32 / B;
     constexpr int NW = NTHR / 32;
     LM m{};
@@ -176,8 +216,8 @@ constexpr LineMap<R, DIM, M, NE, A, NTHR, GS> make_line_map() {
     int spill[LM::LINES > 0 ? LM::LINES : 1] = {};
     int n_spill = 0;
     for (int L = 0; L < LM::LINES; ++L) {
-        const int o = line_offset<DIM, M, NE, A, GS>(L);
-        const int c = o % B;
+        const int o = line_offset<DIM, M, NE, A, GS, S::BLKP>(L);
+        const int c = (o / VW) % B;
         const int idx = next[c]++;
         const int it = idx / (NW * HALVES);
         if (it >= LM::ITERS) {
@@ -196,6 +236,44 @@ constexpr LineMap<R, DIM, M, NE, A, NTHR, GS> make_line_map() {
 template <class R, int DIM, int M, int NE, int A, int NTHR, int GS = NE>
 __device__ const LineMap<R, DIM, M, NE, A, NTHR, GS> kLineMap = make_line_map<R, DIM, M, NE, A, NTHR, GS>();
 
+template <class R, int M, int VW>
+__device__ __forceinline__ void load_row(const R* __restrict__ q, R (&out)[M]) {
+    static_assert(VW * sizeof(R) == 16 || VW * sizeof(R) == 8, "8- or 16-byte rows");
+    if constexpr (sizeof(R) == 4 && VW == 4) {
+#pragma unroll
+        for (int t = 0; t < M; t += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(q + t);
+            out[t] = v.x; out[t + 1] = v.y; out[t + 2] = v.z; out[t + 3] = v.w;
+        }
+    } else if constexpr (sizeof(R) == 4) {
+#pragma unroll
+        for (int t = 0; t < M; t += 2) {
+            const float2 v = *reinterpret_cast<const float2*>(q + t);
+            out[t] = v.x; out[t + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < M; t += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(q + t);
+            out[t] = v.x; out[t + 1] = v.y;
+        }
+    }
+}
+
+template <class R, int M, int VW>
+__device__ __forceinline__ void store_row(R* __restrict__ q, const R (&in)[M]) {
+    if constexpr (sizeof(R) == 4 && VW == 4) {
+#pragma unroll
+        for (int t = 0; t < M; t += 4) *reinterpret_cast<float4*>(q + t) = make_float4(in[t], in[t + 1], in[t + 2], in[t + 3]);
+    } else if constexpr (sizeof(R) == 4) {
+#pragma unroll
+        for (int t = 0; t < M; t += 2) *reinterpret_cast<float2*>(q + t) = make_float2(in[t], in[t + 1]);
+    } else {
+#pragma unroll
+        for (int t = 0; t < M; t += 2) *reinterpret_cast<double2*>(q + t) = make_double2(in[t], in[t + 1]);
+    }
+}
+
 // One sweep along axis A.  PHASE: 0 = first sweep, 1 = middle, 2 = last.
 // `o` = the line's first word inside the chunk (line_offset()).
 template <class R, int DIM, int M, int NE, bool SRC, int A, int PHASE, int GS = NE>
@@ -206,24 +284,47 @@ __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ a
 
     R* __restrict__ sb = s + o;
     R* __restrict__ ab = acc + S::acc_of(o);
-
     const R nu = p.nu;
     using PR = Pair<R>;
     // W[b][t] = (V_b, M_ba) at line point t: both lines are contracted with the same D rows
     PR W[DIM][M];
-#pragma unroll
-    for (int t = 0; t < M; ++t) {
-        const R* q = sb + GS * STRIDE * t;
-        const R P = q[0];
-        R V[DIM];
-#pragma unroll
-        for (int b = 0; b < DIM; ++b) V[b] = q[VS * (1 + b)];
+    constexpr int VW = x_line_vec<R, M, GS, S::BLKP, VS, A>();
+    // element-major chunk (GS = 1): an x-line's M points are consecutive words, so each
+    // variable's row is read (and each gradient row of the first sweep written) with VW-wide
+    // accesses -- a quarter-warp of LDS.128 covers the 32 banks, where scalar accesses of
+    // lines at multiples of M words would collide M-way
+    constexpr bool VEC_ST = VW > 1 && PHASE == 0;
+    R G[DIM][M], Gout[DIM][VEC_ST ? M : 1];
+    if constexpr (VW > 1) {
+        R P[M], V[DIM][M];
+        load_row<R, M, VW>(sb, P);
 #pragma unroll
         for (int b = 0; b < DIM; ++b) {
-            const R g = q[VS * var_grad_c(DIM, b, A)];
-            // codegen_util.hpp:191-202 operation order: base, then fma(V_b, V_a, base)
-            const R base = (b == A) ? fma(-nu, g, P) : (-nu) * g;
-            W[b][t] = PR::make(V[b], fma(V[b], V[A], base));
+            load_row<R, M, VW>(sb + VS * (1 + b), V[b]);
+            load_row<R, M, VW>(sb + VS * var_grad_c(DIM, b, A), G[b]);
+        }
+#pragma unroll
+        for (int t = 0; t < M; ++t)
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) {
+                const R base = (b == A) ? fma(-nu, G[b][t], P[t]) : (-nu) * G[b][t];
+                W[b][t] = PR::make(V[b][t], fma(V[b][t], V[A][t], base));
+            }
+    } else {
+#pragma unroll
+        for (int t = 0; t < M; ++t) {
+            const R* q = sb + GS * STRIDE * t;
+            const R P = q[0];
+            R V[DIM];
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) V[b] = q[VS * (1 + b)];
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) {
+                const R g = q[VS * var_grad_c(DIM, b, A)];
+                // codegen_util.hpp:191-202 operation order: base, then fma(V_b, V_a, base)
+                const R base = (b == A) ? fma(-nu, g, P) : (-nu) * g;
+                W[b][t] = PR::make(V[b], fma(V[b], V[A], base));
+            }
         }
     }
 
@@ -238,7 +339,15 @@ __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ a
             dV_[b_] = (DP)[b_].x();                                                                            \
             dQ_[b_] = (DP)[b_].y();                                                                            \
         }                                                                                                      \
-        lines_emit<R, DIM, M, NE, SRC, A, PHASE, GS>(sb + GS * STRIDE * (I), ab + NE * STRIDE * (I), p, dV_, dQ_); \
+        if constexpr (VEC_ST) {                                                                                \
+            _Pragma("unroll") for (int b_ = 0; b_ < DIM; ++b_) {                                               \
+                R o_ = p.jac_invT[A] * dV_[b_];                                                                \
+                if constexpr (SRC) o_ = fma(-p.invT, G[b_][(I)], o_);                                          \
+                Gout[b_][(I)] = o_;                                                                            \
+            }                                                                                                   \
+        }                                                                                                       \
+        lines_emit<R, DIM, M, NE, SRC, A, PHASE, GS, !VEC_ST>(sb + GS * STRIDE * (I), ab + NE * STRIDE * (I), p, dV_, \
+                                                              dQ_);                                            \
     } while (0)
     if constexpr (M < HF_EVEN_ODD_MIN_M) {
 #pragma unroll
@@ -301,6 +410,9 @@ __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ a
             HF_EMIT(H, d);
         }
     }
+    if constexpr (VEC_ST)
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) store_row<R, M, VW>(sb + VS * var_grad_c(DIM, b, A), Gout[b]);
 }
 
 #undef HF_EMIT
@@ -572,8 +684,11 @@ __device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
     // one contiguous byte range: the chunk is one group (GS = NE) or NE / GS whole groups
     const bool contiguous = (p.group == GS);
     const bool full = E0 + nvalid <= p.n_elem;
-    const bool fast = p.tile ? (p.fast_ok && full) : chunk_bulk_ok<R, S::IN_WORDS>(p, gbase, full, contiguous);
-    const int head = (fast && !p.tile) ? IO::head_bytes(p.u + gbase, contiguous) : 0;
+    // padded grouped chunk (S::PADW): one exact 16-byte-multiple copy per group, no superset
+    const bool fast = p.tile ? (p.fast_ok && full)
+                             : (S::PADW ? (p.fast_ok && full && contiguous)
+                                        : chunk_bulk_ok<R, S::IN_WORDS>(p, gbase, full, contiguous));
+    const int head = (fast && !p.tile && !S::PADW) ? IO::head_bytes(p.u + gbase, contiguous) : 0;
     R* s = reinterpret_cast<R*>(smem_raw + S::HDR);  // guarded path (head == 0)
     __shared__ long long ebase[NE];                   // guarded path: element word bases, -1 = absent
 
@@ -584,7 +699,13 @@ __device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
             fence_mbar_init();
         }
         __syncthreads();
-        if (p.tile) {
+        if constexpr (S::PADW > 0) {  // one bulk copy per group, each to its padded slot
+            if (tid == 0) mbar_arrive_expect_tx(bar, uint32_t(S::IN_BYTES));
+            __syncthreads();
+            for (int g = tid; g < NE / GS; g += BS)
+                bulk_g2s(buf + g * S::BLKP * int(sizeof(R)), p.u + gbase + static_cast<long long>(g) * S::BLK,
+                         S::BLK * int(sizeof(R)), bar);
+        } else if (p.tile) {
             if (tid == 0) {  // one TMA tensor copy: the box {NE, m, m^(d-1), n_v, 1}; e_l >= group zero-filled
                 mbar_arrive_expect_tx(bar, uint32_t(S::IN_BYTES));
                 tma_load_5d(buf, &p.tm_u, sub * NE, 0, 0, 0, static_cast<int>(grp), bar);
@@ -612,12 +733,13 @@ __device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
         __syncthreads();
         const long long G = p.group;
         for (int idx = tid; idx < S::IN_WORDS; idx += BS) {
-            const int blk = idx / S::BLK, rem = idx - blk * S::BLK;  // staged word -> (el, row)
+            const int blk = idx / S::BLK, rem = idx - blk * S::BLK;  // image word -> (el, row)
             const int el = blk * GS + rem % GS;
             const int row = rem / GS;
             const long long b = ebase[el];
-            if (b >= 0) cp_async_word(s + idx, p.u + b + G * row);
-            else s[idx] = R(0);
+            R* dst = s + S::staged(idx);
+            if (b >= 0) cp_async_word(dst, p.u + b + G * row);
+            else *dst = R(0);
         }
         cp_async_wait_all();
         __syncthreads();
@@ -634,7 +756,13 @@ __device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
     if (fast) {
         fence_proxy_async_smem();
         __syncthreads();
-        if (p.tile) {
+        if constexpr (S::PADW > 0) {
+            for (int g = tid; g < NE / GS; g += BS)
+                bulk_s2g(p.out + gbase + static_cast<long long>(g) * S::BLK, buf + g * S::BLKP * int(sizeof(R)),
+                         S::BLK * int(sizeof(R)));
+            bulk_commit();
+            bulk_wait_read_all();
+        } else if (p.tile) {
             if (tid == 0) {  // elements past the group's end are clipped by the tensor map
                 tma_store_5d(&p.tm_out, sub * NE, 0, 0, 0, static_cast<int>(grp), buf);
                 bulk_commit();
@@ -652,7 +780,7 @@ __device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
             const int el = blk * GS + rem % GS;
             const int row = rem / GS;
             const long long b = ebase[el];
-            if (b >= 0) __stcs(p.out + b + G * row, s[idx]);
+            if (b >= 0) __stcs(p.out + b + G * row, s[S::staged(idx)]);
         }
     }
 }
