@@ -173,12 +173,13 @@ __host__ __device__ constexpr int line_offset(int L) {
 // the variable stride VS are byte multiples of the vector too.  1 = scalar reads.
 template <class R, int M, int GS, int BLKP, int VS, int A>
 __host__ __device__ constexpr int x_line_vec() {
-    if (A != 0 || GS != 1) return 1;
-    for (int vb = 16; vb > int(sizeof(R)); vb /= 2) {
-        const int vw = vb / int(sizeof(R));
-        if (M % vw == 0 && (BLKP * int(sizeof(R))) % vb == 0 && (VS * int(sizeof(R))) % vb == 0) return vw;
-    }
-    return 1;
+    int best = 1;
+    if (A == 0 && GS == 1)
+        for (int vb = int(sizeof(R)) * 2; vb <= 16; vb *= 2) {
+            const int vw = vb / int(sizeof(R));
+            if (M % vw == 0 && (BLKP * int(sizeof(R))) % vb == 0 && (VS * int(sizeof(R))) % vb == 0) best = vw;
+        }
+    return best;
 }
 
 // Bank-conflict-free assignment of a sweep's lines to (iteration, thread).

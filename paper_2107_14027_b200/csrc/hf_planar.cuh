@@ -37,6 +37,17 @@ struct PlanarShape {
     static constexpr size_t SMEM = size_t(KS) * M * sizeof(R);
 };
 
+// Unrolling of the per-thread y loop (j): whole at low order, where the loop body is small
+// and the interleaved iterations hide latency; rolled from m = 5, where the unrolled body's
+// registers cap the resident warps (managed FP64, same box: p4 0.47 -> 0.59, p5 0.22 -> 0.34,
+// p6 0.11 -> 0.16 of the roofline rolled; p3 0.83 unrolled vs 0.76 rolled).
+template <int M>
+inline constexpr int kPlanarJUnroll = M <= 4 ? M : 1;
+// ... and of the unmanaged kernel's x loop (i): whole up to m = 3 (p1 FP64 0.76 rolled vs
+// 0.997 unrolled), rolled above (p3 FP64 0.22 -> 0.40, p5 0.10 -> 0.17).
+template <int M>
+inline constexpr int kPlanarIUnroll = M <= 3 ? M : 1;
+
 // Running accumulators per output row (codegen_util.hpp:149-161): first
 // contribution is a multiply, later ones fused multiply-adds.
 template <class R>
@@ -88,33 +99,36 @@ __global__ void __launch_bounds__(PlanarShape<R, M, NE>::BS)
 
     R* __restrict__ myplane = plane + KS * kp + el;
 
-#pragma unroll
+#pragma unroll(kPlanarIUnroll<M>)
     for (int i = 0; i < M; ++i) {
-        // plane slice: y-line (i, *, kp) -> registers + shared
-        R rY[M][NV];
+        // plane slice: y-line (i, *, kp) -> shared, and its y-line operands (P, V, the
+        // y-gradient column: 7 of the 13 rows) -> registers
+        R rY[M][7];
 #pragma unroll
         for (int j = 0; j < M; ++j)
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 const R x = act ? __ldg(ub + gofs(i, j, kp, v)) : R(0);
-                rY[j][v] = x;
+                if (v < 4) rY[j][v] = x;
+                else if ((v - 4) % 3 == 1) rY[j][4 + (v - 4) / 3] = x;
                 myplane[NE * (v + NV * j)] = x;
             }
         __syncthreads();
 
-#pragma unroll
+#pragma unroll(kPlanarJUnroll<M>)
         for (int j = 0; j < M; ++j) {
             R tx[13], ty[13], tz[13];
-            // x line from global (the i2 == i point from registers)
+            const R* __restrict__ own = myplane + NE * NV * j;  // this thread's point (i, j, kp)
+            // x line from global (the i2 == i point from the thread's own plane slice)
 #pragma unroll
             for (int i2 = 0; i2 < M; ++i2) {
                 R P, V[3], Gc[3];
                 if (i2 == i) {
-                    P = rY[j][0];
+                    P = own[0];
 #pragma unroll
                     for (int b = 0; b < 3; ++b) {
-                        V[b] = rY[j][1 + b];
-                        Gc[b] = rY[j][var_grad_c(3, b, 0)];
+                        V[b] = own[NE * (1 + b)];
+                        Gc[b] = own[NE * var_grad_c(3, b, 0)];
                     }
                 } else {
                     P = act ? __ldg(ub + gofs(i2, j, kp, 0)) : R(0);
@@ -130,8 +144,7 @@ __global__ void __launch_bounds__(PlanarShape<R, M, NE>::BS)
 #pragma unroll
             for (int j2 = 0; j2 < M; ++j2) {
                 const R V[3] = {rY[j2][1], rY[j2][2], rY[j2][3]};
-                const R Gc[3] = {rY[j2][var_grad_c(3, 0, 1)], rY[j2][var_grad_c(3, 1, 1)],
-                                 rY[j2][var_grad_c(3, 2, 1)]};
+                const R Gc[3] = {rY[j2][4], rY[j2][5], rY[j2][6]};
                 accumulate_column<R, 1>(ty, j2 == 0, p.D[j * M + j2], rY[j2][0], V, Gc, p);
             }
             // z line from the shared y-z plane (only P, V, z-gradient column: zcol_needs :225-228)
@@ -157,7 +170,7 @@ __global__ void __launch_bounds__(PlanarShape<R, M, NE>::BS)
                     if (hz) { r = have ? fma(p.jac[2], tz[v], r) : p.jac[2] * tz[v]; }
                     R o = -r;
                     if constexpr (SRC)
-                        if (v >= 4) o = fma(-p.invT, rY[j][v], o);
+                        if (v >= 4) o = fma(-p.invT, own[NE * v], o);
                     ob[gofs(i, j, kp, v)] = o;
                 }
             }
@@ -263,12 +276,17 @@ __global__ void __launch_bounds__(PlanarManagedShape<R, M, NE>::BS)
 
 #pragma unroll 1
     for (int i = 0; i < M; ++i) {
-        R rY[M][NV];  // plane slice: y-line (i, *, kp) (high-priority request, :118-131)
+        // plane slice: the y-line (i, *, kp) operands P, V and the y-gradient column
+        // (high-priority request, :118-131) -- 7 of the 13 rows
+        R rY[M][7];
 #pragma unroll
-        for (int j = 0; j < M; ++j)
+        for (int j = 0; j < M; ++j) {
 #pragma unroll
-            for (int v = 0; v < NV; ++v) rY[j][v] = s[sofs(i, j, kp, v)];
+            for (int v = 0; v < 4; ++v) rY[j][v] = s[sofs(i, j, kp, v)];
 #pragma unroll
+            for (int b = 0; b < 3; ++b) rY[j][4 + b] = s[sofs(i, j, kp, var_grad_c(3, b, 1))];
+        }
+#pragma unroll(kPlanarJUnroll<M>)
         for (int j = 0; j < M; ++j) {
             R tx[13], ty[13], tz[13];
 #pragma unroll
@@ -285,8 +303,7 @@ __global__ void __launch_bounds__(PlanarManagedShape<R, M, NE>::BS)
 #pragma unroll
             for (int j2 = 0; j2 < M; ++j2) {  // y line from registers
                 const R V[3] = {rY[j2][1], rY[j2][2], rY[j2][3]};
-                const R Gc[3] = {rY[j2][var_grad_c(3, 0, 1)], rY[j2][var_grad_c(3, 1, 1)],
-                                 rY[j2][var_grad_c(3, 2, 1)]};
+                const R Gc[3] = {rY[j2][4], rY[j2][5], rY[j2][6]};
                 accumulate_column<R, 1>(ty, j2 == 0, p.D[j * M + j2], rY[j2][0], V, Gc, p);
             }
 #pragma unroll
@@ -309,7 +326,7 @@ __global__ void __launch_bounds__(PlanarManagedShape<R, M, NE>::BS)
                     if (hz) { r = have ? fma(p.jac[2], tz[v], r) : p.jac[2] * tz[v]; }
                     R o = -r;
                     if constexpr (SRC)
-                        if (v >= 4) o = fma(-p.invT, rY[j][v], o);
+                        if (v >= 4) o = fma(-p.invT, s[sofs(i, j, kp, v)], o);
                     ob[gofs(i, j, kp, v)] = o;
                 }
             }
