@@ -23,7 +23,9 @@
 //      contracts the 1+d continuity/momentum lines, then d batches of d
 //      gradient lines S_ab V_c; partial sums of all n_v rows accumulate in a
 //      shared region (n_v words/pt);
-//   3. final pass: out = -acc/|J| (+ -g/T) written over the staged input, bulk store.
+//   3. the last sweep finishes each point: out = -acc/|J| (+ -g/T) over the staged
+//      input (|J| = row A of adj(J) . column A of J, the column constant along the line);
+//      bulk store.
 // HBM traffic stays n_v words in + n_v out per point plus 2^d d words per
 // element of geometry.
 #pragma once
@@ -262,16 +264,55 @@ __device__ __forceinline__ void mapped_contract(const Params<R>& p, const R (&Y)
     }
 }
 
+// The last sweep's contraction: the row's partial sum is complete at each point, so the
+// output -(acc + scale d) / |J| (+ the source of gradient rows) goes straight over the staged
+// input (this line's points, whose inputs the line has already read) -- no final pass.
+template <class R, int M, int NE, int STRIDE, int NROW, bool SRCROWS>
+__device__ __forceinline__ void mapped_contract_last(const Params<R>& p, const R (&Y)[NROW][M],
+                                                     const R* __restrict__ acc_line, R* __restrict__ s_line,
+                                                     const int (&rows)[NROW], R scale, const R (&inv)[M]) {
+    constexpr int NP_STRIDE = NE * STRIDE;
+    using PR = Pair<R>;
+    auto fin = [&](int row, int i, R dv) {
+        const int w = row + NP_STRIDE * i;
+        R o = -fma(scale, dv, acc_line[w]) * inv[i];
+        if constexpr (SRCROWS) o = fma(-p.invT, s_line[w], o);
+        s_line[w] = o;
+    };
+#pragma unroll
+    for (int r = 0; r < NROW; r += 2) {
+        if (r + 1 < NROW) {
+            PR y[M], d[M];
+#pragma unroll
+            for (int t = 0; t < M; ++t) y[t] = PR::make(Y[r][t], Y[r + 1][t]);
+            line_derivative<R, M>(p, y, d);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                fin(rows[r], i, d[i].x());
+                fin(rows[r + 1], i, d[i].y());
+            }
+        } else {
+            R y[M], d[M];
+#pragma unroll
+            for (int t = 0; t < M; ++t) y[t] = Y[r][t];
+            line_derivative<R, M>(p, y, d);
+#pragma unroll
+            for (int i = 0; i < M; ++i) fin(rows[r], i, d[i]);
+        }
+    }
+}
+
 // One sweep along axis A for the line whose first point is word `o` of the chunk.
-template <class R, int DIM, int M, int NE, int A>
-__device__ __forceinline__ void mapped_sweep(const R* __restrict__ s, R* __restrict__ acc, const R* __restrict__ geo,
+// LAST: the final sweep finishes the outputs in place (mapped_contract_last).
+template <class R, int DIM, int M, int NE, int A, bool LAST = false, bool SRC = false>
+__device__ __forceinline__ void mapped_sweep(R* __restrict__ s, R* __restrict__ acc, const R* __restrict__ geo,
                                              const Params<R>& p, int o) {
     constexpr int NP = ipow_c(M, DIM);
     constexpr int VS = NE * NP;  // word stride between variables (and metric entries)
     constexpr int STRIDE = (A == 0) ? 1 : (A == 1) ? M : M * M;
     constexpr int NV = n_vars_c(DIM);
     const bool first = (A == 0);
-    const R* sb = s + o;
+    R* sb = s + o;
     const int el = o % NE;
     const int bp = o / NE;  // the line's first point: its A index is 0
     R xi[3] = {p.xg[bp % M], p.xg[(bp / M) % M], DIM == 3 ? p.xg[bp / (M * M)] : R(0)};
@@ -282,6 +323,22 @@ __device__ __forceinline__ void mapped_sweep(const R* __restrict__ s, R* __restr
 #pragma unroll
         for (int t = 0; t < M; ++t) lm.row(p.xg[t], SL[t]);
     }
+    // LAST: 1/|J| along the line.  Column A of J does not depend on xi_A (the map is
+    // multilinear), and row A of adj(J) times column A of J is |J|.
+    R inv[LAST ? M : 1];
+    if constexpr (LAST) {
+        R JA[DIM];
+        mapped_jcol<R, DIM, NE>(geo, el, A, xi, JA);
+#pragma unroll
+        for (int t = 0; t < M; ++t) {
+            R det = SL[t][0] * JA[0];
+#pragma unroll
+            for (int b = 1; b < DIM; ++b) det = fma(SL[t][b], JA[b], det);
+            inv[t] = R(1) / det;
+        }
+    }
+    // LAST: the velocity rows of the line, read before batch 0 overwrites them
+    R VL[LAST ? M : 1][DIM];
 
     // batch 0: continuity + momentum rows
     {
@@ -293,6 +350,9 @@ __device__ __forceinline__ void mapped_sweep(const R* __restrict__ s, R* __restr
             R V[DIM];
 #pragma unroll
             for (int b = 0; b < DIM; ++b) V[b] = sb[q + VS * (1 + b)];
+            if constexpr (LAST)
+#pragma unroll
+                for (int b = 0; b < DIM; ++b) VL[t][b] = V[b];
             const R P = sb[q];
             R W = Sa[0] * V[0];
 #pragma unroll
@@ -309,7 +369,10 @@ __device__ __forceinline__ void mapped_sweep(const R* __restrict__ s, R* __restr
         int rows[1 + DIM];
 #pragma unroll
         for (int r = 0; r <= DIM; ++r) rows[r] = VS * r;
-        mapped_contract<R, M, NE, STRIDE, 1 + DIM>(p, Y, acc + o, rows, R(1), first);
+        if constexpr (LAST)
+            mapped_contract_last<R, M, NE, STRIDE, 1 + DIM, false>(p, Y, acc + o, sb, rows, R(1), inv);
+        else
+            mapped_contract<R, M, NE, STRIDE, 1 + DIM>(p, Y, acc + o, rows, R(1), first);
     }
     // batches 1..d: gradient rows g(c, b) <- D (S_ab V_c) * (-1/T)
 #pragma unroll
@@ -318,14 +381,19 @@ __device__ __forceinline__ void mapped_sweep(const R* __restrict__ s, R* __restr
 #pragma unroll
         for (int t = 0; t < M; ++t) {
             const int q = NE * STRIDE * t;
-            const R Vc = sb[q + VS * (1 + c)];
+            R Vc;
+            if constexpr (LAST) Vc = VL[t][c];
+            else Vc = sb[q + VS * (1 + c)];
 #pragma unroll
             for (int b = 0; b < DIM; ++b) Y[b][t] = SL[t][b] * Vc;
         }
         int rows[DIM];
 #pragma unroll
         for (int b = 0; b < DIM; ++b) rows[b] = VS * var_grad_c(DIM, c, b);
-        mapped_contract<R, M, NE, STRIDE, DIM>(p, Y, acc + o, rows, -p.invT, first);
+        if constexpr (LAST)
+            mapped_contract_last<R, M, NE, STRIDE, DIM, SRC>(p, Y, acc + o, sb, rows, -p.invT, inv);
+        else
+            mapped_contract<R, M, NE, STRIDE, DIM>(p, Y, acc + o, rows, -p.invT, first);
     }
     (void)NV;
 }
@@ -415,12 +483,13 @@ __global__ void __launch_bounds__(MappedShape<R, DIM, M, NE>::BS)
     R* s = reinterpret_cast<R*>(buf + head);
     auto sweep = [&](auto a_tag) {
         constexpr int A = decltype(a_tag)::value;
+        constexpr bool LAST = (A == DIM - 1);
         using LM = LineMap<R, DIM, M, NE, A, BS>;
         const unsigned short* map = kLineMap<R, DIM, M, NE, A, BS>.off;
 #pragma unroll 1
         for (int k = 0; k < LM::ITERS; ++k) {
             const int o = map[k * BS + tid];
-            if (o != 0xFFFF) mapped_sweep<R, DIM, M, NE, A>(s, acc, geo, p, o);
+            if (o != 0xFFFF) mapped_sweep<R, DIM, M, NE, A, LAST, SRC>(s, acc, geo, p, o);
         }
     };
     sweep(std::integral_constant<int, 0>{});
@@ -429,29 +498,6 @@ __global__ void __launch_bounds__(MappedShape<R, DIM, M, NE>::BS)
     if constexpr (DIM == 3) {
         __syncthreads();
         sweep(std::integral_constant<int, 2>{});
-    }
-    __syncthreads();
-
-    // ---------------- out = -acc / |J| (+ source), over the staged input ----------------
-    for (int idx = tid; idx < NE * NP; idx += BS) {
-        const int el = idx % NE;
-        const int pt = idx / NE;
-        const R xi[3] = {p.xg[pt % M], p.xg[(pt / M) % M], DIM == 3 ? p.xg[pt / (M * M)] : R(0)};
-        R J[DIM * DIM], col[DIM], Sm[DIM * DIM];
-#pragma unroll
-        for (int j = 0; j < DIM; ++j) {
-            mapped_jcol<R, DIM, NE>(geo, el, j, xi, col);
-#pragma unroll
-            for (int i = 0; i < DIM; ++i) J[i * DIM + j] = col[i];
-        }
-        const R inv = R(1) / mapped_adjugate<R, DIM>(J, Sm);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            R o = -acc[idx + VS * v] * inv;
-            if constexpr (SRC)
-                if (v >= 1 + DIM) o = fma(-p.invT, s[idx + VS * v], o);
-            s[idx + VS * v] = o;
-        }
     }
 
     // ---------------- write the finished chunk ----------------
