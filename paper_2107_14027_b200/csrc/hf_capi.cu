@@ -356,6 +356,20 @@ int lines_variant_for_group(const hf_problem* pr, int variant, const hfb::Params
             consider(v, fill * (row >= 64 ? 1.0 : row >= 32 ? 0.9 : 0.53) * occupancy(ne));
         }
     }
+    // the tile ring (variant 24, built at d3 p5): 2 NE0 elements in a two-stage TMA ring, so
+    // chunk loads and stores overlap the sweeps although the chunk leaves one CTA per SM
+    if (!faces && available(hfb::kTileRingVariant)) {
+        const int ne = hfb::variant_ne_of(ne0, hfb::kTileRingVariant);
+        if (G == ne) {
+            consider(hfb::kTileRingVariant, 1.0);
+        } else if ((int64_t(G) * w) % 16 == 0 && (ne * w) % 16 == 0 && G % ne == 0) {
+            // whole sub-chunks only: with a short last sub-chunk per group (G = 12, 20 at NE = 8)
+            // the ring measured 0.40-0.43 against 0.53 for the one-chunk NE0 tile
+            // (profiles/r02/tile_ring/groups_p5.jsonl)
+            const int row = ne * w;
+            consider(hfb::kTileRingVariant, row >= 64 ? 1.0 : row >= 32 ? 0.9 : 0.53);
+        }
+    }
     if (best >= 0) return best;
     // guarded path (a group that is not a 16-byte stride and no chunk size): every staged word
     // is one cp.async copy, so the contiguous run per row (min(NE, G) words) and the resident

@@ -14,8 +14,9 @@ int lines_variant_f(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info
     if constexpr (is_pipe_variant<VARIANT>()) {
         constexpr int ST = pipe_stages<VARIANT>();
         constexpr int GR = pipe_groups<VARIANT>();
-        return src ? int(launch_lines_pipe<R, DIM, M, NE, ST, GR, true, FACES, CS>(prm, st, info, dry))
-                   : int(launch_lines_pipe<R, DIM, M, NE, ST, GR, false, FACES, CS>(prm, st, info, dry));
+        constexpr bool TL = VARIANT == kTileRingVariant;
+        return src ? int(launch_lines_pipe<R, DIM, M, NE, ST, GR, true, FACES, CS, TL>(prm, st, info, dry))
+                   : int(launch_lines_pipe<R, DIM, M, NE, ST, GR, false, FACES, CS, TL>(prm, st, info, dry));
     } else {
         constexpr int LPT = lines_per_thread<VARIANT>();
         return src ? int(launch_lines<R, DIM, M, NE, true, LPT, FACES, NE, CS>(prm, st, info, dry))
@@ -32,7 +33,8 @@ int lines_variant(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info, 
         return kUnsupported;
     } else if constexpr (is_pipe_variant<VARIANT>() &&
                          (PipeShape<R, DIM, M, NE, pipe_stages<VARIANT>(), pipe_groups<VARIANT>(),
-                                    is_cs_variant(VARIANT)>::SMEM > size_t(kMaxSmemPerCta) ||
+                                    is_cs_variant(VARIANT), VARIANT == kTileRingVariant>::SMEM >
+                              size_t(kMaxSmemPerCta) ||
                           PipeShape<R, DIM, M, NE, pipe_stages<VARIANT>(), pipe_groups<VARIANT>(),
                                     is_cs_variant(VARIANT)>::BS > 1024)) {
         return kUnsupported;
@@ -241,7 +243,7 @@ int run_unfused_impl(int d, int p, bool src, const Params<R>& prm, cudaStream_t 
     }
 }
 
-// Entry points defined in the instantiation units (lines: variants 0-9 in *_lo, 10-15 in *_hi).
+// Entry points defined in the instantiation units (lines: variants 0-9 in *_lo, 10-24 in *_hi).
 #define HF_LINES_DECL(NAME, R)                                                                        \
     int NAME##_lo(int p, int variant, bool src, const Params<R>&, cudaStream_t, KInfo*, bool, bool);   \
     int NAME##_hi(int p, int variant, bool src, const Params<R>&, cudaStream_t, KInfo*, bool, bool);   \

@@ -73,8 +73,9 @@ constexpr int lines_ne_default() {
 // The contiguous bulk path accepts any NE >= 1 (hf_chunk_io.cuh), so the small-NE
 // variants exist for every order; a variant whose shape does not fit (shared
 // memory, 1024 threads) reports unsupported.
-constexpr int kLinesVariants = 24;
+constexpr int kLinesVariants = 25;
 constexpr bool is_cs_variant(int v) { return v >= 19 && v <= 23; }
+constexpr int kTileRingVariant = 24;  // TMA ring, 2 NE0 elements, 2 stages, 1 group, tile mode
 
 // The measured selection (tools/select_methods.py -> hf_select_table.inc).
 struct SelRow {
@@ -123,6 +124,9 @@ constexpr bool variant_built() {
     return true;
 #else
     if (is_one_chunk_variant(VARIANT) || VARIANT == 3 || VARIANT == 10) return true;
+    // the tile ring (2 NE0 elements, 2 stages): caller groups of >= 32-byte rows at d3 p5,
+    // where the one-chunk kernel of that chunk fits one CTA per SM (lines_variant_for_group)
+    if (VARIANT == kTileRingVariant) return DIM == 3 && M == 6;
     for (const SelRow& r : kSelect)
         if (r.d == DIM && r.p == M - 1 && r.prec == (sizeof(R) == 8 ? 1 : 0) && r.method == 2 && r.variant == VARIANT)
             return true;
@@ -136,7 +140,7 @@ constexpr bool is_pipe_variant() {
 constexpr int variant_ne_of(int ne0, int v) {
     const int ne = (v == 0 || v == 3 || v == 6 || v == 14 || v == 19 || v == 23)     ? ne0
                    : (v == 1 || v == 4 || v == 5 || v == 10 || v == 11 || v == 20)  ? ne0 / 2
-                   : (v == 2 || v == 16 || v == 21)                                 ? ne0 * 2
+                   : (v == 2 || v == 16 || v == 21 || v == 24)                      ? ne0 * 2
                    : (v == 17)                                                      ? ne0
                    : (v == 18)                                                      ? ne0 * 4
                                                                                     : ne0 / 4;
@@ -365,16 +369,31 @@ inline int num_sms() {
 }
 
 // Persistent pipelined lines kernel over the whole chunks, guarded tail through hf_lines_kernel.
-template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES = false, bool CS = false>
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES = false, bool CS = false,
+          bool TILE = false>
 cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
-    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS, CS>;
+    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS, CS, TILE>;
     using L = LinesShape<R, DIM, M, NE, 1, NE, CS>;
-    auto kernel = hf_lines_pipe_kernel<R, DIM, M, NE, STAGES, GROUPS, SRC, FACES, CS>;
-    const bool fast_layout = bulk_layout<R, NE>(p.group);
+    auto kernel = hf_lines_pipe_kernel<R, DIM, M, NE, STAGES, GROUPS, SRC, FACES, CS, TILE>;
+    // TILE ring: a group that is not the chunk goes through TMA tensor copies (tile_layout)
+    const bool tile = TILE && !FACES && tile_layout<R, NE>(p.group) &&
+                      (p.u == nullptr || (aligned16(p.u) && aligned16(p.out)));
+    const bool fast_layout = tile || bulk_layout<R, NE>(p.group);
+    const int sub = (p.group + NE - 1) / NE;
+    const long long n_groups = (p.n_elem + p.group - 1) / p.group;
     long long n_full = p.n_elem / NE;
+    long long n_chunks = (p.n_elem + NE - 1) / NE;
+    if (tile) {
+        // sub-chunks wholly inside n_elem: every one of the whole groups, and the leading ones
+        // of a partial last group; the rest (guarded) go to the tail launch
+        const long long whole = p.n_elem / p.group;
+        n_full = whole * sub + (p.n_elem - whole * p.group) / NE;
+        n_chunks = n_groups * sub;
+    }
     // contiguous chunks load a 16-byte superset: keep the allocation's last chunk
     // (whose superset could run past the end) for the guarded tail launch
-    if (p.group == NE && n_full > 0 && n_full * NE == p.n_elem && (p.total_words * (long long)sizeof(R)) % 16 != 0)
+    if (!tile && p.group == NE && n_full > 0 && n_full * NE == p.n_elem &&
+        (p.total_words * (long long)sizeof(R)) % 16 != 0)
         n_full -= 1;
     // resident CTAs per SM: measured once per device (thread-safe: atomics), the
     // shared-memory attribute set on every launch (it is per device)
@@ -409,8 +428,8 @@ cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dr
         info->grid = grid;
         info->bulk_path = fast_layout ? 1 : 0;
         if (GROUPS == 1)
-            std::snprintf(info->name, sizeof(info->name), "hf_lines_pipe_d%d_p%d_%s_ne%d_s%d%s%s", DIM, M - 1,
-                          prec_name(sizeof(R)), NE, STAGES, CS ? "_cs" : "", SRC ? "_src" : "");
+            std::snprintf(info->name, sizeof(info->name), "hf_lines_pipe_d%d_p%d_%s_ne%d_s%d%s%s%s", DIM, M - 1,
+                          prec_name(sizeof(R)), NE, STAGES, CS ? "_cs" : "", tile ? "_tile" : "", SRC ? "_src" : "");
         else
             std::snprintf(info->name, sizeof(info->name), "hf_lines_pipe_d%d_p%d_%s_ne%d_s%d_g%d%s", DIM, M - 1,
                           prec_name(sizeof(R)), NE, STAGES, GROUPS, SRC ? "_src" : "");
@@ -418,12 +437,18 @@ cudaError_t launch_lines_pipe(Params<R> p, cudaStream_t st, KInfo* info, bool dr
     }
     if (dry || p.n_elem == 0) return cudaSuccess;
     p.fast_ok = fast_layout && aligned16(p.u) && aligned16(p.out);
+    if (tile && p.fast_ok) {
+        p.tile = 1;
+        p.sub_per_group = sub;
+        if (!encode_chunk_map<R>(&p.tm_u, p.u, DIM, M, p.group, n_groups, NE) ||
+            !encode_chunk_map<R>(&p.tm_out, p.out, DIM, M, p.group, n_groups, NE))
+            p.fast_ok = 0;
+    }
     if (!p.fast_ok || n_full == 0) return launch_lines<R, DIM, M, NE, SRC, 1, FACES, NE, CS>(p, st, nullptr, false);
     p.chunk0 = 0;
     p.n_chunks = n_full;
     cudaError_t e = launch_kernel(kernel, dim3(unsigned(grid)), dim3(S::BS), S::SMEM, st, p);
     if (e != cudaSuccess) return e;
-    const long long n_chunks = (p.n_elem + NE - 1) / NE;
     if (n_full < n_chunks) {  // the partial (or allocation-final) chunk(s)
         auto tail = hf_lines_kernel<R, DIM, M, NE, SRC, 1, FACES, NE, CS>;
         if (int e2 = set_smem_attr(tail, L::SMEM)) return cudaError_t(e2);

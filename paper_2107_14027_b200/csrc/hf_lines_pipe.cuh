@@ -27,7 +27,8 @@
 //
 // One CTA per SM slot, chunks assigned round-robin (all chunks cost the same).
 // Only whole chunks inside one AoSoA group run here (group % NE == 0, 16-byte
-// rows, or group == NE); the guarded tail goes through hf_lines_kernel with
+// rows, or group == NE; with TILE also any 16-byte-stride group through one TMA
+// tensor copy per chunk); the guarded tail goes through hf_lines_kernel with
 // chunk0 = n_chunks.
 #pragma once
 
@@ -35,7 +36,10 @@
 
 namespace hfb {
 
-template <class R, int DIM, int M, int NE, int STAGES, int GROUPS = 1, bool CS = false>
+// TILE: the ring may run tile mode (p.tile: the caller's AoSoA group is not the chunk; one
+// TMA tensor copy per chunk and direction, as hf_lines_kernel's tile mode), so every stage
+// starts 128-byte aligned (the tensor copy's shared-memory destination).
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS = 1, bool CS = false, bool TILE = false>
 struct PipeShape {
     using L = LinesShape<R, DIM, M, NE>;
     static_assert(STAGES % GROUPS == 0, "every group owns STAGES / GROUPS stages");
@@ -44,7 +48,7 @@ struct PipeShape {
     static constexpr int NCONS = CS ? DIM * NT : NT;          // consumer threads per group (CS: one per component)
     static constexpr int BS = GROUPS * NCONS + 32;            // + producer warp
     static constexpr int HDR = 256;                           // 2*STAGES mbarriers (<= 32)
-    static constexpr size_t STAGE_BYTES = size_t(L::BUF_BYTES);
+    static constexpr size_t STAGE_BYTES = TILE ? (size_t(L::BUF_BYTES) + 127) / 128 * 128 : size_t(L::BUF_BYTES);
     static constexpr size_t ACC_BYTES = ((size_t(L::ACC_WORDS) * sizeof(R) + 127) / 128) * 128;
     static constexpr size_t SMEM = HDR + STAGES * STAGE_BYTES + GROUPS * ACC_BYTES;
     static_assert(2 * STAGES * 8 <= HDR, "mbarrier header too small");
@@ -56,11 +60,12 @@ struct PipeShape {
 // accumulator region) is a runtime offset from the __shared__ window, so every
 // group runs the same code -- one copy of the sweeps per stage, not per
 // (group, stage), which keeps the kernel inside the instruction cache.
-template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES, bool CS = false>
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES, bool CS = false,
+          bool TILE = false>
 __device__ __forceinline__ void pipe_consume(unsigned char* smem_raw, uint64_t* full, uint64_t* computed,
                                              const Params<R>& p, long long count, long long first, long long step,
                                              int g, int ct) {
-    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS, CS>;
+    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS, CS, TILE>;
     using L = LinesShape<R, DIM, M, NE>;
     using IO = typename L::IO;
     constexpr int SPG = S::SPG;
@@ -74,17 +79,22 @@ __device__ __forceinline__ void pipe_consume(unsigned char* smem_raw, uint64_t* 
             const long long it = g + (q0 + j) * GROUPS;
             if (it >= count) break;
             const int s = g * SPG + j;
-            const long long E0 = (first + it * step) * NE;
-            const long long grp = E0 / p.group;
-            const long long cb = grp * p.group_words + (E0 - grp * p.group);
+            long long E0 = (first + it * step) * NE;
+            int head = 0;
+            if (TILE && p.tile) {  // sub-chunk b % sub of group b / sub: the box lands at offset 0
+                const long long b = first + it * step;
+                const long long grp = b / p.sub_per_group;
+                E0 = grp * p.group + (b - grp * p.sub_per_group) * NE;
+            } else {
+                const long long grp = E0 / p.group;
+                head = IO::head_bytes(p.u + grp * p.group_words + (E0 - grp * p.group), contiguous);
+            }
             unsigned char* buf = gbuf + size_t(j) * S::STAGE_BYTES;
             mbar_wait_parity(&full[s], ph);
             if constexpr (GROUPS == 1)
-                lines_sweeps_at<R, DIM, M, NE, SRC, 1, S::NT, FACES, NE, CS>(
-                    buf, IO::head_bytes(p.u + cb, contiguous), acc, p, ct, 0, E0);
+                lines_sweeps_at<R, DIM, M, NE, SRC, 1, S::NT, FACES, NE, CS>(buf, head, acc, p, ct, 0, E0);
             else
-                lines_sweeps_at<R, DIM, M, NE, SRC, -1, S::NT, FACES, NE, CS>(
-                    buf, IO::head_bytes(p.u + cb, contiguous), acc, p, ct, 1 + g, E0);
+                lines_sweeps_at<R, DIM, M, NE, SRC, -1, S::NT, FACES, NE, CS>(buf, head, acc, p, ct, 1 + g, E0);
             fence_proxy_async_smem();
             named_bar_sync(1 + g, S::NCONS);
             if (ct == 0) mbar_arrive(&computed[s]);
@@ -92,11 +102,12 @@ __device__ __forceinline__ void pipe_consume(unsigned char* smem_raw, uint64_t* 
     }
 }
 
-template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES = false, bool CS = false>
-__global__ void __launch_bounds__(PipeShape<R, DIM, M, NE, STAGES, GROUPS, CS>::BS)
+template <class R, int DIM, int M, int NE, int STAGES, int GROUPS, bool SRC, bool FACES = false, bool CS = false,
+          bool TILE = false>
+__global__ void __launch_bounds__(PipeShape<R, DIM, M, NE, STAGES, GROUPS, CS, TILE>::BS)
     hf_lines_pipe_kernel(const __grid_constant__ Params<R> p) {
     using L = LinesShape<R, DIM, M, NE>;
-    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS, CS>;
+    using S = PipeShape<R, DIM, M, NE, STAGES, GROUPS, CS, TILE>;
     constexpr int SPG = S::SPG;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -133,6 +144,46 @@ __global__ void __launch_bounds__(PipeShape<R, DIM, M, NE, STAGES, GROUPS, CS>::
 
     if (warp == 0) {
         // ---------------- producer ----------------
+        if (TILE && p.tile) {
+            // tile mode: chunk b = sub-chunk b % sub of group b / sub, one TMA tensor copy per
+            // direction issued by lane 0 (the box {NE, m, m^(d-1), n_v, 1}; elements past the
+            // group's end zero-filled on load, clipped on store)
+            if (lane == 0) {
+                tma_prefetch_desc(&p.tm_u);
+                tma_prefetch_desc(&p.tm_out);
+                auto coords = [&](long long it, int& c0, int& c4) {
+                    const long long b = first + it * step;
+                    const long long grp = b / p.sub_per_group;
+                    c0 = static_cast<int>(b - grp * p.sub_per_group) * NE;
+                    c4 = static_cast<int>(grp);
+                };
+                const long long pre = count < STAGES ? count : STAGES;
+                for (long long it = 0; it < pre; ++it) {
+                    const int s = stage_of(it);
+                    int c0, c4;
+                    coords(it, c0, c4);
+                    mbar_arrive_expect_tx(&full[s], uint32_t(L::IN_BYTES));
+                    tma_load_5d(stage0 + size_t(s) * S::STAGE_BYTES, &p.tm_u, c0, 0, 0, 0, c4, &full[s]);
+                }
+                for (long long it = 0; it < count; ++it) {
+                    const int s = stage_of(it);
+                    unsigned char* buf = stage0 + size_t(s) * S::STAGE_BYTES;
+                    mbar_wait_parity(&computed[s], uint32_t((it / STAGES) & 1));
+                    int c0, c4;
+                    coords(it, c0, c4);
+                    tma_store_5d(&p.tm_out, c0, 0, 0, 0, c4, buf);
+                    bulk_commit();
+                    if (it + STAGES < count) {
+                        bulk_wait_read_all();  // the box has left shared memory
+                        coords(it + STAGES, c0, c4);
+                        mbar_arrive_expect_tx(&full[s], uint32_t(L::IN_BYTES));
+                        tma_load_5d(buf, &p.tm_u, c0, 0, 0, 0, c4, &full[s]);
+                    }
+                }
+                bulk_wait_read_all();
+            }
+            return;
+        }
         const long long pre = count < STAGES ? count : STAGES;
         for (long long it = 0; it < pre; ++it) {
             const int s = stage_of(it);
@@ -163,8 +214,8 @@ __global__ void __launch_bounds__(PipeShape<R, DIM, M, NE, STAGES, GROUPS, CS>::
     // ---------------- consumer groups ----------------
     const int g = (tid - 32) / S::NCONS;
     const int ct = (tid - 32) - g * S::NCONS;
-    pipe_consume<R, DIM, M, NE, STAGES, GROUPS, SRC, FACES, CS>(smem_raw, full, computed, p, count, first, step, g,
-                                                                ct);
+    pipe_consume<R, DIM, M, NE, STAGES, GROUPS, SRC, FACES, CS, TILE>(smem_raw, full, computed, p, count, first,
+                                                                      step, g, ct);
 }
 
 }  // namespace hfb

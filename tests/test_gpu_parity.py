@@ -72,7 +72,7 @@ def test_lines_misaligned_pointer(cuda):
     check_parity(3, 2, 64, 16, False, U, method=Method.lines, offset_bytes=8)
 
 
-@pytest.mark.parametrize("variant", list(range(24)))
+@pytest.mark.parametrize("variant", list(range(25)))
 @pytest.mark.parametrize("d,p,fp32", [(3, 1, True), (3, 3, False), (3, 4, True), (3, 6, False), (3, 6, True),
                                       (2, 3, True), (2, 8, True)])
 def test_lines_variants(cuda, d, p, fp32, variant):
@@ -285,6 +285,27 @@ def test_caller_groups_d3(cuda, p, fp32):
     pr = hf.make_problem(3, p, 100, 40, Precision.fp32 if fp32 else Precision.fp64, PAR)
     name = hf.kernel_info(pr)["name"]
     assert "_tile" in name or "ne40" in name, name
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+def test_tile_ring_caller_groups_d3_p5(cuda, fp32):
+    """The tile ring (lines variant 24: two-stage TMA ring, one tensor copy per chunk and
+    direction) with several chunks per CTA -- the ring's refill path -- for whole groups and a
+    partial last group; forced on groups that leave the last sub-chunk of every group short
+    (12, 20: zero-filled and clipped by the tensor maps)."""
+    import paper_2107_14027_b200 as hf
+    from paper_2107_14027_b200 import Precision
+    prec = Precision.fp32 if fp32 else Precision.fp64
+    for gi, g in enumerate((8, 16, 32, 64, 4 if not fp32 else 8)):
+        n = (3 * 148 * 8 // g) * g + g // 2 + 3
+        pr = hf.make_problem(3, 5, n, g, prec, PAR)
+        assert hf.kernel_info(pr)["name"].startswith("hf_lines_pipe_d3_p5"), hf.kernel_info(pr)["name"]
+        U = _field(3, 5, n, g, fp32, 7000 + gi)
+        check_parity(3, 5, n, g, fp32, U, with_source=(gi % 2 == 1))
+    for gi, g in enumerate((12, 20)):
+        n = (3 * 148 * 8 // g) * g + 5
+        U = _field(3, 5, n, g, fp32, 7100 + gi)
+        check_parity(3, 5, n, g, fp32, U, method=Method.lines, variant=24, with_source=(gi == 0))
 
 
 @pytest.mark.parametrize("p", [1, 3, 5, 8])

@@ -134,7 +134,7 @@ def main():
         pmax = 7 if d == 3 else 8
         for prec in (Precision.fp32, Precision.fp64):
             for p in ([int(x) for x in args.ps.split(",")] if args.ps else range(1, pmax + 1)):
-                vs = [int(x) for x in args.variants.split(",")] if args.variants else range(24)
+                vs = [int(x) for x in args.variants.split(",")] if args.variants else range(25)
                 cands = [(Method.lines, v) for v in vs]
                 if d == 3 and not args.no_planar:
                     cands.append((Method.planar, 0))
