@@ -3,7 +3,7 @@
 # the reference arm, the ncu launch list of the default bench (per-launch time + DRAM bytes), one ncu
 # --set full capture of the dominant kernel.
 set -o pipefail
-O=gpurun_out/bench_r02; mkdir -p $O
+O=gpurun_out/${OUT:-bench_r02}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/gpu.txt
 timeout 1500 python -m pytest tests -q -m gpu -x > $O/pytest.log 2>&1; echo "pytest rc=$?"; tail -1 $O/pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"
