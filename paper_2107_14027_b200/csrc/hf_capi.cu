@@ -839,6 +839,16 @@ int ctx_reserve(hf_context* c, size_t bytes) {
     return HF_OK;
 }
 
+// Base slice of the host path: 48 MB (HF_HOST_SLICE_MB overrides it, for tools/host_probe.py).
+int64_t host_slice_bytes() {
+    static const int64_t b = [] {
+        const char* v = std::getenv("HF_HOST_SLICE_MB");
+        const long mb = v ? std::atol(v) : 0;
+        return int64_t(mb > 0 ? mb : 48) << 20;
+    }();
+    return b;
+}
+
 bool is_pinned(const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -936,7 +946,7 @@ int hf_fused_divergence_host_batch(hf_context* c, int n_fields, const hf_problem
         if (pref < 1) pref = 1;
         const int64_t chunk_groups = std::max<int64_t>(1, (pref + pr->group - 1) / pr->group);
         auto rnd = [&](int64_t x) { return std::max<int64_t>(chunk_groups, x / chunk_groups * chunk_groups); };
-        const int64_t base = std::min<int64_t>(rnd((int64_t(48) << 20) / int64_t(gw * w)), n_groups);
+        const int64_t base = std::min<int64_t>(rnd(host_slice_bytes() / int64_t(gw * w)), n_groups);
         const bool up = plan.empty();
         bool down = true;  // the last field with elements ramps down
         for (int k = i + 1; k < n_fields; ++k) down = down && prs[k].n_elem == 0;
