@@ -52,13 +52,17 @@ def mangled(info, d, p, prec, src=False):
         st = int(re.search(r"_s(\d+)", name).group(1))
         gr = re.search(r"_s\d+_g(\d+)", name)
         gr = int(gr.group(1)) if gr else 1
-        return f"_ZN3hfb20hf_lines_pipe_kernelI{R}Li{d}ELi{m}ELi{ne}ELi{st}ELi{gr}ELb{b}ELb0EEEvNS_6ParamsIT_EE"
+        cs = "1" if "_cs" in name else "0"
+        tile = "1" if "_tile" in name else "0"  # variant 24 (the tile ring) is never a selected kernel
+        return (f"_ZN3hfb20hf_lines_pipe_kernelI{R}Li{d}ELi{m}ELi{ne}ELi{st}ELi{gr}ELb{b}ELb0ELb{cs}ELb{tile}"
+                "EEEvNS_6ParamsIT_EE")
     if name.startswith("hf_lines"):
         lpt = re.search(r"_l(\d+)", name)
         lpt = int(lpt.group(1)) if lpt else 1
         gs = re.search(r"_g(\d+)", name)
         gs = int(gs.group(1)) if gs else ne
-        return f"_ZN3hfb15hf_lines_kernelI{R}Li{d}ELi{m}ELi{ne}ELb{b}ELi{lpt}ELb0ELi{gs}EEEvNS_6ParamsIT_EE"
+        cs = "1" if "_cs" in name else "0"
+        return f"_ZN3hfb15hf_lines_kernelI{R}Li{d}ELi{m}ELi{ne}ELb{b}ELi{lpt}ELb0ELi{gs}ELb{cs}EEEvNS_6ParamsIT_EE"
     if name.startswith("hf_planar_managed"):
         return f"_ZN3hfb24hf_planar_managed_kernelI{R}Li{m}ELi{ne}ELb{b}EEEvNS_6ParamsIT_EE"
     if name.startswith("hf_planar"):
