@@ -48,6 +48,15 @@ inline constexpr int kPlanarJUnroll = M <= 4 ? M : 1;
 template <int M>
 inline constexpr int kPlanarIUnroll = M <= 3 ? M : 1;
 
+// Resident CTAs the unmanaged planar kernel is compiled for (__launch_bounds__ min blocks):
+// registers capped near 128 per thread at p1-p3 (FP64 from p2) -- fully unrolled, the
+// kernel takes 236-255 and runs 2 CTAs per SM.  Same box, 1e7 points (planar_ab/): FP32 p1
+// 0.73 -> 0.79, p2 0.45 -> 0.51, p3 0.20 -> 0.29; FP64 p2 0.64 -> 0.74, p3 0.39 -> 0.41;
+// FP64 p1 126 registers either way; a 96-register cap spills.
+// (0 from p4: no constraint, the compiler's own register choice.)
+template <class R, int M, int BS>
+inline constexpr int kPlanarMinBlocks = M <= 4 ? (65536 / (128 * BS) > 1 ? 65536 / (128 * BS) : 1) : 0;
+
 // Running accumulators per output row (codegen_util.hpp:149-161): first
 // contribution is a multiply, later ones fused multiply-adds.
 template <class R>
@@ -73,7 +82,7 @@ __device__ __forceinline__ void accumulate_column(R (&acc)[13], bool first, R co
 }
 
 template <class R, int M, int NE, bool SRC>
-__global__ void __launch_bounds__(PlanarShape<R, M, NE>::BS)
+__global__ void __launch_bounds__(PlanarShape<R, M, NE>::BS, kPlanarMinBlocks<R, M, PlanarShape<R, M, NE>::BS>)
     hf_planar_kernel(const __grid_constant__ Params<R> p) {
     using S = PlanarShape<R, M, NE>;
     constexpr int NP = S::NP, NV = S::NV, KS = S::KS;
