@@ -53,6 +53,9 @@ struct Params {
     // per direction over the 5-d view {e_l, i, (j,k), v, group} of the AoSoA field.
     int tile;
     int sub_per_group;        // ceil(group / NE)
+    // Padded chunks (lines variants 25-27): tm_u / tm_out hold the 4-d view {x-row, rows, v,
+    // group} of a field whose group is the chunk, with a box one pad wider than the row.
+    int xpad;
     CUtensorMap tm_u;         // 64-byte aligned descriptors, read from the parameter space
     CUtensorMap tm_out;
 };
@@ -156,6 +159,23 @@ __device__ __forceinline__ void tma_load_5d(void* dst_smem, const CUtensorMap* t
         "%6}], [%7];" ::"r"(smem_u32(dst_smem)),
         "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
         : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst_smem, const CUtensorMap* tmap, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_u32(dst_smem)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* tmap, int c0, int c1, int c2, int c3,
+                                             const void* src_smem) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src_smem))
+                 : "memory");
 }
 
 __device__ __forceinline__ void tma_store_5d(const CUtensorMap* tmap, int c0, int c1, int c2, int c3, int c4,

@@ -19,8 +19,9 @@ int lines_variant_f(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info
                    : int(launch_lines_pipe<R, DIM, M, NE, ST, GR, false, FACES, CS, TL>(prm, st, info, dry));
     } else {
         constexpr int LPT = lines_per_thread<VARIANT>();
-        return src ? int(launch_lines<R, DIM, M, NE, true, LPT, FACES, NE, CS>(prm, st, info, dry))
-                   : int(launch_lines<R, DIM, M, NE, false, LPT, FACES, NE, CS>(prm, st, info, dry));
+        constexpr int XP = is_xpad_variant(VARIANT) ? xpad_words<R, DIM, M, NE>() : 0;
+        return src ? int(launch_lines<R, DIM, M, NE, true, LPT, FACES, NE, CS, XP>(prm, st, info, dry))
+                   : int(launch_lines<R, DIM, M, NE, false, LPT, FACES, NE, CS, XP>(prm, st, info, dry));
     }
 }
 
@@ -243,7 +244,7 @@ int run_unfused_impl(int d, int p, bool src, const Params<R>& prm, cudaStream_t 
     }
 }
 
-// Entry points defined in the instantiation units (lines: variants 0-9 in *_lo, 10-24 in *_hi).
+// Entry points defined in the instantiation units (lines: variants 0-9 in *_lo, 10-27 in *_hi).
 #define HF_LINES_DECL(NAME, R)                                                                        \
     int NAME##_lo(int p, int variant, bool src, const Params<R>&, cudaStream_t, KInfo*, bool, bool);   \
     int NAME##_hi(int p, int variant, bool src, const Params<R>&, cudaStream_t, KInfo*, bool, bool);   \

@@ -606,6 +606,7 @@ constexpr int fr_fused_variant() {
             if (r.variant == 20) return 1;
             if (r.variant == 21) return 2;
             if (r.variant == 22) return 7;
+            if (is_xpad_variant(r.variant)) return xpad_base_variant(r.variant);
         }
     return 0;
 }

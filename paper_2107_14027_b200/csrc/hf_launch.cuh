@@ -73,9 +73,14 @@ constexpr int lines_ne_default() {
 // The contiguous bulk path accepts any NE >= 1 (hf_chunk_io.cuh), so the small-NE
 // variants exist for every order; a variant whose shape does not fit (shared
 // memory, 1024 threads) reports unsupported.
-constexpr int kLinesVariants = 25;
+constexpr int kLinesVariants = 28;
 constexpr bool is_cs_variant(int v) { return v >= 19 && v <= 23; }
 constexpr int kTileRingVariant = 24;  // TMA ring, 2 NE0 elements, 2 stages, 1 group, tile mode
+// 25 / 26 / 27: one chunk per CTA of NE0/4, NE0/2, NE0 elements staged with padded x-rows
+// (LinesShape XP, xpad_words): the chunk layout of variants 7 / 1 / 0 with a row stride
+// that spreads the x-lines and accumulator lines over the banks.
+constexpr bool is_xpad_variant(int v) { return v >= 25 && v <= 27; }
+constexpr int xpad_base_variant(int v) { return v == 25 ? 7 : v == 26 ? 1 : v == 27 ? 0 : v; }
 
 // The measured selection (tools/select_methods.py -> hf_select_table.inc).
 struct SelRow {
@@ -100,6 +105,7 @@ constexpr int faces_variant_override(int d, int p) { return (d == 3 && p == 6) ?
 // The FACES (fused FR stage 1) form: the selected variant of each configuration.
 template <class R, int DIM, int M, int VARIANT>
 constexpr bool variant_faces_built() {
+    if (is_xpad_variant(VARIANT)) return false;  // FR stage 1 rides on the unpadded chunk (xpad_base_variant)
 #ifdef HF_TUNING
     return VARIANT == 0 || VARIANT == 3;
 #else
@@ -127,6 +133,8 @@ constexpr bool variant_built() {
     // the tile ring (2 NE0 elements, 2 stages): caller groups of >= 32-byte rows at d3 p5,
     // where the one-chunk kernel of that chunk fits one CTA per SM (lines_variant_for_group)
     if (VARIANT == kTileRingVariant) return DIM == 3 && M == 6;
+    // the padded one-chunk variants: all three at d3 p3 (parity coverage), else where selected
+    if (is_xpad_variant(VARIANT) && DIM == 3 && M == 4) return true;
     for (const SelRow& r : kSelect)
         if (r.d == DIM && r.p == M - 1 && r.prec == (sizeof(R) == 8 ? 1 : 0) && r.method == 2 && r.variant == VARIANT)
             return true;
@@ -135,11 +143,12 @@ constexpr bool variant_built() {
 }
 template <int VARIANT>
 constexpr bool is_pipe_variant() {
-    return !(VARIANT == 0 || VARIANT == 1 || VARIANT == 2 || VARIANT == 7 || (VARIANT >= 16 && VARIANT <= 22));
+    return !(VARIANT == 0 || VARIANT == 1 || VARIANT == 2 || VARIANT == 7 || (VARIANT >= 16 && VARIANT <= 22) ||
+             is_xpad_variant(VARIANT));
 }
 constexpr int variant_ne_of(int ne0, int v) {
-    const int ne = (v == 0 || v == 3 || v == 6 || v == 14 || v == 19 || v == 23)     ? ne0
-                   : (v == 1 || v == 4 || v == 5 || v == 10 || v == 11 || v == 20)  ? ne0 / 2
+    const int ne = (v == 0 || v == 3 || v == 6 || v == 14 || v == 19 || v == 23 || v == 27)     ? ne0
+                   : (v == 1 || v == 4 || v == 5 || v == 10 || v == 11 || v == 20 || v == 26)  ? ne0 / 2
                    : (v == 2 || v == 16 || v == 21 || v == 24)                      ? ne0 * 2
                    : (v == 17)                                                      ? ne0
                    : (v == 18)                                                      ? ne0 * 4
@@ -241,6 +250,29 @@ inline bool encode_chunk_map(CUtensorMap* tm, const void* base, int dim, int m, 
     return r == CUDA_SUCCESS;
 }
 
+// The padded-chunk view of a field whose group is the chunk: {x-row (i, e_l): m NE words,
+// rows (j, k): m^(d-1), v: n_v, group}, box {m NE + XP, m^(d-1), n_v, 1} -- the XP words past
+// each row are out of bounds (zero-filled on load, clipped on store), so the box lands in
+// shared memory with the padded row stride.  16-byte x-rows only.
+template <class R>
+inline bool encode_xpad_map(CUtensorMap* tm, const void* base, int dim, int m, int ne, long long n_groups, int rs) {
+    EncodeTiled enc = encode_tiled_fn();
+    const cuuint64_t w = sizeof(R);
+    const cuuint64_t rw = cuuint64_t(m) * ne;
+    if (!enc || (rw * w) % 16 != 0 || rs > 256) return false;
+    const cuuint64_t xr = dim == 3 ? cuuint64_t(m) * m : cuuint64_t(m);
+    const cuuint64_t nv = cuuint64_t(n_vars_c(dim));
+    const cuuint64_t dims[4] = {rw, xr, nv, cuuint64_t(n_groups)};
+    const cuuint64_t strides[3] = {rw * w, rw * w * xr, rw * w * xr * nv};
+    const cuuint32_t box[4] = {cuuint32_t(rs), cuuint32_t(xr), cuuint32_t(nv), 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = enc(tm, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                           const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // Kernel launch with programmatic dependent launch (PDL): consecutive fused launches on
 // a stream overlap one kernel's launch and ramp-up with the previous one's tail; the
 // kernels wait (griddepcontrol.wait) before touching HBM, so stream order is kept.
@@ -305,10 +337,26 @@ inline void fill_regs(K kernel, KInfo* info) {
 inline const char* prec_name(size_t w) { return w == 4 ? "fp32" : "fp64"; }
 
 // Launch (or, with dry = true, only describe) the lines kernel.
-template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false, int GS = NE, bool CS = false>
+template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false, int GS = NE, bool CS = false,
+          int XP = 0>
 cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
-    using S = LinesShape<R, DIM, M, NE, LPT, GS, CS>;
-    auto kernel = hf_lines_kernel<R, DIM, M, NE, SRC, LPT, FACES, GS, CS>;
+    if constexpr (XP > 0) {
+        // padded chunks: the group is the chunk, 16-byte x-rows no wider than a tensor box
+        // (256 words with the pad), aligned buffers, both tensor maps encoded; else the same
+        // chunk unpadded
+        bool ok = p.group == NE && (M * NE * sizeof(R)) % 16 == 0 && M * NE + XP <= 256 &&
+                  (p.u == nullptr || (aligned16(p.u) && aligned16(p.out)));
+        if (ok && !dry && p.n_elem > 0) {
+            const long long n_groups = (p.n_elem + p.group - 1) / p.group;
+            const int rs = M * NE + XP;
+            ok = encode_xpad_map<R>(&p.tm_u, p.u, DIM, M, NE, n_groups, rs) &&
+                 encode_xpad_map<R>(&p.tm_out, p.out, DIM, M, NE, n_groups, rs);
+            p.xpad = ok ? 1 : 0;
+        }
+        if (!ok) return launch_lines<R, DIM, M, NE, SRC, LPT, FACES, GS, CS, 0>(p, st, info, dry);
+    }
+    using S = LinesShape<R, DIM, M, NE, LPT, GS, CS, XP>;
+    auto kernel = hf_lines_kernel<R, DIM, M, NE, SRC, LPT, FACES, GS, CS, XP>;
     const bool tile = GS == NE && tile_layout<R, NE>(p.group) && (p.u == nullptr || (aligned16(p.u) && aligned16(p.out)));
     const long long n_groups = (p.n_elem + p.group - 1) / p.group;
     const int sub = (p.group + NE - 1) / NE;
@@ -329,8 +377,9 @@ cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
             std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d_g%d%s", DIM, M - 1,
                           prec_name(sizeof(R)), NE, GS, SRC ? "_src" : "");
         else if (LPT == 1)
-            std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d%s%s%s", DIM, M - 1,
-                          prec_name(sizeof(R)), NE, CS ? "_cs" : "", tile ? "_tile" : "", SRC ? "_src" : "");
+            std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d%s%s%s%s", DIM, M - 1,
+                          prec_name(sizeof(R)), NE, CS ? "_cs" : "", XP ? "_xp" : "", tile ? "_tile" : "",
+                          SRC ? "_src" : "");
         else
             std::snprintf(info->name, sizeof(info->name), "hf_lines_d%d_p%d_%s_ne%d_l%d%s", DIM, M - 1,
                           prec_name(sizeof(R)), NE, LPT, SRC ? "_src" : "");

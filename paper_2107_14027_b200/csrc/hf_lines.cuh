@@ -66,9 +66,25 @@ constexpr int grouped_pad_words(int w, int blk_words) {
 // CS: component split -- each a-line is worked by d threads, one per velocity component b
 // (V_b and the momentum flux M_ba, lines_sweep_comp): d times the threads per chunk for the
 // high orders whose chunks are few per SM (shared-memory bound), same arithmetic.
-template <class R, int DIM, int M, int NE, int LPT = 1, int GS = NE, bool CS = false>
+// Padding (words) of the x-rows of a padded chunk (lines variants 25-27, XP): the chunk is
+// staged as rows of the m x NE words (i, el) of one (j, k, v), and x-lines (and the
+// accumulator lines) all start at multiples of the row stride; a stride that is an odd
+// multiple of 16 bytes spreads them over the banks.  The padded image is moved by one TMA
+// tensor copy whose box is wider than the row -- the pad words are out of bounds, zero-filled
+// on load and clipped on store -- so the copy engine does the deconfliction that the
+// reference's planar kernels get from a padded plane stride (banks.hpp:59-120).
+template <class R, int DIM, int M, int NE>
+constexpr int xpad_words() {
+    constexpr int gran = 16 / int(sizeof(R));
+    int xp = 0;
+    while ((M * NE + xp) % gran != 0 || ((M * NE + xp) / gran) % 2 == 0) ++xp;
+    return xp;
+}
+
+template <class R, int DIM, int M, int NE, int LPT = 1, int GS = NE, bool CS = false, int XP = 0>
 struct LinesShape {
     static_assert(NE % GS == 0, "a grouped chunk holds whole groups");
+    static_assert(XP == 0 || (GS == NE && !CS), "padded x-rows: plain chunks only");
     static constexpr int NV = n_vars_c(DIM);
     static constexpr int NP = ipow_c(M, DIM);
     static constexpr int LINES = NE * ipow_c(M, DIM - 1);
@@ -77,25 +93,46 @@ struct LinesShape {
     static constexpr int BS = CS ? (DIM * NT < 64 ? 64 : DIM * NT) : (NT < 64 ? 64 : NT);
     static constexpr int NACC = 1 + DIM;  // continuity + d momentum partials
     static constexpr int IN_WORDS = NE * NP * NV;
-    static constexpr int ACC_WORDS = NE * NP * NACC;
+    static constexpr int RW = M * NE;                   // x-row words (i, el)
+    static constexpr int RS = RW + XP;                  // staged x-row stride
+    static constexpr int XR = ipow_c(M, DIM - 1);       // x-rows per variable
+    static constexpr int AS = XP ? RS * XR : NE * NP;   // accumulator row stride
+    static constexpr int ACC_WORDS = AS * NACC;
     static constexpr int HDR = 128;  // mbarrier + alignment pad
     static constexpr int IN_BYTES = IN_WORDS * int(sizeof(R));
     static constexpr int ROW_BYTES = NE * int(sizeof(R));
     using IO = ChunkIO<R, NE, NP * NV, IN_BYTES>;
-    static constexpr int VS = GS * NP;          // word stride between variables
+    static constexpr int VS = XP ? RS * XR : GS * NP;  // word stride between variables
     static constexpr int BLK = GS * NP * NV;    // one group in HBM
     static constexpr int PADW = GS < NE ? grouped_pad_words(int(sizeof(R)), BLK) : 0;
     static constexpr int BLKP = BLK + PADW;     // one staged group (padded: one bulk copy per group)
     static constexpr int BUF_BYTES =            // chunk buffer incl. alignment slack
-        PADW ? ((NE / GS) * BLKP * int(sizeof(R)) + 15) / 16 * 16 : IO::BUF_BYTES;
+        XP ? (NV * VS * int(sizeof(R)) + 127) / 128 * 128
+           : PADW ? ((NE / GS) * BLKP * int(sizeof(R)) + 15) / 16 * 16 : IO::BUF_BYTES;
     static constexpr size_t SMEM = HDR + size_t(BUF_BYTES) + size_t(ACC_WORDS) * sizeof(R);
     // word of (element, point, variable) in the staged chunk
     __host__ __device__ static constexpr int word(int el, int pt, int v) {
+        if constexpr (XP > 0) return el + NE * (pt % M) + RS * (pt / M) + VS * v;
         return (el % GS) + GS * pt + VS * v + (el / GS) * BLKP;
+    }
+    // word step between consecutive points of an A-line (state; accumulators: acc_step)
+    template <int A>
+    __host__ __device__ static constexpr int step() {
+        if constexpr (XP > 0) return A == 0 ? NE : A == 1 ? RS : RS * M;
+        return GS * (A == 0 ? 1 : A == 1 ? M : M * M);
+    }
+    template <int A>
+    __host__ __device__ static constexpr int acc_step() {
+        if constexpr (XP > 0) return step<A>();
+        return NE * (A == 0 ? 1 : A == 1 ? M : M * M);
     }
     // staged position of the li-th word of the chunk's HBM image (li = group * BLK + rem)
     __host__ __device__ static constexpr int staged(int li) {
-        if constexpr (PADW == 0) {
+        if constexpr (XP > 0) {
+            const int v = li / (NE * NP), rem = li - v * (NE * NP);
+            const int row = rem / RW, col = rem - row * RW;
+            return col + RS * row + VS * v;
+        } else if constexpr (PADW == 0) {
             return li;
         } else {
             const int b = li / BLK;
@@ -107,7 +144,7 @@ struct LinesShape {
     // cannot be re-laid out -- it is the HBM image).  Offset of the line at chunk offset o:
     __host__ __device__ static constexpr int acc_of(int o) {
         if constexpr (GS == NE) {
-            return o;
+            return o;  // (padded chunks: the accumulators share the padded layout)
         } else {
             const int blk = o / BLKP, rem = o - blk * BLKP;
             return blk * GS + rem % GS + NE * (rem / GS);
@@ -128,11 +165,11 @@ __device__ __forceinline__ bool chunk_bulk_ok(const Params<R>& p, long long gbas
 // Outputs of one line point (index i of the sweep's line): gradient rows final
 // (+ source), continuity / momentum partials accumulated or finished.
 // GRAD = false: the caller stores the gradient rows itself (vectorised x-lines, lines_sweep).
-template <class R, int DIM, int M, int NE, bool SRC, int A, int PHASE, int GS = NE, bool GRAD = true>
+template <class R, int DIM, int M, int NE, bool SRC, int A, int PHASE, int GS = NE, bool GRAD = true, int XP = 0>
 __device__ __forceinline__ void lines_emit(R* __restrict__ q, R* __restrict__ a, const Params<R>& p, const R (&dV)[DIM],
                                            const R (&dQ)[DIM]) {
-    constexpr int VS = GS * ipow_c(M, DIM);   // state rows
-    constexpr int AS = NE * ipow_c(M, DIM);   // accumulator rows
+    constexpr int VS = LinesShape<R, DIM, M, NE, 1, GS, false, XP>::VS;  // state rows
+    constexpr int AS = LinesShape<R, DIM, M, NE, 1, GS, false, XP>::AS;  // accumulator rows
     if constexpr (GRAD)
 #pragma unroll
         for (int b = 0; b < DIM; ++b) {
@@ -158,10 +195,15 @@ __device__ __forceinline__ void lines_emit(R* __restrict__ q, R* __restrict__ a,
 
 // Word offset (inside a chunk) of the first point of line L of a sweep along A:
 // L = el + NE * r, r enumerating the two fixed indices (layout.hpp:128-134).
-template <int DIM, int M, int NE, int A, int GS = NE, int BLKS = GS * ipow_c(M, DIM) * n_vars_c(DIM)>
+template <int DIM, int M, int NE, int A, int GS = NE, int BLKS = GS * ipow_c(M, DIM) * n_vars_c(DIM), int RS = 0>
 __host__ __device__ constexpr int line_offset(int L) {
     const int el = L % NE;
     const int r = L / NE;
+    if (RS > 0) {  // padded x-rows (GS == NE): row = j + M k of the line's first point
+        if (A == 0) return el + RS * r;                                   // r = j + M k
+        if (DIM == 3 && A == 1) return el + NE * (r % M) + RS * M * (r / M);  // r = i + M k
+        return el + NE * (r % M) + RS * (r / M);                            // d3 A=2: r = i + M j; d2 A=1: r = i
+    }
     int base_pt = r;                                  // d3 A=2: r = i + M j;  d2 A=1: r = i
     if (A == 0) base_pt = M * r;                      // d3: r = j + M k;  d2: r = j
     if (DIM == 3 && A == 1) base_pt = (r % M) + M * M * (r / M);  // r = i + M k
@@ -194,7 +236,7 @@ __host__ __device__ constexpr int x_line_vec() {
 // slots (a conflict, but no extra iteration).  With the natural order (L = t,
 // t + NTHR, ...) the y-sweep conflicts whenever NE*m is not a multiple of the
 // bank count (e.g. 2-way at p6 FP64).  Built at compile time; 0xFFFF = idle.
-template <class R, int DIM, int M, int NE, int A, int NTHR, int GS = NE>
+template <class R, int DIM, int M, int NE, int A, int NTHR, int GS = NE, int XP = 0>
 struct LineMap {
     static constexpr int LINES = NE * ipow_c(M, DIM - 1);
     static constexpr int ITERS = (LINES + NTHR - 1) / NTHR;
@@ -202,10 +244,10 @@ struct LineMap {
     unsigned short off[N];
 };
 
-template <class R, int DIM, int M, int NE, int A, int NTHR, int GS = NE>
-constexpr LineMap<R, DIM, M, NE, A, NTHR, GS> make_line_map() {
-    using LM = LineMap<R, DIM, M, NE, A, NTHR, GS>;
-    using S = LinesShape<R, DIM, M, NE, 1, GS>;
+template <class R, int DIM, int M, int NE, int A, int NTHR, int GS = NE, int XP = 0>
+constexpr LineMap<R, DIM, M, NE, A, NTHR, GS, XP> make_line_map() {
+    using LM = LineMap<R, DIM, M, NE, A, NTHR, GS, XP>;
+    using S = LinesShape<R, DIM, M, NE, 1, GS, false, XP>;
     // vectorised x-lines (x_line_vec): a VW-word access, 128 / (VW * sizeof(R)) lanes per wavefront
     constexpr int VW = x_line_vec<R, M, GS, S::BLKP, S::VS, A>();
     constexpr int B = VW > 1 ? 128 / (VW * int(sizeof(R))) : sizeof(R) == 4 ? 32 : 16;  // bank classes per phase
@@ -217,7 +259,7 @@ constexpr LineMap<R, DIM, M, NE, A, NTHR, GS> make_line_map() {
     int spill[LM::LINES > 0 ? LM::LINES : 1] = {};
     int n_spill = 0;
     for (int L = 0; L < LM::LINES; ++L) {
-        const int o = line_offset<DIM, M, NE, A, GS, S::BLKP>(L);
+        const int o = line_offset<DIM, M, NE, A, GS, S::BLKP, (XP ? S::RS : 0)>(L);
         const int c = (o / VW) % B;
         const int idx = next[c]++;
         const int it = idx / (NW * HALVES);
@@ -234,8 +276,8 @@ constexpr LineMap<R, DIM, M, NE, A, NTHR, GS> make_line_map() {
     return m;
 }
 
-template <class R, int DIM, int M, int NE, int A, int NTHR, int GS = NE>
-__device__ const LineMap<R, DIM, M, NE, A, NTHR, GS> kLineMap = make_line_map<R, DIM, M, NE, A, NTHR, GS>();
+template <class R, int DIM, int M, int NE, int A, int NTHR, int GS = NE, int XP = 0>
+__device__ const LineMap<R, DIM, M, NE, A, NTHR, GS, XP> kLineMap = make_line_map<R, DIM, M, NE, A, NTHR, GS, XP>();
 
 template <class R, int M, int VW>
 __device__ __forceinline__ void load_row(const R* __restrict__ q, R (&out)[M]) {
@@ -277,11 +319,12 @@ __device__ __forceinline__ void store_row(R* __restrict__ q, const R (&in)[M]) {
 
 // One sweep along axis A.  PHASE: 0 = first sweep, 1 = middle, 2 = last.
 // `o` = the line's first word inside the chunk (line_offset()).
-template <class R, int DIM, int M, int NE, bool SRC, int A, int PHASE, int GS = NE>
+template <class R, int DIM, int M, int NE, bool SRC, int A, int PHASE, int GS = NE, int XP = 0>
 __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ acc, const Params<R>& p, int o) {
-    using S = LinesShape<R, DIM, M, NE, 1, GS>;
+    using S = LinesShape<R, DIM, M, NE, 1, GS, false, XP>;
     constexpr int VS = S::VS;  // word stride between variables
-    constexpr int STRIDE = (A == 0) ? 1 : (A == 1) ? M : M * M;  // point stride along the line
+    constexpr int PS = S::template step<A>();      // point step along the line (state)
+    constexpr int APS = S::template acc_step<A>();  // ... and in the accumulator region
 
     R* __restrict__ sb = s + o;
     R* __restrict__ ab = acc + S::acc_of(o);
@@ -289,7 +332,7 @@ __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ a
     using PR = Pair<R>;
     // W[b][t] = (V_b, M_ba) at line point t: both lines are contracted with the same D rows
     PR W[DIM][M];
-    constexpr int VW = x_line_vec<R, M, GS, S::BLKP, VS, A>();
+    constexpr int VW = x_line_vec<R, M, GS, (XP ? S::RS : S::BLKP), VS, A>();
     // element-major chunk (GS = 1): an x-line's M points are consecutive words, so each
     // variable's row is read (and each gradient row of the first sweep written) with VW-wide
     // accesses -- a quarter-warp of LDS.128 covers the 32 banks, where scalar accesses of
@@ -314,7 +357,7 @@ __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ a
     } else {
 #pragma unroll
         for (int t = 0; t < M; ++t) {
-            const R* q = sb + GS * STRIDE * t;
+            const R* q = sb + PS * t;
             const R P = q[0];
             R V[DIM];
 #pragma unroll
@@ -347,8 +390,7 @@ __device__ __forceinline__ void lines_sweep(R* __restrict__ s, R* __restrict__ a
                 Gout[b_][(I)] = o_;                                                                            \
             }                                                                                                   \
         }                                                                                                       \
-        lines_emit<R, DIM, M, NE, SRC, A, PHASE, GS, !VEC_ST>(sb + GS * STRIDE * (I), ab + NE * STRIDE * (I), p, dV_, \
-                                                              dQ_);                                            \
+        lines_emit<R, DIM, M, NE, SRC, A, PHASE, GS, !VEC_ST, XP>(sb + PS * (I), ab + APS * (I), p, dV_, dQ_);    \
     } while (0)
     if constexpr (M < HF_EVEN_ODD_MIN_M) {
 #pragma unroll
@@ -554,9 +596,10 @@ __device__ __forceinline__ void lines_project_faces(const R* __restrict__ s, con
 }
 
 template <class R, int DIM, int M, int NE, bool SRC, int HEADB, int BAR, int NTHR, bool FACES = false, int GS = NE,
-          bool CS = false>
+          bool CS = false, int XP = 0>
 __device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const Params<R>& p, int t, int bar_id = 0,
                                              long long E0 = 0, int nvalid = NE) {
+    static_assert(XP == 0 || (!FACES && !CS && HEADB == 0), "padded x-rows: plain sweeps of an aligned chunk");
     // NTHR: line slots per sweep iteration (LineMap); CS: d component groups of NTHR threads
     constexpr int NALL = CS ? DIM * NTHR : NTHR;
     R* s = reinterpret_cast<R*>(buf + HEADB);
@@ -572,13 +615,13 @@ __device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const P
     auto sweep = [&](auto a_tag, auto phase_tag) {
         constexpr int A = decltype(a_tag)::value;
         constexpr int PH = decltype(phase_tag)::value;
-        using LM = LineMap<R, DIM, M, NE, A, NTHR, GS>;
-        const unsigned short* map = kLineMap<R, DIM, M, NE, A, NTHR, GS>.off;
+        using LM = LineMap<R, DIM, M, NE, A, NTHR, GS, XP>;
+        const unsigned short* map = kLineMap<R, DIM, M, NE, A, NTHR, GS, XP>.off;
         if constexpr (!CS) {
 #pragma unroll 1
             for (int k = 0; k < LM::ITERS; ++k) {
                 const int o = map[k * NTHR + t];
-                if (o != 0xFFFF) lines_sweep<R, DIM, M, NE, SRC, A, PH, GS>(s, acc, p, o);
+                if (o != 0xFFFF) lines_sweep<R, DIM, M, NE, SRC, A, PH, GS, XP>(s, acc, p, o);
             }
         } else {
             // warp-uniform component: component group b = threads [b*NTHR, (b+1)*NTHR)
@@ -628,10 +671,12 @@ __device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const P
 // Runtime head (bytes, a multiple of sizeof(R), < 16) -> compile-time HEADB.
 // Chunks whose byte size is a multiple of 16 always start aligned: one instance.
 template <class R, int DIM, int M, int NE, bool SRC, int BAR, int NTHR, bool FACES = false, int GS = NE,
-          bool CS = false>
+          bool CS = false, int XP = 0>
 __device__ __forceinline__ void lines_sweeps_at(unsigned char* buf, int head, R* acc, const Params<R>& p, int t,
                                                 int bar_id = 0, long long E0 = 0, int nv = NE) {
-    if constexpr (LinesShape<R, DIM, M, NE>::IN_BYTES % 16 == 0) {
+    if constexpr (XP > 0) {  // padded chunks are staged by a tensor copy or word by word: head 0
+        lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES, GS, CS, XP>(buf, acc, p, t, bar_id, E0, nv);
+    } else if constexpr (LinesShape<R, DIM, M, NE>::IN_BYTES % 16 == 0) {
         lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES, GS, CS>(buf, acc, p, t, bar_id, E0, nv);
     } else if constexpr (sizeof(R) == 8) {
         if (head == 0) lines_sweeps<R, DIM, M, NE, SRC, 0, BAR, NTHR, FACES, GS, CS>(buf, acc, p, t, bar_id, E0, nv);
@@ -653,9 +698,10 @@ struct NoChunkHook {};
 // runs on the finished divergence in shared memory (layout [v][pt][el] of NE elements, GS ==
 // NE) between two CTA barriers -- the FR interface correction of hf_fr.cuh uses it to apply
 // stages 4+5 before the chunk leaves shared memory.
-template <class R, int DIM, int M, int NE, bool SRC, int LPT, bool FACES, int GS, bool CS, class Hook>
+template <class R, int DIM, int M, int NE, bool SRC, int LPT, bool FACES, int GS, bool CS, class Hook, int XP = 0>
 __device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
-    using S = LinesShape<R, DIM, M, NE, LPT, GS, CS>;
+    using S = LinesShape<R, DIM, M, NE, LPT, GS, CS, XP>;
+    static_assert(XP == 0 || (LPT == 1 && std::is_same_v<std::decay_t<Hook>, NoChunkHook>), "padded: plain kernel");
     constexpr int BS = S::BS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     using IO = typename S::IO;
@@ -686,10 +732,11 @@ __device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
     const bool contiguous = (p.group == GS);
     const bool full = E0 + nvalid <= p.n_elem;
     // padded grouped chunk (S::PADW): one exact 16-byte-multiple copy per group, no superset
-    const bool fast = p.tile ? (p.fast_ok && full)
-                             : (S::PADW ? (p.fast_ok && full && contiguous)
-                                        : chunk_bulk_ok<R, S::IN_WORDS>(p, gbase, full, contiguous));
-    const int head = (fast && !p.tile && !S::PADW) ? IO::head_bytes(p.u + gbase, contiguous) : 0;
+    const bool fast = XP ? (p.xpad && full && contiguous)
+                  : p.tile ? (p.fast_ok && full)
+                           : (S::PADW ? (p.fast_ok && full && contiguous)
+                                      : chunk_bulk_ok<R, S::IN_WORDS>(p, gbase, full, contiguous));
+    const int head = (fast && !XP && !p.tile && !S::PADW) ? IO::head_bytes(p.u + gbase, contiguous) : 0;
     R* s = reinterpret_cast<R*>(smem_raw + S::HDR);  // guarded path (head == 0)
     __shared__ long long ebase[NE];                   // guarded path: element word bases, -1 = absent
 
@@ -700,7 +747,12 @@ __device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
             fence_mbar_init();
         }
         __syncthreads();
-        if constexpr (S::PADW > 0) {  // one bulk copy per group, each to its padded slot
+        if constexpr (XP > 0) {  // one tensor copy: box {m NE + XP, m^(d-1), n_v, 1}, the pad zero-filled
+            if (tid == 0) {
+                mbar_arrive_expect_tx(bar, uint32_t(S::NV * S::VS * int(sizeof(R))));
+                tma_load_4d(buf, &p.tm_u, 0, 0, 0, static_cast<int>(grp), bar);
+            }
+        } else if constexpr (S::PADW > 0) {  // one bulk copy per group, each to its padded slot
             if (tid == 0) mbar_arrive_expect_tx(bar, uint32_t(S::IN_BYTES));
             __syncthreads();
             for (int g = tid; g < NE / GS; g += BS)
@@ -747,7 +799,7 @@ __device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
     }
 
     // ---------------- d sweeps ----------------
-    lines_sweeps_at<R, DIM, M, NE, SRC, 0, (CS ? S::NT : BS), FACES, GS, CS>(buf, head, acc, p, tid, 0, E0, nvalid);
+    lines_sweeps_at<R, DIM, M, NE, SRC, 0, (CS ? S::NT : BS), FACES, GS, CS, XP>(buf, head, acc, p, tid, 0, E0, nvalid);
     if constexpr (!std::is_same_v<std::decay_t<Hook>, NoChunkHook>) {
         __syncthreads();
         hook(reinterpret_cast<R*>(buf + head), E0, nvalid, tid);
@@ -757,7 +809,13 @@ __device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
     if (fast) {
         fence_proxy_async_smem();
         __syncthreads();
-        if constexpr (S::PADW > 0) {
+        if constexpr (XP > 0) {
+            if (tid == 0) {  // the pad words are out of bounds: clipped
+                tma_store_4d(&p.tm_out, 0, 0, 0, static_cast<int>(grp), buf);
+                bulk_commit();
+                bulk_wait_read_all();
+            }
+        } else if constexpr (S::PADW > 0) {
             for (int g = tid; g < NE / GS; g += BS)
                 bulk_s2g(p.out + gbase + static_cast<long long>(g) * S::BLK, buf + g * S::BLKP * int(sizeof(R)),
                          S::BLK * int(sizeof(R)));
@@ -786,10 +844,11 @@ __device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
     }
 }
 
-template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false, int GS = NE, bool CS = false>
-__global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT, GS, CS>::BS)
+template <class R, int DIM, int M, int NE, bool SRC, int LPT = 1, bool FACES = false, int GS = NE, bool CS = false,
+          int XP = 0>
+__global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, LPT, GS, CS, XP>::BS)
     hf_lines_kernel(const __grid_constant__ Params<R> p) {
-    lines_chunk<R, DIM, M, NE, SRC, LPT, FACES, GS, CS>(p, NoChunkHook{});
+    lines_chunk<R, DIM, M, NE, SRC, LPT, FACES, GS, CS, NoChunkHook, XP>(p, NoChunkHook{});
 }
 
 }  // namespace hfb

@@ -72,7 +72,7 @@ def test_lines_misaligned_pointer(cuda):
     check_parity(3, 2, 64, 16, False, U, method=Method.lines, offset_bytes=8)
 
 
-@pytest.mark.parametrize("variant", list(range(25)))
+@pytest.mark.parametrize("variant", list(range(28)))
 @pytest.mark.parametrize("d,p,fp32", [(3, 1, True), (3, 3, False), (3, 4, True), (3, 6, False), (3, 6, True),
                                       (2, 3, True), (2, 8, True)])
 def test_lines_variants(cuda, d, p, fp32, variant):

@@ -118,7 +118,7 @@ def main():
     ap.add_argument("--parse", nargs=2, default=None)
     ap.add_argument("--points", type=float, default=2e6)
     ap.add_argument("--dims", default="3,2")
-    ap.add_argument("--variants", default=",".join(str(v) for v in range(25)))
+    ap.add_argument("--variants", default=",".join(str(v) for v in range(28)))
     a = ap.parse_args()
     if a.metrics:
         print(",".join(METRICS))

@@ -35,7 +35,7 @@ def main():
             o = torch.empty_like(u)
             alg = n * npt * 2 * hf.n_vars(d) * u.element_size()
             rows = []
-            for v in range(25):
+            for v in range(28):
                 pr0 = hf.make_problem(d, p, 1, 1, prec, PAR)
                 try:
                     info = hf.variant_info(pr0, Method.lines, v)
