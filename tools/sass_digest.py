@@ -62,7 +62,13 @@ def mangled(info, d, p, prec, src=False):
         gs = re.search(r"_g(\d+)", name)
         gs = int(gs.group(1)) if gs else ne
         cs = "1" if "_cs" in name else "0"
-        return f"_ZN3hfb15hf_lines_kernelI{R}Li{d}ELi{m}ELi{ne}ELb{b}ELi{lpt}ELb0ELi{gs}ELb{cs}EEEvNS_6ParamsIT_EE"
+        xp = 0
+        if "_xp" in name:  # xpad_words (hf_lines.cuh): row stride an odd multiple of 16 bytes
+            gran = 16 // (4 if prec == Precision.fp32 else 8)
+            while (m * ne + xp) % gran or ((m * ne + xp) // gran) % 2 == 0:
+                xp += 1
+        return (f"_ZN3hfb15hf_lines_kernelI{R}Li{d}ELi{m}ELi{ne}ELb{b}ELi{lpt}ELb0ELi{gs}ELb{cs}ELi{xp}E"
+                "EEvNS_6ParamsIT_EE")
     if name.startswith("hf_planar_managed"):
         return f"_ZN3hfb24hf_planar_managed_kernelI{R}Li{m}ELi{ne}ELb{b}EEEvNS_6ParamsIT_EE"
     if name.startswith("hf_planar"):
