@@ -73,8 +73,8 @@ def test_lines_misaligned_pointer(cuda):
 
 
 @pytest.mark.parametrize("variant", list(range(28)))
-@pytest.mark.parametrize("d,p,fp32", [(3, 1, True), (3, 3, False), (3, 4, True), (3, 6, False), (3, 6, True),
-                                      (2, 3, True), (2, 8, True)])
+@pytest.mark.parametrize("d,p,fp32", [(3, 1, True), (3, 3, False), (3, 3, True), (3, 4, True), (3, 6, False),
+                                      (3, 6, True), (2, 3, True), (2, 7, True), (2, 8, True)])
 def test_lines_variants(cuda, d, p, fp32, variant):
     """Every lines variant (3..6 = persistent TMA-ring kernel), bulk chunks + guarded tail, +-source."""
     import paper_2107_14027_b200 as hf
