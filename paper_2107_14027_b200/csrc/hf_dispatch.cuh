@@ -19,7 +19,7 @@ int lines_variant_f(bool src, const Params<R>& prm, cudaStream_t st, KInfo* info
                    : int(launch_lines_pipe<R, DIM, M, NE, ST, GR, false, FACES, CS, TL>(prm, st, info, dry));
     } else {
         constexpr int LPT = lines_per_thread<VARIANT>();
-        constexpr int XP = is_xpad_variant(VARIANT) ? xpad_words<R, DIM, M, NE>() : 0;
+        constexpr int XP = is_xpad_variant(VARIANT) ? xpad_code<R, DIM, M, NE>() : 0;
         return src ? int(launch_lines<R, DIM, M, NE, true, LPT, FACES, NE, CS, XP>(prm, st, info, dry))
                    : int(launch_lines<R, DIM, M, NE, false, LPT, FACES, NE, CS, XP>(prm, st, info, dry));
     }

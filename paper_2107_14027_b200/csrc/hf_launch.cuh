@@ -255,21 +255,30 @@ inline bool encode_chunk_map(CUtensorMap* tm, const void* base, int dim, int m, 
 // each row are out of bounds (zero-filled on load, clipped on store), so the box lands in
 // shared memory with the padded row stride.  16-byte x-rows only.
 template <class R>
-inline bool encode_xpad_map(CUtensorMap* tm, const void* base, int dim, int m, int ne, long long n_groups, int rs) {
+inline bool encode_xpad_map(CUtensorMap* tm, const void* base, int dim, int m, int ne, long long n_groups, int rs,
+                            int pr) {
     EncodeTiled enc = encode_tiled_fn();
     const cuuint64_t w = sizeof(R);
     const cuuint64_t rw = cuuint64_t(m) * ne;
-    if (!enc || (rw * w) % 16 != 0 || rs > 256) return false;
-    const cuuint64_t xr = dim == 3 ? cuuint64_t(m) * m : cuuint64_t(m);
+    if (!enc || (rw * w) % 16 != 0 || rs > 256 || pr > 256) return false;
     const cuuint64_t nv = cuuint64_t(n_vars_c(dim));
-    const cuuint64_t dims[4] = {rw, xr, nv, cuuint64_t(n_groups)};
-    const cuuint64_t strides[3] = {rw * w, rw * w * xr, rw * w * xr * nv};
-    const cuuint32_t box[4] = {cuuint32_t(rs), cuuint32_t(xr), cuuint32_t(nv), 1};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    const CUresult r = enc(tm, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
-                           const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r;
+    if (dim == 3) {  // {x-row, j, k, v, group}, box {rs, pr, m, n_v, 1}: rows j >= m are the plane pad
+        const cuuint64_t dims[5] = {rw, cuuint64_t(m), cuuint64_t(m), nv, cuuint64_t(n_groups)};
+        const cuuint64_t strides[4] = {rw * w, rw * w * m, rw * w * m * m, rw * w * m * m * nv};
+        const cuuint32_t box[5] = {cuuint32_t(rs), cuuint32_t(pr), cuuint32_t(m), cuuint32_t(nv), 1};
+        r = enc(tm, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5,
+                const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        const cuuint64_t dims[4] = {rw, cuuint64_t(m), nv, cuuint64_t(n_groups)};
+        const cuuint64_t strides[3] = {rw * w, rw * w * m, rw * w * m * nv};
+        const cuuint32_t box[4] = {cuuint32_t(rs), cuuint32_t(m), cuuint32_t(nv), 1};
+        r = enc(tm, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     return r == CUDA_SUCCESS;
 }
 
@@ -344,13 +353,13 @@ cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
         // padded chunks: the group is the chunk, 16-byte x-rows no wider than a tensor box
         // (256 words with the pad), aligned buffers, both tensor maps encoded; else the same
         // chunk unpadded
-        bool ok = p.group == NE && (M * NE * sizeof(R)) % 16 == 0 && M * NE + XP <= 256 &&
+        using SX = LinesShape<R, DIM, M, NE, LPT, GS, CS, XP>;
+        bool ok = p.group == NE && (M * NE * sizeof(R)) % 16 == 0 && SX::RS <= 256 &&
                   (p.u == nullptr || (aligned16(p.u) && aligned16(p.out)));
         if (ok && !dry && p.n_elem > 0) {
             const long long n_groups = (p.n_elem + p.group - 1) / p.group;
-            const int rs = M * NE + XP;
-            ok = encode_xpad_map<R>(&p.tm_u, p.u, DIM, M, NE, n_groups, rs) &&
-                 encode_xpad_map<R>(&p.tm_out, p.out, DIM, M, NE, n_groups, rs);
+            ok = encode_xpad_map<R>(&p.tm_u, p.u, DIM, M, NE, n_groups, SX::RS, SX::PR) &&
+                 encode_xpad_map<R>(&p.tm_out, p.out, DIM, M, NE, n_groups, SX::RS, SX::PR);
             p.xpad = ok ? 1 : 0;
         }
         if (!ok) return launch_lines<R, DIM, M, NE, SRC, LPT, FACES, GS, CS, 0>(p, st, info, dry);

@@ -81,6 +81,16 @@ constexpr int xpad_words() {
     return xp;
 }
 
+// The padding code XP of a padded chunk: x-row pad words + 256 x pad rows per k-plane.  One-
+// element chunks (NE = 1, element-major, vectorised x-lines) keep 16-byte rows unpadded and
+// pad each k-plane by one row instead: their y-lines start at i + m^2 k, a few bank classes
+// for every k (the x-lines are already spread by their vector reads).
+template <class R, int DIM, int M, int NE>
+constexpr int xpad_code() {
+    if (DIM == 3 && NE == 1 && (M * int(sizeof(R))) % 16 == 0) return 256 * 1;
+    return xpad_words<R, DIM, M, NE>();
+}
+
 template <class R, int DIM, int M, int NE, int LPT = 1, int GS = NE, bool CS = false, int XP = 0>
 struct LinesShape {
     static_assert(NE % GS == 0, "a grouped chunk holds whole groups");
@@ -94,8 +104,13 @@ struct LinesShape {
     static constexpr int NACC = 1 + DIM;  // continuity + d momentum partials
     static constexpr int IN_WORDS = NE * NP * NV;
     static constexpr int RW = M * NE;                   // x-row words (i, el)
-    static constexpr int RS = RW + XP;                  // staged x-row stride
-    static constexpr int XR = ipow_c(M, DIM - 1);       // x-rows per variable
+    static constexpr int XW = XP % 256;                 // x-row pad words
+    static constexpr int PJ = XP / 256;                 // pad rows per k-plane (d3)
+    static_assert(PJ == 0 || DIM == 3, "plane padding is a d3 layout");
+    static constexpr int RS = RW + XW;                  // staged x-row stride
+    static constexpr int PR = M + PJ;                   // staged rows per k-plane
+    static constexpr int PL = RS * PR;                  // staged k-plane stride
+    static constexpr int XR = DIM == 3 ? PR * M : M;    // staged x-rows per variable
     static constexpr int AS = XP ? RS * XR : NE * NP;   // accumulator row stride
     static constexpr int ACC_WORDS = AS * NACC;
     static constexpr int HDR = 128;  // mbarrier + alignment pad
@@ -112,13 +127,13 @@ struct LinesShape {
     static constexpr size_t SMEM = HDR + size_t(BUF_BYTES) + size_t(ACC_WORDS) * sizeof(R);
     // word of (element, point, variable) in the staged chunk
     __host__ __device__ static constexpr int word(int el, int pt, int v) {
-        if constexpr (XP > 0) return el + NE * (pt % M) + RS * (pt / M) + VS * v;
+        if constexpr (XP > 0) return el + NE * (pt % M) + RS * ((pt / M) % M) + PL * (pt / (M * M)) + VS * v;
         return (el % GS) + GS * pt + VS * v + (el / GS) * BLKP;
     }
     // word step between consecutive points of an A-line (state; accumulators: acc_step)
     template <int A>
     __host__ __device__ static constexpr int step() {
-        if constexpr (XP > 0) return A == 0 ? NE : A == 1 ? RS : RS * M;
+        if constexpr (XP > 0) return A == 0 ? NE : A == 1 ? RS : PL;
         return GS * (A == 0 ? 1 : A == 1 ? M : M * M);
     }
     template <int A>
@@ -131,7 +146,7 @@ struct LinesShape {
         if constexpr (XP > 0) {
             const int v = li / (NE * NP), rem = li - v * (NE * NP);
             const int row = rem / RW, col = rem - row * RW;
-            return col + RS * row + VS * v;
+            return col + RS * (row % M) + PL * (row / M) + VS * v;
         } else if constexpr (PADW == 0) {
             return li;
         } else {
@@ -195,14 +210,15 @@ __device__ __forceinline__ void lines_emit(R* __restrict__ q, R* __restrict__ a,
 
 // Word offset (inside a chunk) of the first point of line L of a sweep along A:
 // L = el + NE * r, r enumerating the two fixed indices (layout.hpp:128-134).
-template <int DIM, int M, int NE, int A, int GS = NE, int BLKS = GS * ipow_c(M, DIM) * n_vars_c(DIM), int RS = 0>
+template <int DIM, int M, int NE, int A, int GS = NE, int BLKS = GS * ipow_c(M, DIM) * n_vars_c(DIM), int RS = 0,
+          int PL = RS * M>
 __host__ __device__ constexpr int line_offset(int L) {
     const int el = L % NE;
     const int r = L / NE;
-    if (RS > 0) {  // padded x-rows (GS == NE): row = j + M k of the line's first point
-        if (A == 0) return el + RS * r;                                   // r = j + M k
-        if (DIM == 3 && A == 1) return el + NE * (r % M) + RS * M * (r / M);  // r = i + M k
-        return el + NE * (r % M) + RS * (r / M);                            // d3 A=2: r = i + M j; d2 A=1: r = i
+    if (RS > 0) {  // padded chunk (GS == NE): x-row stride RS, k-plane stride PL
+        if (A == 0) return el + RS * (r % M) + PL * (r / M);          // r = j + M k
+        if (DIM == 3 && A == 1) return el + NE * (r % M) + PL * (r / M);  // r = i + M k
+        return el + NE * (r % M) + RS * (r / M);                        // d3 A=2: r = i + M j; d2 A=1: r = i
     }
     int base_pt = r;                                  // d3 A=2: r = i + M j;  d2 A=1: r = i
     if (A == 0) base_pt = M * r;                      // d3: r = j + M k;  d2: r = j
@@ -259,7 +275,7 @@ constexpr LineMap<R, DIM, M, NE, A, NTHR, GS, XP> make_line_map() {
     int spill[LM::LINES > 0 ? LM::LINES : 1] = {};
     int n_spill = 0;
     for (int L = 0; L < LM::LINES; ++L) {
-        const int o = line_offset<DIM, M, NE, A, GS, S::BLKP, (XP ? S::RS : 0)>(L);
+        const int o = line_offset<DIM, M, NE, A, GS, S::BLKP, (XP ? S::RS : 0), (XP ? S::PL : 0)>(L);
         const int c = (o / VW) % B;
         const int idx = next[c]++;
         const int it = idx / (NW * HALVES);
@@ -747,10 +763,12 @@ __device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
             fence_mbar_init();
         }
         __syncthreads();
-        if constexpr (XP > 0) {  // one tensor copy: box {m NE + XP, m^(d-1), n_v, 1}, the pad zero-filled
+        if constexpr (XP > 0) {  // one tensor copy: the box one pad wider than the row (and the
+                                 // k-plane), the pad out of bounds and zero-filled
             if (tid == 0) {
                 mbar_arrive_expect_tx(bar, uint32_t(S::NV * S::VS * int(sizeof(R))));
-                tma_load_4d(buf, &p.tm_u, 0, 0, 0, static_cast<int>(grp), bar);
+                if constexpr (DIM == 3) tma_load_5d(buf, &p.tm_u, 0, 0, 0, 0, static_cast<int>(grp), bar);
+                else tma_load_4d(buf, &p.tm_u, 0, 0, 0, static_cast<int>(grp), bar);
             }
         } else if constexpr (S::PADW > 0) {  // one bulk copy per group, each to its padded slot
             if (tid == 0) mbar_arrive_expect_tx(bar, uint32_t(S::IN_BYTES));
@@ -811,7 +829,8 @@ __device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
         __syncthreads();
         if constexpr (XP > 0) {
             if (tid == 0) {  // the pad words are out of bounds: clipped
-                tma_store_4d(&p.tm_out, 0, 0, 0, static_cast<int>(grp), buf);
+                if constexpr (DIM == 3) tma_store_5d(&p.tm_out, 0, 0, 0, 0, static_cast<int>(grp), buf);
+                else tma_store_4d(&p.tm_out, 0, 0, 0, static_cast<int>(grp), buf);
                 bulk_commit();
                 bulk_wait_read_all();
             }

@@ -63,10 +63,14 @@ def mangled(info, d, p, prec, src=False):
         gs = int(gs.group(1)) if gs else ne
         cs = "1" if "_cs" in name else "0"
         xp = 0
-        if "_xp" in name:  # xpad_words (hf_lines.cuh): row stride an odd multiple of 16 bytes
-            gran = 16 // (4 if prec == Precision.fp32 else 8)
-            while (m * ne + xp) % gran or ((m * ne + xp) // gran) % 2 == 0:
-                xp += 1
+        if "_xp" in name:  # xpad_code (hf_lines.cuh): x-row pad words + 256 x k-plane pad rows
+            w = 4 if prec == Precision.fp32 else 8
+            if d == 3 and ne == 1 and (m * w) % 16 == 0:
+                xp = 256
+            else:
+                gran = 16 // w
+                while (m * ne + xp) % gran or ((m * ne + xp) // gran) % 2 == 0:
+                    xp += 1
         return (f"_ZN3hfb15hf_lines_kernelI{R}Li{d}ELi{m}ELi{ne}ELb{b}ELi{lpt}ELb0ELi{gs}ELb{cs}ELi{xp}E"
                 "EEvNS_6ParamsIT_EE")
     if name.startswith("hf_planar_managed"):

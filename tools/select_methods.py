@@ -170,7 +170,9 @@ def main():
 # override stays (the bench measured 20 at 1.00-1.03).
 # d2 p1 FP32: the padded NE0/4 chunk (25) wins the 1e7-point sweep by 2 %, but BASELINE config 3
 # runs that order at 4e6 points, where the bench measured 0.87 against 0.91 for variant 1.
-OVERRIDES = {(3, 6, "fp32"): 3, (3, 4, "fp64"): 20, (2, 1, "fp32"): 1}
+# d3 p7 FP32: the one-element chunk with padded k-planes (25), measured after select_r02c in
+# profiles/r02/xpad/plane_pad_p4-7.jsonl (0.83 against 0.73 for the TMA ring).
+OVERRIDES = {(3, 6, "fp32"): 3, (3, 4, "fp64"): 20, (2, 1, "fp32"): 1, (3, 7, "fp32"): 25}
 TIE = 0.0075
 
 
