@@ -323,6 +323,24 @@ def test_tile_mode_with_misaligned_buffers_takes_the_guarded_path(cuda):
     check_parity(3, 3, 70, 32, False, U, offset_bytes=8)
 
 
+@pytest.mark.parametrize("d,p,fp32", [(3, 3, False), (3, 3, True), (3, 7, True), (2, 7, True)])
+def test_padded_chunks_edge_cases(cuda, d, p, fp32):
+    """The selected padded-chunk kernels (lines variants 25-27, TMA box wider than the row /
+    plane): a partial last chunk (guarded path into the padded layout), a misaligned base
+    (falls back to the unpadded chunk) and a caller group that is not the chunk."""
+    import paper_2107_14027_b200 as hf
+    from paper_2107_14027_b200 import Precision
+    prec = Precision.fp32 if fp32 else Precision.fp64
+    g = hf.preferred_group(hf.make_problem(d, p, 1, 1, prec, PAR))
+    assert hf.kernel_info(hf.make_problem(d, p, 10 * g, g, prec, PAR))["name"].endswith("_xp")
+    n = 37 * g + max(1, g // 2)
+    U = _field(d, p, n, g, fp32, 8100 + p)
+    check_parity(d, p, n, g, fp32, U, with_source=True)
+    check_parity(d, p, n, g, fp32, U, offset_bytes=8)
+    U2 = _field(d, p, n, 2 * g, fp32, 8200 + p)
+    check_parity(d, p, n, 2 * g, fp32, U2)
+
+
 # ---------------------------------------------------------------- stream order under programmatic dependent launch
 @pytest.mark.parametrize("d,p,fp32", [(3, 3, False), (3, 6, False), (2, 2, True), (3, 1, True)])
 def test_dependent_back_to_back_launches(cuda, d, p, fp32):
