@@ -396,7 +396,6 @@ int dispatch(const hf_problem* pr, const void* u, void* out, void* ws, cudaStrea
     select_method(pr, &method, &variant);
     if (faces && method == HF_METHOD_LINES && hfb::faces_variant_override(pr->d, pr->p) >= 0)
         variant = hfb::faces_variant_override(pr->d, pr->p);
-    if (faces && method == HF_METHOD_LINES) variant = hfb::xpad_base_variant(variant);  // stage 1 rides unpadded
     if (force_method >= 0) method = force_method;
     if (force_variant >= 0) variant = force_variant;
     const bool src = pr->with_source != 0;

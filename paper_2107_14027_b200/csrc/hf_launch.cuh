@@ -105,7 +105,6 @@ constexpr int faces_variant_override(int d, int p) { return (d == 3 && p == 6) ?
 // The FACES (fused FR stage 1) form: the selected variant of each configuration.
 template <class R, int DIM, int M, int VARIANT>
 constexpr bool variant_faces_built() {
-    if (is_xpad_variant(VARIANT)) return false;  // FR stage 1 rides on the unpadded chunk (xpad_base_variant)
 #ifdef HF_TUNING
     return VARIANT == 0 || VARIANT == 3;
 #else

@@ -579,10 +579,10 @@ __device__ __forceinline__ void comp_contract_emit(R* __restrict__ s, R* __restr
 // FACES: FR stage 1 fused in (hf_fr.cuh): before the sweeps overwrite the staged
 // chunk, every a-line of every variable is extrapolated to xi_a = -1, +1 and
 // written to p.uf -- the face projection without a second read of the field.
-template <class R, int DIM, int M, int NE, int GS = NE>
+template <class R, int DIM, int M, int NE, int GS = NE, int XP = 0>
 __device__ __forceinline__ void lines_project_faces(const R* __restrict__ s, const Params<R>& p, long long E0, int t,
                                                     int nthr, int nvalid) {
-    using S = LinesShape<R, DIM, M, NE, 1, GS>;
+    using S = LinesShape<R, DIM, M, NE, 1, GS, false, XP>;
     constexpr int NV = n_vars_c(DIM), LN = ipow_c(M, DIM - 1);
     for (int task = t; task < NE * LN * DIM; task += nthr) {
         const int el = task % NE;
@@ -615,7 +615,7 @@ template <class R, int DIM, int M, int NE, bool SRC, int HEADB, int BAR, int NTH
           bool CS = false, int XP = 0>
 __device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const Params<R>& p, int t, int bar_id = 0,
                                              long long E0 = 0, int nvalid = NE) {
-    static_assert(XP == 0 || (!FACES && !CS && HEADB == 0), "padded x-rows: plain sweeps of an aligned chunk");
+    static_assert(XP == 0 || (!CS && HEADB == 0), "padded chunks: one thread per line, an aligned chunk");
     // NTHR: line slots per sweep iteration (LineMap); CS: d component groups of NTHR threads
     constexpr int NALL = CS ? DIM * NTHR : NTHR;
     R* s = reinterpret_cast<R*>(buf + HEADB);
@@ -668,7 +668,7 @@ __device__ __forceinline__ void lines_sweeps(unsigned char* buf, R* acc, const P
     using I1 = std::integral_constant<int, 1>;
     using I2 = std::integral_constant<int, 2>;
     if constexpr (FACES) {
-        lines_project_faces<R, DIM, M, NE, GS>(s, p, E0, t, NALL, nvalid);
+        lines_project_faces<R, DIM, M, NE, GS, XP>(s, p, E0, t, NALL, nvalid);
         sync();  // every line is read before sweep 0 writes in place
     }
     if constexpr (DIM == 3) {
