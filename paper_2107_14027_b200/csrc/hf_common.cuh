@@ -53,8 +53,9 @@ struct Params {
     // per direction over the 5-d view {e_l, i, (j,k), v, group} of the AoSoA field.
     int tile;
     int sub_per_group;        // ceil(group / NE)
-    // Padded chunks (lines variants 25-27): tm_u / tm_out hold the 4-d view {x-row, rows, v,
-    // group} of a field whose group is the chunk, with a box one pad wider than the row.
+    // Padded chunks (lines variants 25-27): tm_u / tm_out hold the view {x-row, j, (k), v,
+    // group} of a field whose group is the chunk, the box wider than the row / taller than the
+    // k-plane by the pad (encode_xpad_map).
     int xpad;
     CUtensorMap tm_u;         // 64-byte aligned descriptors, read from the parameter space
     CUtensorMap tm_out;

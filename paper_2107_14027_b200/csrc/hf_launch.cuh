@@ -76,9 +76,9 @@ constexpr int lines_ne_default() {
 constexpr int kLinesVariants = 28;
 constexpr bool is_cs_variant(int v) { return v >= 19 && v <= 23; }
 constexpr int kTileRingVariant = 24;  // TMA ring, 2 NE0 elements, 2 stages, 1 group, tile mode
-// 25 / 26 / 27: one chunk per CTA of NE0/4, NE0/2, NE0 elements staged with padded x-rows
-// (LinesShape XP, xpad_words): the chunk layout of variants 7 / 1 / 0 with a row stride
-// that spreads the x-lines and accumulator lines over the banks.
+// 25 / 26 / 27: one chunk per CTA of NE0/4, NE0/2, NE0 elements staged padded (LinesShape XP,
+// xpad_code): the chunk layout of variants 7 / 1 / 0 with an x-row stride (one-element
+// chunks: a k-plane stride) that spreads the lines over the banks.
 constexpr bool is_xpad_variant(int v) { return v >= 25 && v <= 27; }
 constexpr int xpad_base_variant(int v) { return v == 25 ? 7 : v == 26 ? 1 : v == 27 ? 0 : v; }
 
@@ -249,10 +249,11 @@ inline bool encode_chunk_map(CUtensorMap* tm, const void* base, int dim, int m, 
     return r == CUDA_SUCCESS;
 }
 
-// The padded-chunk view of a field whose group is the chunk: {x-row (i, e_l): m NE words,
-// rows (j, k): m^(d-1), v: n_v, group}, box {m NE + XP, m^(d-1), n_v, 1} -- the XP words past
-// each row are out of bounds (zero-filled on load, clipped on store), so the box lands in
-// shared memory with the padded row stride.  16-byte x-rows only.
+// The padded-chunk view of a field whose group is the chunk: d3 {x-row (i, e_l): m NE words,
+// j: m, k: m, v: n_v, group} with box {rs, pr, m, n_v, 1}; d2 {x-row, j, v, group} with box
+// {rs, m, n_v, 1}.  The words past each row (rs > m NE) and the rows past each k-plane
+// (pr > m) are out of bounds -- zero-filled on load, clipped on store -- so the box lands in
+// shared memory with the padded row and plane strides.  16-byte x-rows only.
 template <class R>
 inline bool encode_xpad_map(CUtensorMap* tm, const void* base, int dim, int m, int ne, long long n_groups, int rs,
                             int pr) {

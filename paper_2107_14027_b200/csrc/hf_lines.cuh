@@ -94,7 +94,7 @@ constexpr int xpad_code() {
 template <class R, int DIM, int M, int NE, int LPT = 1, int GS = NE, bool CS = false, int XP = 0>
 struct LinesShape {
     static_assert(NE % GS == 0, "a grouped chunk holds whole groups");
-    static_assert(XP == 0 || (GS == NE && !CS), "padded x-rows: plain chunks only");
+    static_assert(XP == 0 || (GS == NE && !CS), "padded chunks: plain chunks only");
     static constexpr int NV = n_vars_c(DIM);
     static constexpr int NP = ipow_c(M, DIM);
     static constexpr int LINES = NE * ipow_c(M, DIM - 1);
