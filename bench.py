@@ -137,7 +137,8 @@ def load_traffic():
 
 # ------------------------------------------------------------------------------------------------ clocks
 class ClockSampler:
-    """Samples SM clock + throttle reasons through NVML every ~10 ms while running."""
+    """Samples SM clock + throttle reasons through NVML every ~1 ms while running (short timed
+    regions -- config 1 is ~7 ms for both passes -- still get several samples)."""
 
     def __init__(self, device_index: int):
         self.samples = []
@@ -172,7 +173,7 @@ class ClockSampler:
                         self.reasons.add(nm)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.001)
 
     def __enter__(self):
         if self._ok:
@@ -387,6 +388,18 @@ def run_ours(args, R: Ranks):
         torch.cuda.synchronize()
         R.barrier()
     elapsed = R.max(t0.elapsed_time(t1) * 1e-3)
+    # A timed region of a few milliseconds (config 1) fits one or two NVML samples: the same
+    # step is then repeated for ~0.3 s, untimed, with a second sampler -- the clocks the
+    # workload runs at under sustained load, reported beside the in-region ones.
+    clk_sustained = None
+    if len(clk.samples) < 5:
+        with ClockSampler(local_rank) as clk2:
+            t_end = time.perf_counter() + 0.3
+            while time.perf_counter() < t_end:
+                for _ in range(10):
+                    step()
+                torch.cuda.synchronize()
+        clk_sustained = clk2.summary()
     per_case = [0.0] * len(cases)
     for (c_i, reps), (a, b) in zip(blocks, ev):
         per_case[c_i] += a.elapsed_time(b) * 1e-3 / args.steps
@@ -537,6 +550,7 @@ def run_ours(args, R: Ranks):
                       "cases: just before it, each case K times in blocks of 5 back-to-back launches between "
                       "an event pair, the blocks round-robin over the cases",
             "clocks": clk.summary(),
+            **({"clocks_sustained": clk_sustained} if clk_sustained else {}),
         }
         if unfused:
             line["unfused"] = unfused
