@@ -182,6 +182,7 @@ def ref() -> C.CDLL:
         R.ref_field_rel_error.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp]
         R.ref_field_rel_error.restype = C.c_double
         R.ref_gl_derivative.argtypes = [C.c_int, _dp, _dp]
+        R.ref_derivative_matrix.argtypes = [C.c_int, _dp, _dp]
         R.ref_time_oracle_mt.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_double,
                                          C.c_double, C.c_double, _dp, C.c_int, C.c_int]
         R.ref_time_oracle_mt.restype = C.c_double
@@ -484,6 +485,15 @@ def ref_import_blob(path: str):
     out = np.zeros(n)
     ref().ref_import_blob(path.encode(), shape, out.ctypes.data, n)
     return shape[0], shape[1], shape[2], shape[3], bool(shape[4]), out
+
+
+def ref_derivative_matrix(nodes) -> np.ndarray:
+    """The reference's derivative_matrix (operators.hpp:49-74) on the given nodes."""
+    x = np.ascontiguousarray(nodes, dtype=np.float64)
+    D = np.zeros(x.size * x.size)
+    if ref().ref_derivative_matrix(x.size, x, D) != 0:
+        raise ValueError(ref().ref_last_error().decode())
+    return D.reshape(x.size, x.size)
 
 
 def ref_gl_derivative(m: int):

@@ -13,6 +13,8 @@
 //   ref_oracle_divergence  -> hexfuse::oracle_divergence   (oracle.hpp:20-62)
 //   ref_field_rel_error    -> hexfuse::field_rel_error     (verify.hpp:19-33)
 //   ref_gl_derivative      -> gauss_legendre_points + derivative_matrix (operators.hpp:17-74)
+//   ref_derivative_matrix  -> derivative_matrix on caller nodes (operators.hpp:49-74): pins the
+//                             m = 9 operator of d2 p8, whose nodes the reference does not generate
 //   ref_time_oracle_mt     -> oracle_divergence on T group-aligned sub-fields, one
 //                             std::thread each (the function is pure)
 //   ref_export_blob        -> hexfuse::export_blob        (layout.hpp:161-177)
@@ -121,6 +123,13 @@ int ref_gl_derivative(int m, double* nodes, double* D) {
         const auto x = gauss_legendre_points(m);
         const Matrix M = derivative_matrix(x);
         std::copy(x.begin(), x.end(), nodes);
+        std::copy(M.a.begin(), M.a.end(), D);
+    });
+}
+
+int ref_derivative_matrix(int m, const double* nodes, double* D) {
+    return guarded([&] {
+        const Matrix M = derivative_matrix(std::vector<double>(nodes, nodes + m));
         std::copy(M.a.begin(), M.a.end(), D);
     });
 }
