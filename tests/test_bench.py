@@ -39,8 +39,10 @@ def test_workload_config_is_device_free_and_scales():
                                         for d, p, pr, t in bench.workload_cases("config5"))
     assert bench.workload_config("config5", 4, "weak")["points_per_step"] == 4 * c1["points_per_step"]
     assert bench.workload_config("config5", 4, "strong")["points_per_step"] == c1["points_per_step"]
-    # config 5: 1.5e8 points per case, 2,343,750 / 694,444 elements
-    assert bench.case_elements(3, 3, "fp64", 1.5e8) == (2, 2343750)
+    # config 5: 1.5e8 points per case, 2,343,750 / 694,444 elements, rounded to
+    # whole groups of the selected chunk (p3 FP64: 4 elements)
+    g3, n3 = bench.case_elements(3, 3, "fp64", 1.5e8)
+    assert n3 % g3 == 0 and abs(n3 - 2343750) < g3
     assert abs(bench.case_elements(3, 5, "fp64", 1.5e8)[1] - 694445) <= 1
 
 
