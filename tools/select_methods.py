@@ -179,7 +179,9 @@ def main():
 # 3-8 %: these rows take the sustained winner.
 SUSTAINED = {(3, 3, "fp64"): 26, (3, 3, "fp32"): 26, (3, 2, "fp32"): 26, (3, 1, "fp64"): 0,
              (2, 2, "fp64"): 27, (2, 4, "fp64"): 26, (2, 5, "fp64"): 25, (2, 7, "fp64"): 26,
-             (3, 5, "fp32"): 1}
+             (3, 5, "fp32"): 1,
+             # second round-robin pass over the remaining rows (energy_rr2.jsonl): > 1.5 % only here
+             (2, 5, "fp32"): 25, (3, 1, "fp32"): 25}
 OVERRIDES = {(3, 6, "fp32"): 3, (3, 4, "fp64"): 20, (2, 1, "fp32"): 1, (3, 7, "fp32"): 25, **SUSTAINED}
 TIE = 0.0075
 
@@ -272,7 +274,7 @@ def write_table(rows, points, raw="profiles/select_r01_*.jsonl", ncu=None, raw_n
                      f"bank conflicts/wavefront {n['conflict_per_wavefront']}" if n else "")
             why = ""
             if (d, p, prec) in SUSTAINED:
-                why = " [sustained-load winner, profiles/r02/energy/energy_rr.jsonl]"
+                why = " [sustained-load winner, profiles/r02/energy/energy_rr*.jsonl]"
             elif (d, p, prec) in OVERRIDES:
                 why = " [measured override, tools/select_methods.py OVERRIDES]"
             f.write(f"    {{{d}, {p}, {0 if prec == 'fp32' else 1}, {m}, {r['variant']}}},"
