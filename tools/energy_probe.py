@@ -157,7 +157,10 @@ def round_robin(h, cases, a):
         alg = n * npt * 2 * hf.n_vars(d) * u.element_size()
         runs = []
         for v in variants:
-            g = hf.variant_info(hf.make_problem(d, p, 1, 1, prec, PAR), Method.lines, v)["elems_per_cta"]
+            try:
+                g = hf.variant_info(hf.make_problem(d, p, 1, 1, prec, PAR), Method.lines, v)["elems_per_cta"]
+            except (hf.HexfuseInvalid, hf.HexfuseError):
+                continue  # not instantiated (e.g. its shared memory exceeds a CTA)
             pr = hf.make_problem(d, p, n, g, prec, PAR)
             runs.append((v, hf.variant_info(pr, Method.lines, v)["name"],
                          (lambda pr=pr, v=v: hf.fused_divergence_variant(pr, Method.lines, v, u, o)), []))
