@@ -357,7 +357,9 @@ __device__ __forceinline__ void fr_jump_regs(const R (&Uo)[n_vars_c(DIM)], const
 // out(t) -= jac_A (g_L'(x_t) jump_- + g_R'(x_t) jump_+) in place, one axis after the other.
 // `before_update` runs once per thread ahead of its first shared-memory update (the staged
 // correction kernel waits there for its chunk).  Ends with a CTA barrier.
-template <class R, int DIM, int M, int NE, int BS, class Before>
+// SH: the chunk's shared-memory layout (LinesShape; the padded layouts of lines variants 25-27
+// included) -- word offsets of the line points and variables come from it.
+template <class R, int DIM, int M, int NE, int BS, class SH = LinesShape<R, DIM, M, NE>, class Before>
 __device__ __forceinline__ void fr_correct_smem(R* __restrict__ sm, const Params<R>& p, const FrParams<R>& f,
                                                 long long E0, int ne, int tid, Before&& before_update) {
     constexpr int NV = n_vars_c(DIM), LN = fr_lines<DIM, M>(), NP = ipow_c(M, DIM), FW = 2 * DIM * LN * NV;
@@ -409,14 +411,14 @@ __device__ __forceinline__ void fr_correct_smem(R* __restrict__ sm, const Params
                 before_update();
                 waited = true;
             }
-            R* ln = sm + el + NE * fr_line_point<DIM, M>(A, l, 0);
-            constexpr int TS = NE * (A == 0 ? 1 : (A == 1 ? M : M * M));
+            R* ln = sm + SH::word(el, fr_line_point<DIM, M>(A, l, 0), 0);
+            constexpr int TS = SH::template step<A>();
             const R ja = p.jac[A];
 #pragma unroll
             for (int t = 0; t < M; ++t) {
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
-                    R* q = ln + TS * t + NE * NP * v;
+                    R* q = ln + TS * t + SH::VS * v;
                     *q = *q - ja * fma(f.gl[t], jm[v], f.gr[t] * jp[v]);
                 }
             }
@@ -432,15 +434,17 @@ __device__ __forceinline__ void fr_correct_smem(R* __restrict__ sm, const Params
 // sweeps, gets the interface correction in shared memory and leaves it once -- the residual
 // is written once instead of written, read back and rewritten by a second kernel.  The faces
 // (stage 1) come from a projection launched just before (hf_fr_project_kernel).
-template <class R, int DIM, int M, int NE, bool SRC>
-__global__ void __launch_bounds__(LinesShape<R, DIM, M, NE>::BS)
+template <class R, int DIM, int M, int NE, bool SRC, int XP = 0>
+__global__ void __launch_bounds__(LinesShape<R, DIM, M, NE, 1, NE, false, XP>::BS)
     hf_lines_fr_kernel(const __grid_constant__ Params<R> p, const __grid_constant__ FrParams<R> f) {
-    constexpr int BS = LinesShape<R, DIM, M, NE>::BS;
-    lines_chunk<R, DIM, M, NE, SRC, 1, false, NE, false>(p, [&](R* sm, long long E0, int nvalid, int tid) {
+    using SH = LinesShape<R, DIM, M, NE, 1, NE, false, XP>;
+    constexpr int BS = SH::BS;
+    auto hook = [&](R* sm, long long E0, int nvalid, int tid) {
         const long long left = p.n_elem - E0;
         const int ne = int(left < nvalid ? left : nvalid);
-        fr_correct_smem<R, DIM, M, NE, BS>(sm, p, f, E0, ne, tid, [] {});
-    });
+        fr_correct_smem<R, DIM, M, NE, BS, SH>(sm, p, f, E0, ne, tid, [] {});
+    };
+    lines_chunk<R, DIM, M, NE, SRC, 1, false, NE, false, decltype(hook)&, XP>(p, hook);
 }
 
 template <class R, int DIM, int M, int NE>
@@ -606,14 +610,29 @@ constexpr int fr_fused_variant() {
             if (r.variant == 20) return 1;
             if (r.variant == 21) return 2;
             if (r.variant == 22) return 7;
-            if (is_xpad_variant(r.variant)) return xpad_base_variant(r.variant);
+            if (is_xpad_variant(r.variant)) return r.variant;  // the one-pass kernel runs padded too
         }
     return 0;
 }
 
-template <class R, int DIM, int M, int NE, bool SRC>
+template <class R, int DIM, int M, int NE, bool SRC, int XP = 0>
 int lines_fr_launch(Params<R> p, const FrParams<R>& f, cudaStream_t st) {
-    using S = LinesShape<R, DIM, M, NE>;
+    using S = LinesShape<R, DIM, M, NE, 1, NE, false, XP>;
+    if constexpr (XP > 0) {  // padded chunk (launch_lines): the group is the chunk, maps encoded
+        bool ok = p.group == NE && (M * NE * sizeof(R)) % 16 == 0 && S::RS <= 256 && aligned16(p.u) &&
+                  aligned16(p.out);
+        if (ok) {
+            const long long n_groups = (p.n_elem + p.group - 1) / p.group;
+            ok = encode_xpad_map<R>(&p.tm_u, p.u, DIM, M, NE, n_groups, S::RS, S::PR) &&
+                 encode_xpad_map<R>(&p.tm_out, p.out, DIM, M, NE, n_groups, S::RS, S::PR);
+        }
+        if (!ok) return lines_fr_launch<R, DIM, M, NE, SRC, 0>(p, f, st);
+        p.xpad = 1;
+        p.fast_ok = 1;
+        auto kernel = hf_lines_fr_kernel<R, DIM, M, NE, SRC, XP>;
+        if (int e = set_smem_attr(kernel, S::SMEM)) return e;
+        return int(launch_kernel(kernel, dim3(unsigned((p.n_elem + NE - 1) / NE)), dim3(S::BS), S::SMEM, st, p, f));
+    }
     auto kernel = hf_lines_fr_kernel<R, DIM, M, NE, SRC>;
     const bool tile = tile_layout<R, NE>(p.group) && aligned16(p.u) && aligned16(p.out);
     const long long n_groups = (p.n_elem + p.group - 1) / p.group;
@@ -633,23 +652,25 @@ int lines_fr_launch(Params<R> p, const FrParams<R>& f, cudaStream_t st) {
 
 // (d, p, precision) where the one-pass residual (projection, then the lines kernel with the
 // correction in shared memory) beats the pair (lines kernel with the faces, then the
-// correction kernel) by >= 2 % on one box (1e7 points, profiles/r02/ext_r02_fr_fused_ab.jsonl):
-// d3 FP64 p1 / p2 / p6 (1.04-1.14x), d3 FP32 p6 (1.04-1.06x), d2 FP32 p2-p8 (1.03-1.09x),
-// d2 FP64 p2-p4, p6-p8 (1.04-1.13x).  Elsewhere the pair (up to 5 % faster at d3 FP32 p1).
+// correction kernel).  Decided under sustained (power-capped) load with the one-pass kernel
+// on the selected chunk, padded where the selection pads (profiles/r02/fr_sustained/: every
+// stage 0.5 s back to back, HF_FR_FUSED=1 / 0 alternating, two rounds): the one-pass form
+// wins everywhere (1.01-1.22x) but at d3 FP32 p2, where the pair is 4.7 % ahead.
 template <class R, int DIM, int M>
 constexpr bool fr_residual_fused() {
-    constexpr int p = M - 1;
-    if constexpr (DIM == 3) return sizeof(R) == 8 ? (p == 1 || p == 2 || p == 6) : p == 6;
-    else return sizeof(R) == 4 ? p >= 2 : (p >= 2 && p != 5);
+    return !(DIM == 3 && sizeof(R) == 4 && M == 3);
 }
 
 template <class R, int DIM, int M>
 int lines_fr_dispatch(const Params<R>& prm, const FrParams<R>& fp, bool src, cudaStream_t st) {
-    constexpr int NE = variant_ne<R, DIM, M, fr_fused_variant<R, DIM, M>()>();
-    if constexpr (NE < 1 || LinesShape<R, DIM, M, NE>::SMEM > size_t(kMaxSmemPerCta)) {
+    constexpr int V = fr_fused_variant<R, DIM, M>();
+    constexpr int NE = variant_ne<R, DIM, M, V>();
+    constexpr int XP = is_xpad_variant(V) && NE >= 1 ? xpad_code<R, DIM, M, (NE >= 1 ? NE : 1)>() : 0;
+    if constexpr (NE < 1 || LinesShape<R, DIM, M, NE, 1, NE, false, XP>::SMEM > size_t(kMaxSmemPerCta)) {
         return -1;
     } else {
-        return src ? lines_fr_launch<R, DIM, M, NE, true>(prm, fp, st) : lines_fr_launch<R, DIM, M, NE, false>(prm, fp, st);
+        return src ? lines_fr_launch<R, DIM, M, NE, true, XP>(prm, fp, st)
+                   : lines_fr_launch<R, DIM, M, NE, false, XP>(prm, fp, st);
     }
 }
 

@@ -717,7 +717,7 @@ struct NoChunkHook {};
 template <class R, int DIM, int M, int NE, bool SRC, int LPT, bool FACES, int GS, bool CS, class Hook, int XP = 0>
 __device__ __forceinline__ void lines_chunk(const Params<R>& p, Hook&& hook) {
     using S = LinesShape<R, DIM, M, NE, LPT, GS, CS, XP>;
-    static_assert(XP == 0 || (LPT == 1 && std::is_same_v<std::decay_t<Hook>, NoChunkHook>), "padded: plain kernel");
+    static_assert(XP == 0 || LPT == 1, "padded chunks: one line per thread");
     constexpr int BS = S::BS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     using IO = typename S::IO;

@@ -16,6 +16,7 @@ import argparse
 import json
 import os
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -51,7 +52,22 @@ def main():
     ap.add_argument("--points", type=float, default=1e7)
     ap.add_argument("--out", default=None)
     ap.add_argument("--dims", default="3", help="comma list of dimensions (3, 2)")
+    ap.add_argument("--sustained", type=float, default=0.0,
+                    help="time each stage back to back for this many seconds (power-capped regime)")
     a = ap.parse_args()
+    global timed
+    if a.sustained > 0:
+        def timed(fn, iters=0):  # noqa: F811 -- sustained mode
+            for _ in range(5):
+                fn()
+            torch.cuda.synchronize()
+            t0, n = time.perf_counter(), 0
+            while time.perf_counter() - t0 < a.sustained:
+                for _ in range(10):
+                    fn()
+                n += 10
+                torch.cuda.synchronize()
+            return (time.perf_counter() - t0) / n
     fh = open(a.out, "w") if a.out else None
     for d, prec, p in [(d, prec, p) for d in map(int, a.dims.split(",")) for prec in (Precision.fp32, Precision.fp64)
                        for p in range(1, 7 if d == 3 else 9)]:
