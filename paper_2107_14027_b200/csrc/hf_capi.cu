@@ -353,7 +353,10 @@ int lines_variant_for_group(const hf_problem* pr, int variant, const hfb::Params
             if (ne < 1 || ne == G || (ne * w) % 16 != 0 || !available(v)) continue;
             const double fill = double(G) / (double((G + ne - 1) / ne) * ne);
             const int row = ne * w;
-            consider(v, fill * (row >= 64 ? 1.0 : row >= 32 ? 0.9 : 0.53) * occupancy(ne));
+            // 32-byte rows: 0.9 of the roofline in bursts, 0.8 relative to 64-byte rows under sustained
+            // load (profiles/r02/groups_sustained/: p2 FP32 group 40, NE 16 at 5/6 fill 0.86 against
+            // NE 8 full 0.81)
+            consider(v, fill * (row >= 64 ? 1.0 : row >= 32 ? 0.8 : 0.53) * occupancy(ne));
         }
     }
     // the tile ring (variant 24, built at d3 p5): 2 NE0 elements in a two-stage TMA ring, so
