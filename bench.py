@@ -201,6 +201,7 @@ class Ranks:
         self.rank = int(os.environ.get("RANK", "0"))
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.gpu = self.local
         self.dev = None
 
     def init(self, backend: str, device=None):
@@ -310,7 +311,8 @@ def run_ours(args, R: Ranks):
     import paper_2107_14027_b200 as hf
     from paper_2107_14027_b200 import PhysParams, Precision
 
-    rank, world, local_rank = R.rank, R.world, R.local
+    rank, world = R.rank, R.world
+    local_rank = R.gpu  # the rank's GPU (its local rank; 0 for every rank with HF_BENCH_SHARED_GPU)
     dev = torch.device("cuda", local_rank)
     par = PhysParams(1.0 / 1600.0, 2.5, 1.0)
     peak, peak_src = load_peaks()
@@ -746,10 +748,17 @@ def main():
             R.close()
         return
     import torch
-    if R.world > 1 and torch.cuda.device_count() < R.world:
-        raise SystemExit(f"bench.py: {R.world} ranks but {torch.cuda.device_count()} visible GPUs")
-    torch.cuda.set_device(R.local)
-    R.init("nccl", torch.device("cuda", R.local))
+    if os.environ.get("HF_BENCH_SHARED_GPU") == "1":
+        # functional test of the N-rank path on a one-GPU box: every rank on GPU 0, the
+        # bench's scalar reductions over gloo (timings then share the GPU -- not a bench number)
+        R.gpu = 0
+        torch.cuda.set_device(0)
+        R.init("gloo")
+    else:
+        if R.world > 1 and torch.cuda.device_count() < R.world:
+            raise SystemExit(f"bench.py: {R.world} ranks but {torch.cuda.device_count()} visible GPUs")
+        torch.cuda.set_device(R.local)
+        R.init("nccl", torch.device("cuda", R.local))
     try:
         run_ours(args, R)
     finally:

@@ -81,3 +81,21 @@ def test_reference_arm_runs_without_the_b200_library():
     cb = ref["cpu_baseline"]
     assert cb["kind"] == "reference" and cb["cores"] >= 1 and "-march" in cb["build"]
     assert ref["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+def test_two_rank_bench_on_one_gpu():
+    """The N-rank path of bench.py (re-launch under torch.distributed.run, element partition,
+    max-over-ranks timing, sums of points) with real kernels: two ranks sharing the box's GPU
+    (HF_BENCH_SHARED_GPU: reductions over gloo); weak and strong config 5 partition."""
+    env = dict(os.environ, HF_BENCH_SHARED_GPU="1")
+    for extra, scaling in (([], "weak"), (["--workload", "config5", "--scaling", "strong"], "strong")):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
+                            "--warmup", "3", "--no-cpu", "--no-e2e"] + (extra or ["--workload", "config1"]),
+                           capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+        assert r.returncode == 0, r.stderr[-3000:]
+        line = json.loads(r.stdout.strip().splitlines()[-1])
+        assert line["n_gpus"] == 2 and line["scaling"] == scaling and line["value"] > 0
+        assert line["parity"]["ok"]
+        want = bench.workload_config(line["config"]["workload"], 2, scaling)["points_per_step"]
+        assert line["config"]["points_per_step"] == want
