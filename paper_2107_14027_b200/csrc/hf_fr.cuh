@@ -619,15 +619,7 @@ template <class R, int DIM, int M, int NE, bool SRC, int XP = 0>
 int lines_fr_launch(Params<R> p, const FrParams<R>& f, cudaStream_t st) {
     using S = LinesShape<R, DIM, M, NE, 1, NE, false, XP>;
     if constexpr (XP > 0) {  // padded chunk (launch_lines): the group is the chunk, maps encoded
-        bool ok = p.group == NE && (M * NE * sizeof(R)) % 16 == 0 && S::RS <= 256 && aligned16(p.u) &&
-                  aligned16(p.out);
-        if (ok) {
-            const long long n_groups = (p.n_elem + p.group - 1) / p.group;
-            ok = encode_xpad_map<R>(&p.tm_u, p.u, DIM, M, NE, n_groups, S::RS, S::PR) &&
-                 encode_xpad_map<R>(&p.tm_out, p.out, DIM, M, NE, n_groups, S::RS, S::PR);
-        }
-        if (!ok) return lines_fr_launch<R, DIM, M, NE, SRC, 0>(p, f, st);
-        p.xpad = 1;
+        if (!setup_xpad<R, DIM, M, NE, S>(p)) return lines_fr_launch<R, DIM, M, NE, SRC, 0>(p, f, st);
         p.fast_ok = 1;
         auto kernel = hf_lines_fr_kernel<R, DIM, M, NE, SRC, XP>;
         if (int e = set_smem_attr(kernel, S::SMEM)) return e;

@@ -282,6 +282,22 @@ inline bool encode_xpad_map(CUtensorMap* tm, const void* base, int dim, int m, i
     return r == CUDA_SUCCESS;
 }
 
+// Padded-chunk launch set-up (lines variants 25-27, LinesShape XP): the group must be the
+// chunk with 16-byte x-rows no wider than a tensor box and 16-byte aligned buffers; then both
+// tensor maps are encoded and p.xpad set.  false: run the same chunk unpadded.
+template <class R, int DIM, int M, int NE, class SX>
+inline bool setup_xpad(Params<R>& p) {
+    bool ok = p.group == NE && (M * NE * sizeof(R)) % 16 == 0 && SX::RS <= 256 &&
+              (p.u == nullptr || (aligned16(p.u) && aligned16(p.out)));
+    if (ok && p.u != nullptr && p.n_elem > 0) {
+        const long long n_groups = (p.n_elem + p.group - 1) / p.group;
+        ok = encode_xpad_map<R>(&p.tm_u, p.u, DIM, M, NE, n_groups, SX::RS, SX::PR) &&
+             encode_xpad_map<R>(&p.tm_out, p.out, DIM, M, NE, n_groups, SX::RS, SX::PR);
+        p.xpad = ok ? 1 : 0;
+    }
+    return ok;
+}
+
 // Kernel launch with programmatic dependent launch (PDL): consecutive fused launches on
 // a stream overlap one kernel's launch and ramp-up with the previous one's tail; the
 // kernels wait (griddepcontrol.wait) before touching HBM, so stream order is kept.
@@ -353,16 +369,8 @@ cudaError_t launch_lines(Params<R> p, cudaStream_t st, KInfo* info, bool dry) {
         // padded chunks: the group is the chunk, 16-byte x-rows no wider than a tensor box
         // (256 words with the pad), aligned buffers, both tensor maps encoded; else the same
         // chunk unpadded
-        using SX = LinesShape<R, DIM, M, NE, LPT, GS, CS, XP>;
-        bool ok = p.group == NE && (M * NE * sizeof(R)) % 16 == 0 && SX::RS <= 256 &&
-                  (p.u == nullptr || (aligned16(p.u) && aligned16(p.out)));
-        if (ok && !dry && p.n_elem > 0) {
-            const long long n_groups = (p.n_elem + p.group - 1) / p.group;
-            ok = encode_xpad_map<R>(&p.tm_u, p.u, DIM, M, NE, n_groups, SX::RS, SX::PR) &&
-                 encode_xpad_map<R>(&p.tm_out, p.out, DIM, M, NE, n_groups, SX::RS, SX::PR);
-            p.xpad = ok ? 1 : 0;
-        }
-        if (!ok) return launch_lines<R, DIM, M, NE, SRC, LPT, FACES, GS, CS, 0>(p, st, info, dry);
+        if (!setup_xpad<R, DIM, M, NE, LinesShape<R, DIM, M, NE, LPT, GS, CS, XP>>(p))
+            return launch_lines<R, DIM, M, NE, SRC, LPT, FACES, GS, CS, 0>(p, st, info, dry);
     }
     using S = LinesShape<R, DIM, M, NE, LPT, GS, CS, XP>;
     auto kernel = hf_lines_kernel<R, DIM, M, NE, SRC, LPT, FACES, GS, CS, XP>;
