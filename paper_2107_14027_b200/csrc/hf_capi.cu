@@ -996,8 +996,16 @@ int hf_fused_divergence_host_batch(hf_context* c, int n_fields, const hf_problem
     // where it is refused the input is registered read-write.  If registration fails
     // altogether, the copies stage through the driver's pageable path -- slower, same result.)
     std::vector<const void*> reg;
+    // read-only registration only where the device supports it (otherwise the driver refuses it
+    // and the copy falls back to a read-write registration below)
+    int ro_ok = 0;
+    if (cudaDeviceGetAttribute(&ro_ok, cudaDevAttrHostRegisterReadOnlySupported, c->device) != cudaSuccess) {
+        cudaGetLastError();
+        ro_ok = 0;
+    }
     auto pin = [&](const void* p, size_t bytes, unsigned flags) {
         if (is_pinned(p)) return;
+        if (!ro_ok) flags &= ~unsigned(cudaHostRegisterReadOnly);
         if (cudaHostRegister(const_cast<void*>(p), bytes, flags) == cudaSuccess) {
             reg.push_back(p);
             return;
